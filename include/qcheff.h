@@ -1,0 +1,166 @@
+/* qcheff.h — C-ABI of libqcheff, the B200 (sm_100a) implementation of the two
+ * data-parallel hot paths of the effham reference (arXiv 2411.09982):
+ * NPAD Givens-rotation block diagonalisation and Magnus time coarse-graining.
+ *
+ * Conventions (all entry points):
+ *  - Pointers named d_* are DEVICE pointers (caller-owned; never freed here).
+ *    Complex matrices are complex128, row-major, C-contiguous, interleaved
+ *    (re, im) — exactly numpy's complex128 layout.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls that
+ *    return host scalars synchronise that stream; the others are asynchronous.
+ *  - Return value: QCH_OK or one of the QCH_ERR_* codes below, one per
+ *    exception class of the reference (errors.py:4-64).  The message of the
+ *    last failure on the calling thread is available from qch_last_error().
+ *
+ * The reference has no FFI: its boundary is the Python API in
+ * /root/reference/pkg/src/effham.  Each function cites the reference function
+ * it replaces.  INTEGRATION.md shows the ctypes binding.
+ */
+#ifndef QCHEFF_H_
+#define QCHEFF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  QCH_OK = 0,
+  QCH_ERR_VALUE = 1,            /* ValueError (argument validation)        */
+  QCH_ERR_INDEX = 2,            /* errors.IndexOutOfRange                  */
+  QCH_ERR_ZERO_COUPLING = 3,    /* errors.ZeroCoupling                     */
+  QCH_ERR_OVERLAPPING = 4,      /* errors.OverlappingPairs                 */
+  QCH_ERR_UNITARITY_DRIFT = 5,  /* errors.UnitarityDrift                   */
+  QCH_ERR_NONFINITE = 6,        /* errors.NonFinite                        */
+  QCH_ERR_GRID = 7,             /* errors.GridMismatch                     */
+  QCH_ERR_DIMENSION = 8,        /* errors.DimensionMismatch                */
+  QCH_ERR_NORM_DRIFT = 9,       /* errors.NormDrift                        */
+  QCH_ERR_HERMITICITY = 10,     /* errors.HermiticityViolation             */
+  QCH_ERR_UNSUPPORTED = 11,     /* size/shape this build does not handle   */
+  QCH_ERR_CUDA = 12             /* CUDA runtime failure                    */
+};
+
+int qch_version(void);
+/* Copies the last error message of this thread into buf (NUL-terminated);
+ * returns the full message length. */
+size_t qch_last_error(char* buf, size_t len);
+/* Number of device kernels this library has launched in this process
+ * (bench/evidence counter). */
+int64_t qch_launch_count(void);
+
+/* ---------------------------------------------------------------- NPAD --- */
+
+/* HermitianOperator.max_abs (operators.py:92-99): max_ij |H_ij| with numpy's
+ * |z| rounding, written to the device double *d_out. */
+int qch_max_abs_c128(const void* d_h, int64_t n_elems, double* d_out, void* stream);
+
+/* *d_nonherm = 0 iff H[x,y] == conj(H[y,x]) for all x, y (exact compare), else 1.
+ * Selects the mirrored-column fast path of the rotation kernels. */
+int qch_hermitian_exact_c128(const void* d_h, int64_t n, int* d_nonherm, void* stream);
+
+/* givens_rotation_matrix (npad.py:101-123) for n_pairs (i, j) index pairs of
+ * one operator.  d_pairs: int64[2*n_pairs].  d_params: double[8*n_pairs] =
+ * {cos_half, sin_half, phase, degenerate, s_re, s_im, 0, 0} where
+ * s = -sin_half*exp(i*phase) (_block_params, npad.py:126-128).
+ * d_status[k] = QCH_ERR_ZERO_COUPLING when H[j,i] == 0 (npad.py:112-113).
+ * Index checks (npad.py:109-110) are the caller's (host) job. */
+int qch_givens_params_c128(const void* d_h, int64_t n, const int64_t* d_pairs, int64_t n_pairs,
+                           double* d_params, int* d_status, void* stream);
+
+/* unitary_transformation / eliminate_couplings (npad.py:131-145, 235-241,
+ * 274-297): conjugate H in place by n_pairs index-disjoint rotations, in the
+ * reference's sequential order, in one launch.  d_params as produced by
+ * qch_givens_params_c128.  herm_exact selects mirrored column writes (valid
+ * when qch_hermitian_exact_c128 reported 0).  d_u (nullable): accumulated
+ * unitary, rows i, j updated like _apply_left (npad.py:244-251). */
+int qch_npad_apply_rotations_c128(void* d_h, int64_t n, const int64_t* d_pairs, const double* d_params,
+                                  int64_t n_pairs, int herm_exact, void* d_u, void* stream);
+
+/* npad_run (npad.py:320-354) on one device-resident dense operator, entire
+ * greedy loop on the device.  threshold = tol * max_abs(input) (caller).
+ * d_target (int32, nullable) / n_target: subspace mode (npad.py:300-317).
+ * d_u (nullable): track the accumulated unitary; audited for drift every
+ * 100 rotations (npad.py:254-259) -> QCH_ERR_UNITARITY_DRIFT.
+ * d_pivots (nullable): int32[2*pivot_cap] log of the (i, j) picks.
+ * Outputs: *applied, *converged (host). */
+int qch_npad_run_dense_c128(void* d_h, int64_t n, const int32_t* d_target, int64_t n_target,
+                            double threshold, int64_t max_iter, void* d_u, int32_t* d_pivots,
+                            int64_t pivot_cap, int64_t* applied, int* converged, void* stream);
+
+/* Batched npad_run (new API: a parameter sweep of independent operators).
+ * d_h: (batch, n, n) contiguous.  d_thresholds: double[batch].
+ * Outputs on device: d_applied int64[batch], d_converged int32[batch].
+ * Asynchronous.  All operators must be exactly Hermitian (builders are). */
+int qch_npad_run_batch_c128(void* d_h, int64_t batch, int64_t n, const int32_t* d_target,
+                            int64_t n_target, const double* d_thresholds, int64_t max_iter,
+                            int64_t* d_applied, int32_t* d_converged, void* stream);
+
+/* Device-side builder of the transmon (x) resonator Hamiltonians of the NPAD
+ * configs: for each b, params[4b..4b+3] =
+ * {omega_q, alpha, omega_r, g}; H = wq n + a/2 n(n-1) (x) I + I (x) wr a^dag a
+ * + g (b + b^dag) (x) (a + a^dag), index q*n_r + k.  d_h: (batch, nq*nr)^2. */
+int qch_build_transmon_resonator_c128(void* d_h, int64_t batch, int64_t n_q, int64_t n_r,
+                                      const double* d_params, void* stream);
+
+/* -------------------------------------------------------------- Magnus --- */
+
+/* magnus_coefficients (magnus.py:151-169) and, for order 2, the second-order
+ * coefficients alpha (M,K) and beta (M, K(K-1)/2) of SURVEY.md Appendix B.
+ * d_sig: (K, S) float64.  d_c1: (M, K).  d_c2 (order 2, else nullable):
+ * (M, K + K(K-1)/2) = [alpha_0..alpha_{K-1}, beta_01, beta_02, ..].
+ * dt = grid spacing.  Returns QCH_ERR_GRID for M < 1 or M not dividing S-1. */
+int qch_magnus_coefficients(const double* d_sig, int64_t K, int64_t S, int64_t M, double dt, int order,
+                            double* d_c1, double* d_c2, void* stream);
+
+/* Basis commutators [A,B] = AB - (AB)^dag of Hermitian operands: d_out gets
+ * [H0,H_k] for k < K then [H_k,H_l] for k < l, each (N,N). */
+int qch_magnus_commutators_c128(const void* d_h0, const void* d_hk, int64_t K, int64_t N, void* d_out,
+                                void* stream);
+
+/* assemble_effective_hams (magnus.py:172-190), intervals [m0, m0+mb):
+ * Hbar_n = dt_int*H0 + sum_k c1[n,k] H_k  (+ (-i/2) X_n for order 2). */
+int qch_magnus_assemble_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                             const double* d_c1, const double* d_c2, int64_t m0, int64_t mb, double dt_int,
+                             int order, void* d_hbar, void* stream);
+
+/* _expm_minus_i (expm.py:56-71) for a batch: U_b = exp(-i H_b), scaling and
+ * squaring Taylor order 18.  d_work: scratch of 3*batch*n*n complex128.
+ * Checks finiteness (expm.py:81-82, 97-99): QCH_ERR_NONFINITE, first bad
+ * item index in *bad_index (host, nullable). */
+int qch_expm_minus_i_batch_c128(const void* d_h, int64_t batch, int64_t n, void* d_u, void* d_work,
+                                int64_t* bad_index, void* stream);
+
+/* UnitaryPropagator.validate (expm.py:40-47) for a batch: returns
+ * QCH_ERR_NONFINITE (and *bad_index) for the first propagator with
+ * ||UU^dag - I||_F > 1e-10*n or ||det U| - 1| > 1e-8. */
+int qch_validate_unitary_batch_c128(const void* d_u, int64_t batch, int64_t n, int64_t* bad_index,
+                                    void* stream);
+
+/* evolve (magnus.py:214-267), whole pipeline on the device: coefficients,
+ * assembly (order 1|2), propagators, ordered product and trajectory.
+ * d_h0 (N,N), d_hk (K,N,N), d_sig (K,S), d_psi0 (N).  d_traj: (M+1, N).
+ * d_props (nullable): (M, N, N) propagators.  check: validate propagators.
+ * NormDrift (magnus.py:270-273) -> QCH_ERR_NORM_DRIFT with the interval in
+ * *bad_index. */
+int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, int64_t K, int64_t N, const double* d_sig,
+                           int64_t S, double t_start, double t_end, int64_t M, int order, const void* d_psi0,
+                           void* d_traj, void* d_props, int check, int64_t* bad_index, void* stream);
+
+/* ||U_b U_b^dag - I||_F for a batch (DMMA GEMM with a fused reduction):
+ * the unitarity audit of npad.py:257 and expm.py:35-38.  d_defect: (batch). */
+int qch_unitarity_defect_c128(const void* d_u, int64_t batch, int64_t n, double* d_defect, void* stream);
+
+/* ------------------------------------------------------------ GEMM ------- */
+
+/* Batched complex128 GEMM on the FP64 tensor pipe (DMMA, mma.sync f64):
+ * C_b = A_b @ B_b, (m,k) x (k,n), batch strides in elements; C must not
+ * alias A or B. */
+int qch_zgemm_batched(const void* d_a, const void* d_b, void* d_c, int64_t m, int64_t n, int64_t k,
+                      int64_t batch, int64_t stride_a, int64_t stride_b, int64_t stride_c, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QCHEFF_H_ */

@@ -1,0 +1,157 @@
+"""Generate tests/golden/*.npz by running THE REFERENCE ITSELF.
+
+Run in the build container (the reference does not exist on the GPU box):
+    python oracle/gen_golden.py [--ref /root/reference/pkg/src]
+
+The reference package is imported read-only from its source tree; the pivot
+sequence is captured by wrapping effham.npad.eliminate_coupling in this
+harness (npad_run resolves the name at call time, npad.py:354).  Inputs come
+from the product's host-side builders (plain numpy), so tests can rebuild
+them bit-identically.  Outputs are small (a few MB total).
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLD = ROOT / "tests" / "golden"
+
+
+def _import_reference(path: str):
+    os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, path)
+    import effham  # noqa: F401
+
+    return sys.modules["effham"]
+
+
+def _logged_run(effham, op, target=None, **kw):
+    log = []
+    orig = effham.npad.eliminate_coupling
+
+    def wrapped(state, i, j):
+        log.append((i, j))
+        return orig(state, i, j)
+
+    effham.npad.eliminate_coupling = wrapped
+    try:
+        st = effham.npad.npad_run(op, target, **kw)
+    finally:
+        effham.npad.eliminate_coupling = orig
+    return st, np.asarray(log, dtype=np.int64).reshape(-1, 2)
+
+
+def random_hermitian(n: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    return (a + a.conj().T) / 2.0
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--ref", default="/root/reference/pkg/src")
+    args = ap.parse_args()
+    eff = _import_reference(args.ref)
+    sys.path.insert(0, str(ROOT))
+    from paper_2411_09982_b200 import models as M  # host builders only (numpy)
+
+    GOLD.mkdir(parents=True, exist_ok=True)
+
+    # 1. NPAD config 1: transmon 3 x resonator 20, full mode, tol 1e-12
+    h = M.transmon_resonator_hamiltonian(3, 20).data
+    st, piv = _logged_run(eff, eff.HermitianOperator(h), tol=1e-12)
+    np.savez_compressed(GOLD / "npad_tr3x20_full.npz", h=h, pivots=piv, final=st.current.data,
+                        applied=st.applied, converged=st.converged, tol=1e-12)
+    print("tr3x20", st.applied, st.converged)
+
+    # 2. random complex Hermitian, full mode, with unitary tracking
+    h = random_hermitian(24, 7)
+    st, piv = _logged_run(eff, eff.HermitianOperator(h), tol=1e-12, track_unitary=True)
+    np.savez_compressed(GOLD / "npad_rand24_full_u.npz", h=h, pivots=piv, final=st.current.data,
+                        applied=st.applied, converged=st.converged, u=st.accumulated_unitary, tol=1e-12)
+    print("rand24", st.applied, st.converged)
+
+    # 3. subspace mode on 4 x 30
+    h = M.transmon_resonator_hamiltonian(4, 30, omega_q=6.2, g=0.15).data
+    tgt = M.sweep_target(30)
+    st, piv = _logged_run(eff, eff.HermitianOperator(h), tgt, tol=1e-12)
+    np.savez_compressed(GOLD / "npad_tr4x30_sub.npz", h=h, pivots=piv, final=st.current.data, target=np.array(tgt),
+                        applied=st.applied, converged=st.converged, tol=1e-12)
+    print("tr4x30 sub", st.applied, st.converged)
+
+    # 4. max_iter truncation on 4 x 60 (dim 240)
+    h = M.transmon_resonator_hamiltonian(4, 60).data
+    st, piv = _logged_run(eff, eff.HermitianOperator(h), tol=1e-12, max_iter=150)
+    np.savez_compressed(GOLD / "npad_tr4x60_k150.npz", h=h, pivots=piv, final=st.current.data,
+                        applied=st.applied, converged=st.converged, tol=1e-12, max_iter=150)
+    print("tr4x60 k150", st.applied, st.converged)
+
+    # 5. eliminate_couplings on the JC site (Mott pairs), dense input
+    p = eff.JCSiteParams(omega=1.0, qubit_freq=0.8, g=0.1, mu=0.3, n_max=8)
+    hjc = eff.jc_onsite_hamiltonian(p).to_dense()
+    pairs = [(2 * m - 1, 2 * m) for m in range(1, 6)]
+    st = eff.eliminate_couplings(eff.NPADState.from_operator(eff.HermitianOperator(hjc), track_unitary=True), pairs)
+    np.savez_compressed(GOLD / "npad_jc_pairs.npz", h=hjc, pairs=np.array(pairs), final=st.current.data,
+                        u=st.accumulated_unitary, applied=st.applied)
+
+    # 6. AC1: 1000 random 2-level rotations (givens scalars)
+    rng = np.random.default_rng(11)
+    eps = rng.uniform(-2, 2, 1000)
+    dl = rng.uniform(-1, 1, 1000)
+    dl[:20] = 0.0  # degenerate cases
+    g = rng.uniform(1e-3, 1, 1000)
+    phi = rng.uniform(-np.pi, np.pi, 1000)
+    mats = np.empty((1000, 2, 2), dtype=np.complex128)
+    rows = np.empty((1000, 4))
+    after = np.empty((1000, 2, 2), dtype=np.complex128)
+    for k in range(1000):
+        m2 = np.array([[eps[k] + dl[k], g[k] * np.exp(-1j * phi[k])], [g[k] * np.exp(1j * phi[k]), eps[k] - dl[k]]])
+        mats[k] = m2
+        op = eff.HermitianOperator(m2)
+        rot = eff.givens_rotation_matrix(op, 0, 1)
+        rows[k] = (rot.cos_half, rot.sin_half, rot.phase, float(rot.degenerate))
+        after[k] = eff.unitary_transformation(op, rot).data
+    np.savez_compressed(GOLD / "givens_2x2.npz", mats=mats, params=rows, after=after)
+
+    # 7. expm on random Hermitian matrices of several sizes
+    hs = {f"h{n}": random_hermitian(n, 100 + n) * s for n, s in [(3, 0.1), (3, 3.0), (8, 0.7), (40, 0.05), (64, 2.0)]}
+    us = {k.replace("h", "u"): eff.expm_unitary(v).entries for k, v in hs.items()}
+    np.savez_compressed(GOLD / "expm.npz", **hs, **us)
+
+    # 8. Magnus order 1: driven transmon (config-2 family), M = 2000, sub = 4
+    ch, grid = M.driven_transmon(3, intervals=2000, sub=4)
+    d0 = ch.drift.data
+    ctr = np.stack([c.data for c in ch.controls])
+    ref_ch = eff.ControlledHamiltonian(eff.HermitianOperator(d0), [eff.HermitianOperator(c) for c in ctr])
+    ref_grid = eff.ControlGrid(grid.t_start, grid.t_end, grid.signals)
+    psi0 = np.zeros(3, dtype=np.complex128)
+    psi0[0] = 1
+    iv = eff.magnus_intervals(ref_ch, ref_grid, 2000)
+    traj, props = eff.evolve(ref_ch, ref_grid, 2000, psi0, return_propagators=True, check=True)
+    np.savez_compressed(GOLD / "magnus_transmon_m2000.npz", drift=d0, controls=ctr, signals=grid.signals,
+                        t=np.array([grid.t_start, grid.t_end]), m=2000, psi0=psi0, coeffs=iv.coefficients,
+                        hbar_head=np.stack([iv.effective_hams[k].data for k in range(16)]),
+                        u_head=np.stack([props[k].entries for k in range(16)]), traj=traj.amplitudes)
+
+    # 9. Magnus order 1 on the reference spin chain (L = 6, M = 20, sub = 8)
+    pc = eff.SpinChainParams(length=6, qubit_freq=1.0, j_nn=0.25, g_nnn=0.05)
+    ch6 = eff.spin_chain_hamiltonians(pc)
+    grid6 = eff.synthetic_transfer_pulse(25.0, 20 * 8 + 1, seed=3)
+    psi6 = np.zeros(64, dtype=np.complex128)
+    psi6[0] = 1
+    traj6 = eff.evolve(ch6, grid6, 20, psi6, check=True)
+    np.savez_compressed(GOLD / "magnus_spin6_m20.npz", drift=ch6.drift.to_dense(),
+                        controls=np.stack([c.to_dense() for c in ch6.controls]), signals=grid6.signals,
+                        t=np.array([grid6.t_start, grid6.t_end]), m=20, psi0=psi6, traj=traj6.amplitudes,
+                        coeffs=eff.magnus_coefficients(grid6, 20))
+    print("wrote", sorted(p.name for p in GOLD.glob("*.npz")))
+
+
+if __name__ == "__main__":
+    main()

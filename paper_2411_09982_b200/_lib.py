@@ -1,0 +1,182 @@
+"""ctypes binding of libqcheff.so (include/qcheff.h) and device plumbing.
+
+PyTorch is used only for device memory and the current CUDA stream; every
+numerical operation of the hot paths runs in the hand-written kernels of the
+library.  There is deliberately no CPU fallback: on a machine without a CUDA
+device, or without the built library, every hot-path call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from . import errors
+
+_HERE = Path(__file__).resolve().parent
+_LIB_PATH = _HERE / "libqcheff.so"
+_lock = threading.Lock()
+_lib = None
+
+c_void_p = ctypes.c_void_p
+c_int64 = ctypes.c_int64
+c_int = ctypes.c_int
+c_double = ctypes.c_double
+P_int64 = ctypes.POINTER(ctypes.c_int64)
+P_int = ctypes.POINTER(ctypes.c_int)
+
+# name -> (restype, argtypes); mirrors include/qcheff.h
+PROTOTYPES = {
+    "qch_version": (c_int, []),
+    "qch_last_error": (ctypes.c_size_t, [ctypes.c_char_p, ctypes.c_size_t]),
+    "qch_launch_count": (c_int64, []),
+    "qch_max_abs_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "qch_hermitian_exact_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "qch_givens_params_c128": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "qch_npad_apply_rotations_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
+    "qch_npad_run_dense_c128": (
+        c_int,
+        [c_void_p, c_int64, c_void_p, c_int64, c_double, c_int64, c_void_p, c_void_p, c_int64, P_int64, P_int, c_void_p],
+    ),
+    "qch_npad_run_batch_c128": (
+        c_int,
+        [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p],
+    ),
+    "qch_build_transmon_resonator_c128": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "qch_magnus_coefficients": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_double, c_int, c_void_p, c_void_p, c_void_p]),
+    "qch_magnus_commutators_c128": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "qch_magnus_assemble_c128": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_double, c_int, c_void_p, c_void_p],
+    ),
+    "qch_expm_minus_i_batch_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, P_int64, c_void_p]),
+    "qch_validate_unitary_batch_c128": (c_int, [c_void_p, c_int64, c_int64, P_int64, c_void_p]),
+    "qch_unitarity_defect_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "qch_magnus_evolve_c128": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int, c_void_p,
+         c_void_p, c_void_p, c_int, P_int64, c_void_p],
+    ),
+    "qch_zgemm_batched": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p],
+    ),
+}
+
+QCH_OK = 0
+STATUS_TO_ERROR = {
+    1: ValueError,
+    2: errors.IndexOutOfRange,
+    3: errors.ZeroCoupling,
+    4: errors.OverlappingPairs,
+    5: errors.UnitarityDrift,
+    6: errors.NonFinite,
+    7: errors.GridMismatch,
+    8: errors.DimensionMismatch,
+    9: errors.NormDrift,
+    10: errors.HermiticityViolation,
+    11: NotImplementedError,
+    12: RuntimeError,
+}
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def load(build_if_missing: bool = True):
+    """Load (building in-tree first if needed) and type the shared library."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if build_if_missing and os.environ.get("QCH_AUTOBUILD", "1") == "1":
+            from . import _build
+
+            if _build.stale():
+                _build.build()
+        if not _LIB_PATH.exists():
+            raise RuntimeError(f"{_LIB_PATH} is missing; run __graft_entry__.build()")
+        lib = ctypes.CDLL(str(_LIB_PATH))
+        for name, (res, args) in PROTOTYPES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    lib = load()
+    buf = ctypes.create_string_buffer(1024)
+    lib.qch_last_error(buf, len(buf))
+    return buf.value.decode(errors="replace")
+
+
+def check(status: int) -> None:
+    if status == QCH_OK:
+        return
+    exc = STATUS_TO_ERROR.get(status, RuntimeError)
+    raise exc(last_error())
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args))
+
+
+def launch_count() -> int:
+    return int(load().qch_launch_count())
+
+
+# -- device plumbing (torch owns memory and streams) ---------------------------
+
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError(
+            "paper_2411_09982_b200 needs a CUDA device: the hot paths run only in libqcheff's sm_100a kernels "
+            "(there is no CPU fallback)"
+        )
+    load()
+    return t
+
+
+def stream_ptr():
+    t = torch()
+    return c_void_p(t.cuda.current_stream().cuda_stream)
+
+
+def dptr(tensor) -> c_void_p:
+    if tensor is None:
+        return c_void_p(None)
+    return c_void_p(tensor.data_ptr())
+
+
+def to_device(array, dtype=None):
+    """Host array -> contiguous CUDA tensor (complex128 / float64 / int)."""
+    t = require_cuda()
+    if isinstance(array, t.Tensor):
+        out = array
+        if not out.is_cuda:
+            out = out.cuda()
+        if dtype is not None and out.dtype != dtype:
+            out = out.to(dtype)
+        return out.contiguous()
+    arr = np.ascontiguousarray(array)
+    out = t.from_numpy(arr)
+    if dtype is not None:
+        out = out.to(dtype)
+    return out.cuda(non_blocking=False).contiguous()
+
+
+def to_host(tensor) -> np.ndarray:
+    return tensor.detach().cpu().numpy()

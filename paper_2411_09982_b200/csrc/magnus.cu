@@ -1,0 +1,998 @@
+// magnus.cu — Magnus time coarse-graining on sm_100a.
+//
+// Reference: /root/reference/pkg/src/effham/magnus.py (+ expm.py).  evolve()
+// (magnus.py:214-267) = coefficients (trapezoid, :151-169) -> per-interval
+// effective Hamiltonians (:172-190) -> propagators exp(-i Hbar_n) by
+// scaling-and-squaring Taylor order 18 (expm.py:56-71) -> sequential product
+// psi_{n+1} = U_n psi_n (:249-252).  The second-order term (absent from the
+// reference) adds -(i/2) X_n with
+//   X_n = sum_k alpha_nk [H0,H_k] + sum_{k<l} beta_nkl [H_k,H_l].
+//
+// Two device pipelines:
+//  * N <= 4 (the dim-3 driven transmon): ONE thread per interval does
+//    coefficients + assembly + Taylor expm entirely in registers; the ordered
+//    product is a parallel prefix (block Hillis-Steele over 3x3 products, a
+//    scan of block aggregates, then psi_{n+1} = Q_n E_b psi_0).
+//  * N > 4: batched interval chunks: assembly kernel, Taylor via the DMMA
+//    complex GEMM with the fused "term = term@a/k; out += term" epilogue
+//    (zgemm.cu), squaring, then the sequential ordered product.
+#include <algorithm>
+#include <vector>
+
+#include "qch_internal.h"
+#include "qch_math.cuh"
+
+namespace qch {
+
+int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, int64_t batch, int64_t sa, int64_t sb,
+          int64_t sc, cudaStream_t st);
+int zgemm_taylor(const double2* a, const double2* b, double2* t, double2* o, int n, int64_t batch, double inv_k,
+                 cudaStream_t st);
+int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st);
+
+constexpr int kTaylorOrder = 18;     // expm.py:19
+constexpr double kScaleTarget = 0.5;  // expm.py:20
+
+// ----------------------------------------------------------------------------
+// Coefficients.  First order: magnus.py:164-168 (numpy pairwise sum of
+// (left+right) then * dt/2).  Second order: SURVEY.md Appendix B.
+struct CoefArgs {
+  const double* sig;  // (K, S)
+  int K;
+  int64_t S;
+  int64_t M;
+  int sub;
+  double dt;
+};
+
+__device__ __forceinline__ void interval_coeffs(const CoefArgs& a, int64_t n, int order, double* c1, double* c2) {
+  const int K = a.K, sub = a.sub;
+  const double h = a.dt;
+  for (int k = 0; k < K; ++k) {
+    const double* u = a.sig + (int64_t)k * a.S + n * sub;
+    auto f = [&](int q) { return QADD(u[q], u[q + 1]); };
+    c1[k] = QMUL(QDIV(h, 2.0), np_pairwise(f, sub));
+  }
+  if (order < 2) return;
+  const double hh6 = QDIV(QMUL(h, h), 6.0);
+  const double h2 = QDIV(h, 2.0);
+  // alpha_k = sum_a [h*S_k(a) - a*h*tau_ak] - (h^2/6) sum_a (u_{a+1} - u_a)
+  for (int k = 0; k < K; ++k) {
+    const double* u = a.sig + (int64_t)k * a.S + n * sub;
+    double run = 0.0, acc = 0.0, lin = 0.0;
+    for (int q = 0; q < sub; ++q) {
+      double tau = QMUL(h2, QADD(u[q], u[q + 1]));
+      acc = QADD(acc, QSUB(QMUL(h, run), QMUL(QMUL((double)q, h), tau)));
+      lin = QADD(lin, QSUB(u[q + 1], u[q]));
+      run = QADD(run, tau);
+    }
+    c2[k] = QSUB(acc, QMUL(hh6, lin));
+  }
+  // beta_kl = sum_a [tau_ak S_l(a) - tau_al S_k(a)] - (h^2/6) sum_a (u_k,a u_l,a+1 - u_l,a u_k,a+1)
+  int idx = K;
+  for (int k = 0; k < K; ++k)
+    for (int l = k + 1; l < K; ++l) {
+      const double* uk = a.sig + (int64_t)k * a.S + n * sub;
+      const double* ul = a.sig + (int64_t)l * a.S + n * sub;
+      double sk = 0.0, sl = 0.0, acc = 0.0, cr = 0.0;
+      for (int q = 0; q < sub; ++q) {
+        double tk = QMUL(h2, QADD(uk[q], uk[q + 1]));
+        double tl = QMUL(h2, QADD(ul[q], ul[q + 1]));
+        acc = QADD(acc, QSUB(QMUL(tk, sl), QMUL(tl, sk)));
+        cr = QADD(cr, QSUB(QMUL(uk[q], ul[q + 1]), QMUL(ul[q], uk[q + 1])));
+        sk = QADD(sk, tk);
+        sl = QADD(sl, tl);
+      }
+      c2[idx++] = QSUB(acc, QMUL(hh6, cr));
+    }
+}
+
+constexpr int kMaxK = 8;
+
+__global__ void coeff_kernel(CoefArgs a, int order, double* __restrict__ c1, double* __restrict__ c2) {
+  int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n >= a.M) return;
+  double l1[kMaxK], l2[kMaxK + kMaxK * (kMaxK - 1) / 2];
+  interval_coeffs(a, n, order, l1, l2);
+  for (int k = 0; k < a.K; ++k) c1[n * a.K + k] = l1[k];
+  if (order >= 2) {
+    int nc = a.K + a.K * (a.K - 1) / 2;
+    for (int k = 0; k < nc; ++k) c2[n * nc + k] = l2[k];
+  }
+}
+
+// ----------------------------------------------------------------------------
+// small dense matrices in registers
+template <int N>
+struct Mat {
+  cplx v[N][N];
+};
+template <int N>
+__device__ __forceinline__ Mat<N> mat_eye() {
+  Mat<N> m;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) m.v[r][c] = mkc(r == c ? 1.0 : 0.0, 0.0);
+  return m;
+}
+template <int N>
+__device__ __forceinline__ Mat<N> mat_mul(const Mat<N>& a, const Mat<N>& b) {
+  Mat<N> o;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      cplx acc = np_cmul(a.v[r][0], b.v[0][c]);
+#pragma unroll
+      for (int k = 1; k < N; ++k) acc = cadd(acc, np_cmul(a.v[r][k], b.v[k][c]));
+      o.v[r][c] = acc;
+    }
+  return o;
+}
+template <int N>
+__device__ __forceinline__ cplx mat_det(const Mat<N>& m);
+template <>
+__device__ __forceinline__ cplx mat_det<1>(const Mat<1>& m) {
+  return m.v[0][0];
+}
+template <>
+__device__ __forceinline__ cplx mat_det<2>(const Mat<2>& m) {
+  return csub(np_cmul(m.v[0][0], m.v[1][1]), np_cmul(m.v[0][1], m.v[1][0]));
+}
+template <>
+__device__ __forceinline__ cplx mat_det<3>(const Mat<3>& m) {
+  cplx a = np_cmul(m.v[0][0], csub(np_cmul(m.v[1][1], m.v[2][2]), np_cmul(m.v[1][2], m.v[2][1])));
+  cplx b = np_cmul(m.v[0][1], csub(np_cmul(m.v[1][0], m.v[2][2]), np_cmul(m.v[1][2], m.v[2][0])));
+  cplx c = np_cmul(m.v[0][2], csub(np_cmul(m.v[1][0], m.v[2][1]), np_cmul(m.v[1][1], m.v[2][0])));
+  return cadd(csub(a, b), c);
+}
+template <>
+__device__ __forceinline__ cplx mat_det<4>(const Mat<4>& m) {
+  cplx acc = mkc(0, 0);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    Mat<3> s;
+#pragma unroll
+    for (int r = 1; r < 4; ++r) {
+      int cc = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q != c) s.v[r - 1][cc++] = m.v[r][q];
+    }
+    cplx t = np_cmul(m.v[0][c], mat_det<3>(s));
+    acc = (c & 1) ? csub(acc, t) : cadd(acc, t);
+  }
+  return acc;
+}
+
+// _expm_minus_i (expm.py:56-71) on one register matrix (hbar -> U)
+template <int N>
+__device__ __forceinline__ Mat<N> expm_minus_i_reg(const Mat<N>& hb) {
+  Mat<N> a;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) a.v[r][c] = mkc(hb.v[r][c].im, -hb.v[r][c].re);  // -1j * H, exact
+  double norm = 0.0;
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    double rs = 0.0;  // numpy sequential sum for n < 8
+#pragma unroll
+    for (int c = 0; c < N; ++c) rs = QADD(rs, np_cabs(a.v[r][c]));
+    norm = fmax(norm, rs);
+  }
+  int s = 0;
+  if (norm > kScaleTarget) {
+    s = (int)ceil(log2(QDIV(norm, kScaleTarget)));
+    double scl = ldexp(1.0, -s);  // a / 2**s == a * 2**-s exactly
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) a.v[r][c] = mkc(QMUL(a.v[r][c].re, scl), QMUL(a.v[r][c].im, scl));
+  }
+  Mat<N> out = mat_eye<N>(), term = mat_eye<N>();
+  for (int k = 1; k <= kTaylorOrder; ++k) {
+    term = mat_mul<N>(term, a);
+    double inv = QDIV(1.0, (double)k);
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        term.v[r][c] = mkc(QMUL(term.v[r][c].re, inv), QMUL(term.v[r][c].im, inv));
+        out.v[r][c] = cadd(out.v[r][c], term.v[r][c]);
+      }
+  }
+  for (int q = 0; q < s; ++q) out = mat_mul<N>(out, out);
+  return out;
+}
+
+// UnitaryPropagator.validate (expm.py:40-47)
+template <int N>
+__device__ __forceinline__ bool validate_reg(const Mat<N>& u) {
+  double d2 = 0.0;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      cplx acc = mkc(0, 0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) acc = cadd(acc, np_cmul(u.v[r][k], cconj(u.v[c][k])));
+      double re = acc.re - (r == c ? 1.0 : 0.0);
+      d2 += re * re + acc.im * acc.im;
+    }
+  double defect = sqrt(d2);
+  if (!(defect <= 1e-10 * N)) return false;
+  cplx d = mat_det<N>(u);
+  double ad = hypot_cr(d.re, d.im);
+  return fabs(ad - 1.0) <= 1e-8;
+}
+
+struct SmallArgs {
+  CoefArgs ca;
+  const double2* h0;    // (N,N)
+  const double2* hk;    // (K,N,N)
+  const double2* comm;  // (K + K(K-1)/2, N, N) (order 2)
+  int order;
+  double dt_int;
+  int check;
+  double2* props;   // (M,N,N) or nullptr
+  double2* qloc;    // (M,N,N) block-local prefixes
+  double2* agg;     // (nblocks, N, N)
+  unsigned long long* bad;  // [0] first non-unitary interval
+};
+
+template <int N>
+__device__ __forceinline__ void ld_mat(Mat<N>& m, const double2* p) {
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) m.v[r][c] = d2c(p[r * N + c]);
+}
+template <int N>
+__device__ __forceinline__ void st_mat(double2* p, const Mat<N>& m) {
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) p[r * N + c] = c2d(m.v[r][c]);
+}
+
+constexpr int kScanThreads = 256;
+
+// Hillis-Steele inclusive scan of matrix products in thread order, later
+// intervals multiplied on the LEFT: P_t = U_t ... U_0.
+template <int N>
+__device__ Mat<N> block_scan(Mat<N> p, double2* sm) {
+  const int t = threadIdx.x;
+  for (int d = 1; d < blockDim.x; d <<= 1) {
+    st_mat<N>(sm + t * N * N, p);
+    __syncthreads();
+    if (t >= d) {
+      Mat<N> q;
+      ld_mat<N>(q, sm + (t - d) * N * N);
+      p = mat_mul<N>(p, q);
+    }
+    __syncthreads();
+  }
+  return p;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kScanThreads) magnus_small_k1(SmallArgs g) {
+  extern __shared__ __align__(16) double2 ssm[];
+  const int K = g.ca.K;
+  const int ncomm = K + K * (K - 1) / 2;
+  double2* s_ops = ssm;                                // H0, Hk..., comm...
+  double2* s_scan = ssm + (1 + K + ncomm) * N * N;     // kScanThreads * N*N
+  for (int q = threadIdx.x; q < N * N; q += blockDim.x) s_ops[q] = g.h0[q];
+  for (int q = threadIdx.x; q < K * N * N; q += blockDim.x) s_ops[N * N + q] = g.hk[q];
+  if (g.order >= 2)
+    for (int q = threadIdx.x; q < ncomm * N * N; q += blockDim.x) s_ops[(1 + K) * N * N + q] = g.comm[q];
+  __syncthreads();
+
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  Mat<N> u = mat_eye<N>();
+  if (n < g.ca.M) {
+    double c1[kMaxK], c2[kMaxK + kMaxK * (kMaxK - 1) / 2];
+    interval_coeffs(g.ca, n, g.order, c1, c2);
+    Mat<N> hb;
+    // h = dt*drift; h = h + w*ctrl  (magnus.py:186-188)
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) hb.v[r][c] = np_rmul(g.dt_int, d2c(s_ops[r * N + c]));
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c)
+          hb.v[r][c] = cadd(hb.v[r][c], np_rmul(c1[k], d2c(s_ops[(1 + k) * N * N + r * N + c])));
+    if (g.order >= 2) {
+      Mat<N> x;
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c) x.v[r][c] = mkc(0, 0);
+      for (int q = 0; q < ncomm; ++q)
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int c = 0; c < N; ++c)
+            x.v[r][c] = cadd(x.v[r][c], np_rmul(c2[q], d2c(s_ops[(1 + K + q) * N * N + r * N + c])));
+      // hbar = hbar1 + (-0.5j) * X
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c) hb.v[r][c] = cadd(hb.v[r][c], np_cmul(mkc(0.0, -0.5), x.v[r][c]));
+    }
+    u = expm_minus_i_reg<N>(hb);
+    if (g.check && !validate_reg<N>(u)) atomicMin(g.bad, (unsigned long long)n);
+    if (g.props) st_mat<N>(g.props + n * N * N, u);
+  }
+  Mat<N> p = block_scan<N>(u, s_scan);
+  if (n < g.ca.M) st_mat<N>(g.qloc + n * N * N, p);
+  if (threadIdx.x == blockDim.x - 1) st_mat<N>(g.agg + (int64_t)blockIdx.x * N * N, p);
+}
+
+// exclusive scan of block aggregates: E_0 = I, E_b = A_{b-1} ... A_0 (in place)
+template <int N>
+__global__ void __launch_bounds__(1024) scan_aggregates_kernel(double2* agg, int64_t nb) {
+  extern __shared__ __align__(16) double2 ssm[];
+  Mat<N> carry = mat_eye<N>();
+  for (int64_t base = 0; base < nb; base += blockDim.x) {
+    int64_t b = base + threadIdx.x;
+    Mat<N> a = mat_eye<N>();
+    if (b < nb) ld_mat<N>(a, agg + b * N * N);
+    Mat<N> p = block_scan<N>(a, ssm);
+    // exclusive: E_b = P_{b-1} * carry ; E_base = carry
+    st_mat<N>(ssm + threadIdx.x * N * N, p);
+    __syncthreads();
+    Mat<N> e = carry;
+    if (threadIdx.x > 0) {
+      Mat<N> q;
+      ld_mat<N>(q, ssm + (threadIdx.x - 1) * N * N);
+      e = mat_mul<N>(q, carry);
+    }
+    Mat<N> last;
+    ld_mat<N>(last, ssm + (blockDim.x - 1) * N * N);
+    __syncthreads();
+    if (b < nb) st_mat<N>(agg + b * N * N, e);
+    carry = mat_mul<N>(last, carry);
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kScanThreads) magnus_small_k3(const double2* __restrict__ qloc,
+                                                                const double2* __restrict__ excl,
+                                                                const double2* __restrict__ psi0, int64_t M,
+                                                                double2* __restrict__ traj,
+                                                                unsigned long long* bad_norm) {
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  cplx p0[N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) p0[r] = d2c(psi0[r]);
+  if (n == 0) {
+#pragma unroll
+    for (int r = 0; r < N; ++r) traj[r] = c2d(p0[r]);
+  }
+  if (n >= M) return;
+  Mat<N> e, q;
+  ld_mat<N>(e, excl + (int64_t)blockIdx.x * N * N);
+  ld_mat<N>(q, qloc + n * N * N);
+  cplx v[N], w[N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    cplx acc = np_cmul(e.v[r][0], p0[0]);
+#pragma unroll
+    for (int c = 1; c < N; ++c) acc = cadd(acc, np_cmul(e.v[r][c], p0[c]));
+    v[r] = acc;
+  }
+  double nrm2 = 0.0;
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    cplx acc = np_cmul(q.v[r][0], v[0]);
+#pragma unroll
+    for (int c = 1; c < N; ++c) acc = cadd(acc, np_cmul(q.v[r][c], v[c]));
+    w[r] = acc;
+    nrm2 += acc.re * acc.re + acc.im * acc.im;
+  }
+#pragma unroll
+  for (int r = 0; r < N; ++r) traj[(n + 1) * N + r] = c2d(w[r]);
+  if (!(fabs(sqrt(nrm2) - 1.0) <= 1e-6)) atomicMin(bad_norm, (unsigned long long)n);  // NORM_DRIFT_TOL
+}
+
+// standalone small expm batch (expm_batch for N <= 4)
+template <int N>
+__global__ void expm_small_kernel(const double2* __restrict__ h, int64_t batch, double2* __restrict__ u) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  Mat<N> m;
+  ld_mat<N>(m, h + b * N * N);
+  st_mat<N>(u + b * N * N, expm_minus_i_reg<N>(m));
+}
+template <int N>
+__global__ void validate_small_kernel(const double2* __restrict__ u, int64_t batch, unsigned long long* bad) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  Mat<N> m;
+  ld_mat<N>(m, u + b * N * N);
+  if (!validate_reg<N>(m)) atomicMin(bad, (unsigned long long)b);
+}
+
+// ----------------------------------------------------------------------------
+// generic N
+__global__ void nonfinite_kernel(const double2* __restrict__ h, int64_t per, int64_t batch, unsigned long long* bad) {
+  int64_t total = per * batch;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = h[k];
+    if (!isfinite(v.x) || !isfinite(v.y)) atomicMin(bad, (unsigned long long)(k / per));
+  }
+}
+
+// Hbar for intervals [m0, m0+mb) (magnus.py:185-189 + second order)
+__global__ void assemble_kernel(const double2* __restrict__ h0, const double2* __restrict__ hk,
+                                const double2* __restrict__ comm, int K, int64_t nn, const double* __restrict__ c1,
+                                const double* __restrict__ c2, int64_t m0, int64_t mb, double dt_int, int order,
+                                double2* __restrict__ out) {
+  const int ncomm = K + K * (K - 1) / 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
+    cplx d = d2c(h0[e]);
+    cplx ops[kMaxK];
+    for (int k = 0; k < K; ++k) ops[k] = d2c(hk[k * nn + e]);
+    cplx cm[kMaxK + kMaxK * (kMaxK - 1) / 2];
+    if (order >= 2)
+      for (int q = 0; q < ncomm; ++q) cm[q] = d2c(comm[q * nn + e]);
+    for (int64_t m = 0; m < mb; ++m) {
+      const int64_t gm = m0 + m;
+      cplx v = np_rmul(dt_int, d);
+      for (int k = 0; k < K; ++k) v = cadd(v, np_rmul(c1[gm * K + k], ops[k]));
+      if (order >= 2) {
+        cplx x = mkc(0, 0);
+        for (int q = 0; q < ncomm; ++q) x = cadd(x, np_rmul(c2[gm * ncomm + q], cm[q]));
+        v = cadd(v, np_cmul(mkc(0.0, -0.5), x));
+      }
+      out[m * nn + e] = c2d(v);
+    }
+  }
+}
+
+// X = P - P^dag  (commutator of Hermitian operands from P = A B)
+__global__ void antiherm_kernel(const double2* __restrict__ p, int n, double2* __restrict__ x) {
+  int64_t nn = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / n, c = e - r * n;
+    double2 a = p[e], b = p[c * n + r];
+    x[e] = make_double2(a.x - b.x, a.y + b.y);
+  }
+}
+
+// per-matrix max row sum of |(-i H)|: one thread per row, numpy pairwise
+__global__ void rownorm_kernel(const double2* __restrict__ h, int n, int64_t batch,
+                               unsigned long long* __restrict__ norm) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * batch) return;
+  int64_t b = t / n, r = t - b * n;
+  const double2* row = h + b * (int64_t)n * n + r * n;
+  auto f = [&](int c) {
+    double2 v = row[c];
+    return np_cabs(v.y, -v.x);
+  };
+  double s = np_pairwise(f, n);
+  atomicMax(norm + b, (unsigned long long)__double_as_longlong(s));
+}
+
+// a = (-i H) / 2**s ; out = I + a ; term = a  (Taylor k = 1)
+__global__ void taylor_init_kernel(const double2* __restrict__ h, int n, int64_t batch,
+                                   const unsigned long long* __restrict__ norm, double2* __restrict__ a,
+                                   double2* __restrict__ term, double2* __restrict__ out, int* __restrict__ sarr) {
+  int64_t nn = (int64_t)n * n;
+  int64_t total = nn * batch;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = k / nn, e = k - b * nn;
+    double nm = __longlong_as_double((long long)norm[b]);
+    int s = 0;
+    if (nm > kScaleTarget) s = (int)ceil(log2(QDIV(nm, kScaleTarget)));
+    double scl = ldexp(1.0, -s);
+    double2 v = h[k];
+    double2 av = make_double2(QMUL(v.y, scl), QMUL(-v.x, scl));
+    a[k] = av;
+    term[k] = av;
+    int64_t r = e / n, c = e - r * n;
+    out[k] = make_double2(QADD(r == c ? 1.0 : 0.0, av.x), QADD(0.0, av.y));
+    if (e == 0) sarr[b] = s;
+  }
+}
+
+// out = (s_b > step) ? sq : out
+__global__ void select_square_kernel(double2* __restrict__ out, const double2* __restrict__ sq, int64_t nn,
+                                     int64_t batch, const int* __restrict__ sarr, int step) {
+  int64_t total = nn * batch;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x)
+    if (sarr[k / nn] > step) out[k] = sq[k];
+}
+
+// sequential ordered product for one chunk: psi <- U_m psi, traj rows; one CTA
+__global__ void chain_small_kernel(const double2* __restrict__ u, int n, int64_t mb, double2* __restrict__ psi,
+                                   double2* __restrict__ traj_rows, int64_t m0, unsigned long long* bad_norm) {
+  extern __shared__ __align__(16) double2 csm[];
+  double2* cur = csm;
+  double2* nxt = csm + n;
+  __shared__ double s_red[32];
+  for (int r = threadIdx.x; r < n; r += blockDim.x) cur[r] = psi[r];
+  __syncthreads();
+  for (int64_t m = 0; m < mb; ++m) {
+    const double2* um = u + m * (int64_t)n * n;
+    double part = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      cplx acc = mkc(0, 0);
+      for (int c = 0; c < n; ++c) acc = cadd(acc, np_cmul(d2c(um[(int64_t)r * n + c]), d2c(cur[c])));
+      nxt[r] = c2d(acc);
+      traj_rows[m * n + r] = c2d(acc);
+      part += acc.re * acc.re + acc.im * acc.im;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_red[w];
+      if (!(fabs(sqrt(t) - 1.0) <= 1e-6)) atomicMin(bad_norm, (unsigned long long)(m0 + m));
+    }
+    double2* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+    __syncthreads();
+  }
+  for (int r = threadIdx.x; r < n; r += blockDim.x) psi[r] = cur[r];
+}
+
+// grid-wide GEMV for large n: y = U x; one warp per row
+__global__ void gemv_kernel(const double2* __restrict__ u, int n, const double2* __restrict__ x,
+                            double2* __restrict__ y, double* __restrict__ nrm2) {
+  int lane = threadIdx.x & 31;
+  int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  const double2* row = u + r * n;
+  double ar = 0.0, ai = 0.0;
+  for (int c = lane; c < n; c += 32) {
+    double2 a = __ldcs(row + c), b = x[c];
+    ar = fma(a.x, b.x, ar);
+    ar = fma(-a.y, b.y, ar);
+    ai = fma(a.x, b.y, ai);
+    ai = fma(a.y, b.x, ai);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    ar += __shfl_xor_sync(0xffffffffu, ar, off);
+    ai += __shfl_xor_sync(0xffffffffu, ai, off);
+  }
+  if (lane == 0) {
+    y[r] = make_double2(ar, ai);
+    atomicAdd(nrm2, ar * ar + ai * ai);
+  }
+}
+__global__ void norm_check_kernel(double* nrm2, int64_t m, unsigned long long* bad) {
+  if (!(fabs(sqrt(*nrm2) - 1.0) <= 1e-6)) atomicMin(bad, (unsigned long long)m);
+  *nrm2 = 0.0;
+}
+
+// |det| by LU with partial pivoting, one CTA per matrix (in place on scratch)
+__global__ void lu_absdet_kernel(double2* __restrict__ a, int n, double* __restrict__ out) {
+  double2* m = a + (int64_t)blockIdx.x * n * n;
+  __shared__ double s_best[32];
+  __shared__ int s_bi[32];
+  __shared__ int s_piv;
+  double logdet = 0.0;
+  for (int k = 0; k < n; ++k) {
+    double bm = -1.0;
+    int bi = k;
+    for (int r = k + threadIdx.x; r < n; r += blockDim.x) {
+      double2 v = m[(int64_t)r * n + k];
+      double am = hypot(v.x, v.y);
+      if (am > bm) {
+        bm = am;
+        bi = r;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      double om = __shfl_xor_sync(0xffffffffu, bm, off);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (om > bm || (om == bm && oi < bi)) {
+        bm = om;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_best[threadIdx.x >> 5] = bm;
+      s_bi[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -1.0;
+      int p = k;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        if (s_best[w] > b) {
+          b = s_best[w];
+          p = s_bi[w];
+        }
+      s_piv = p;
+    }
+    __syncthreads();
+    int p = s_piv;
+    if (p != k)
+      for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        double2 t = m[(int64_t)k * n + c];
+        m[(int64_t)k * n + c] = m[(int64_t)p * n + c];
+        m[(int64_t)p * n + c] = t;
+      }
+    __syncthreads();
+    double2 piv = m[(int64_t)k * n + k];
+    double pm = hypot(piv.x, piv.y);
+    logdet += log(pm);
+    if (pm == 0.0) break;
+    double den = piv.x * piv.x + piv.y * piv.y;
+    int64_t rows = n - k - 1;
+    for (int64_t t = threadIdx.x; t < rows * (n - k - 1); t += blockDim.x) {
+      int r = k + 1 + (int)(t / (n - k - 1));
+      int c = k + 1 + (int)(t % (n - k - 1));
+      double2 l = m[(int64_t)r * n + k];
+      double lr = (l.x * piv.x + l.y * piv.y) / den, li = (l.y * piv.x - l.x * piv.y) / den;
+      double2 u = m[(int64_t)k * n + c];
+      double2 v = m[(int64_t)r * n + c];
+      v.x -= lr * u.x - li * u.y;
+      v.y -= lr * u.y + li * u.x;
+      m[(int64_t)r * n + c] = v;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = exp(logdet);
+}
+
+__global__ void validate_flags_kernel(const double* defect, const double* absdet, int n, int64_t batch,
+                                      unsigned long long* bad) {
+  int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  double d = sqrt(defect[b]);
+  if (!(d <= 1e-10 * n) || !(fabs(absdet[b] - 1.0) <= 1e-8)) atomicMin(bad, (unsigned long long)b);
+}
+
+// ----------------------------------------------------------------------------
+static int grid_for(int64_t work, int threads = 256) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, (int64_t)sm_count() * 16));
+}
+
+struct DevBuf {
+  cudaStream_t st;
+  void* p = nullptr;
+  explicit DevBuf(cudaStream_t s) : st(s) {}
+  cudaError_t alloc(size_t b) { return cudaMallocAsync(&p, std::max<size_t>(b, 16), st); }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  T* as() {
+    return (T*)p;
+  }
+};
+
+// exp(-i H) for a batch of n x n (n > 4) with the DMMA GEMM; d_u receives U.
+// work: 3*batch*n*n complex.  sarr: int[batch] (device).
+static int expm_generic(const double2* h, int64_t batch, int n, double2* u, double2* work, int* sarr,
+                        unsigned long long* norm, cudaStream_t st) {
+  const int64_t nn = (int64_t)n * n;
+  double2* a = work;
+  double2* t0 = work + batch * nn;
+  double2* t1 = work + 2 * batch * nn;
+  QCH_CUDA(cudaMemsetAsync(norm, 0, sizeof(unsigned long long) * batch, st));
+  rownorm_kernel<<<(int)((n * batch + 127) / 128), 128, 0, st>>>(h, n, batch, norm);
+  taylor_init_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, n, batch, norm, a, t0, u, sarr);
+  QCH_LAUNCH_CHECK("taylor_init_kernel");
+  note_launch(2);
+  for (int k = 2; k <= kTaylorOrder; ++k) {
+    int rc = zgemm_taylor(t0, a, t1, u, n, batch, QDIV(1.0, (double)k), st);
+    if (rc) return rc;
+    std::swap(t0, t1);
+  }
+  // squaring: s_b times for matrix b
+  std::vector<int> hs(batch);
+  QCH_CUDA(cudaMemcpyAsync(hs.data(), sarr, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+  QCH_CUDA(cudaStreamSynchronize(st));
+  int smax = 0;
+  for (int v : hs) smax = std::max(smax, v);
+  for (int step = 0; step < smax; ++step) {
+    int rc = zgemm(u, u, t0, n, n, n, batch, nn, nn, nn, st);
+    if (rc) return rc;
+    select_square_kernel<<<grid_for(nn * batch), 256, 0, st>>>(u, t0, nn, batch, sarr, step);
+    QCH_LAUNCH_CHECK("select_square_kernel");
+    note_launch(1);
+  }
+  return QCH_OK;
+}
+
+static int validate_generic(const double2* u, int64_t batch, int n, double2* scratch, double* dbuf,
+                            unsigned long long* bad, cudaStream_t st) {
+  const int64_t nn = (int64_t)n * n;
+  double* defect = dbuf;
+  double* absdet = dbuf + batch;
+  QCH_CUDA(cudaMemsetAsync(defect, 0, sizeof(double) * batch, st));
+  int rc = zgemm_defect(u, defect, n, batch, st);
+  if (rc) return rc;
+  QCH_CUDA(cudaMemcpyAsync(scratch, u, sizeof(double2) * nn * batch, cudaMemcpyDeviceToDevice, st));
+  lu_absdet_kernel<<<(unsigned)batch, 256, 0, st>>>(scratch, n, absdet);
+  validate_flags_kernel<<<(int)((batch + 127) / 128), 128, 0, st>>>(defect, absdet, n, batch, bad);
+  QCH_LAUNCH_CHECK("validate_flags_kernel");
+  note_launch(2);
+  return QCH_OK;
+}
+
+}  // namespace qch
+
+// ============================================================================
+using namespace qch;
+
+extern "C" int qch_magnus_coefficients(const double* d_sig, int64_t K, int64_t S, int64_t M, double dt, int order,
+                                       double* d_c1, double* d_c2, void* stream) {
+  if (M < 1) return fail(QCH_ERR_GRID, "need at least one interval");
+  if ((S - 1) % M) return fail(QCH_ERR_GRID, std::to_string(M) + " intervals do not divide " + std::to_string(S - 1) +
+                                                 " sample steps");
+  if (K > kMaxK) return fail(QCH_ERR_UNSUPPORTED, "at most 8 control channels");
+  if (K == 0) return QCH_OK;
+  CoefArgs a{d_sig, (int)K, S, M, (int)((S - 1) / M), dt};
+  cudaStream_t st = (cudaStream_t)stream;
+  coeff_kernel<<<(int)((M + 127) / 128), 128, 0, st>>>(a, order, d_c1, d_c2);
+  QCH_LAUNCH_CHECK("coeff_kernel");
+  note_launch(1);
+  return QCH_OK;
+}
+
+extern "C" int qch_magnus_commutators_c128(const void* d_h0, const void* d_hk, int64_t K, int64_t N, void* d_out,
+                                           void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nn = N * N;
+  DevBuf p(st);
+  QCH_CUDA(p.alloc(sizeof(double2) * nn));
+  const double2* h0 = (const double2*)d_h0;
+  const double2* hk = (const double2*)d_hk;
+  double2* out = (double2*)d_out;
+  int idx = 0;
+  auto one = [&](const double2* A, const double2* B) -> int {
+    int rc = zgemm(A, B, p.as<double2>(), (int)N, (int)N, (int)N, 1, nn, nn, nn, st);
+    if (rc) return rc;
+    antiherm_kernel<<<grid_for(nn), 256, 0, st>>>(p.as<double2>(), (int)N, out + idx * nn);
+    QCH_LAUNCH_CHECK("antiherm_kernel");
+    note_launch(1);
+    ++idx;
+    return QCH_OK;
+  };
+  for (int k = 0; k < K; ++k)
+    if (int rc = one(h0, hk + k * nn)) return rc;
+  for (int k = 0; k < K; ++k)
+    for (int l = k + 1; l < K; ++l)
+      if (int rc = one(hk + k * nn, hk + l * nn)) return rc;
+  return QCH_OK;
+}
+
+extern "C" int qch_magnus_assemble_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                                        const double* d_c1, const double* d_c2, int64_t m0, int64_t mb, double dt_int,
+                                        int order, void* d_hbar, void* stream) {
+  if (K > kMaxK) return fail(QCH_ERR_UNSUPPORTED, "at most 8 control channels");
+  cudaStream_t st = (cudaStream_t)stream;
+  assemble_kernel<<<grid_for(N * N), 256, 0, st>>>((const double2*)d_h0, (const double2*)d_hk,
+                                                    (const double2*)d_comm, (int)K, N * N, d_c1, d_c2, m0, mb, dt_int,
+                                                    order, (double2*)d_hbar);
+  QCH_LAUNCH_CHECK("assemble_kernel");
+  note_launch(1);
+  return QCH_OK;
+}
+
+static int report_bad(unsigned long long* d_bad, int64_t* bad_index, int code, const char* what, cudaStream_t st) {
+  unsigned long long b = 0;
+  QCH_CUDA(cudaMemcpyAsync(&b, d_bad, sizeof b, cudaMemcpyDeviceToHost, st));
+  QCH_CUDA(cudaStreamSynchronize(st));
+  if (b != ~0ull) {
+    if (bad_index) *bad_index = (int64_t)b;
+    return fail(code, std::string(what) + " (item " + std::to_string(b) + ")");
+  }
+  return QCH_OK;
+}
+
+extern "C" int qch_expm_minus_i_batch_c128(const void* d_h, int64_t batch, int64_t n, void* d_u, void* d_work,
+                                           int64_t* bad_index, void* stream) {
+  if (batch <= 0) return QCH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf flags(st);
+  QCH_CUDA(flags.alloc(sizeof(unsigned long long) * (1 + batch) + sizeof(int) * batch));
+  unsigned long long* bad = flags.as<unsigned long long>();
+  QCH_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  const int64_t nn = n * n;
+  nonfinite_kernel<<<grid_for(nn * batch), 256, 0, st>>>((const double2*)d_h, nn, batch, bad);
+  note_launch(1);
+  if (int rc = report_bad(bad, bad_index, QCH_ERR_NONFINITE, "non-finite entries in batch items", st)) return rc;
+  const double2* h = (const double2*)d_h;
+  double2* u = (double2*)d_u;
+  int blocks = (int)((batch + 127) / 128);
+  switch (n) {
+    case 1: expm_small_kernel<1><<<blocks, 128, 0, st>>>(h, batch, u); break;
+    case 2: expm_small_kernel<2><<<blocks, 128, 0, st>>>(h, batch, u); break;
+    case 3: expm_small_kernel<3><<<blocks, 128, 0, st>>>(h, batch, u); break;
+    case 4: expm_small_kernel<4><<<blocks, 128, 0, st>>>(h, batch, u); break;
+    default: {
+      int* sarr = (int*)(bad + 1 + batch);
+      return expm_generic(h, batch, (int)n, u, (double2*)d_work, sarr, bad + 1, st);
+    }
+  }
+  QCH_LAUNCH_CHECK("expm_small_kernel");
+  note_launch(1);
+  return QCH_OK;
+}
+
+extern "C" int qch_validate_unitary_batch_c128(const void* d_u, int64_t batch, int64_t n, int64_t* bad_index,
+                                               void* stream) {
+  if (batch <= 0) return QCH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf flags(st);
+  QCH_CUDA(flags.alloc(sizeof(unsigned long long) + sizeof(double) * 2 * batch));
+  unsigned long long* bad = flags.as<unsigned long long>();
+  QCH_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  const double2* u = (const double2*)d_u;
+  int blocks = (int)((batch + 127) / 128);
+  switch (n) {
+    case 1: validate_small_kernel<1><<<blocks, 128, 0, st>>>(u, batch, bad); break;
+    case 2: validate_small_kernel<2><<<blocks, 128, 0, st>>>(u, batch, bad); break;
+    case 3: validate_small_kernel<3><<<blocks, 128, 0, st>>>(u, batch, bad); break;
+    case 4: validate_small_kernel<4><<<blocks, 128, 0, st>>>(u, batch, bad); break;
+    default: {
+      DevBuf scratch(st);
+      QCH_CUDA(scratch.alloc(sizeof(double2) * n * n * batch));
+      int rc = validate_generic(u, batch, (int)n, scratch.as<double2>(), (double*)(bad + 1), bad, st);
+      if (rc) return rc;
+      return report_bad(bad, bad_index, QCH_ERR_NONFINITE, "propagator not unitary", st);
+    }
+  }
+  QCH_LAUNCH_CHECK("validate_small_kernel");
+  note_launch(1);
+  return report_bad(bad, bad_index, QCH_ERR_NONFINITE, "propagator not unitary", st);
+}
+
+template <int N>
+static int evolve_small(const SmallArgs& base, int64_t M, const double2* psi0, double2* traj,
+                        unsigned long long* bad_norm, cudaStream_t st) {
+  const int K = base.ca.K;
+  const int ncomm = K + K * (K - 1) / 2;
+  const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
+  size_t smem1 = sizeof(double2) * ((size_t)(1 + K + ncomm) * N * N + (size_t)kScanThreads * N * N);
+  QCH_CUDA(cudaFuncSetAttribute(magnus_small_k1<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+  magnus_small_k1<N><<<(unsigned)nb, kScanThreads, smem1, st>>>(base);
+  QCH_LAUNCH_CHECK("magnus_small_k1");
+  int t2 = (int)std::min<int64_t>(1024, std::max<int64_t>(32, ((nb + 31) / 32) * 32));
+  size_t smem2 = sizeof(double2) * (size_t)t2 * N * N;
+  QCH_CUDA(cudaFuncSetAttribute(scan_aggregates_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  scan_aggregates_kernel<N><<<1, t2, smem2, st>>>(base.agg, nb);
+  QCH_LAUNCH_CHECK("scan_aggregates_kernel");
+  magnus_small_k3<N><<<(unsigned)nb, kScanThreads, 0, st>>>(base.qloc, base.agg, psi0, M, traj, bad_norm);
+  QCH_LAUNCH_CHECK("magnus_small_k3");
+  note_launch(3);
+  return QCH_OK;
+}
+
+extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, int64_t K, int64_t N, const double* d_sig,
+                                      int64_t S, double t_start, double t_end, int64_t M, int order,
+                                      const void* d_psi0, void* d_traj, void* d_props, int check, int64_t* bad_index,
+                                      void* stream) {
+  if (M < 1) return fail(QCH_ERR_GRID, "need at least one interval");
+  if ((S - 1) % M)
+    return fail(QCH_ERR_GRID, std::to_string(M) + " intervals do not divide " + std::to_string(S - 1) + " sample steps");
+  if (K > kMaxK) return fail(QCH_ERR_UNSUPPORTED, "at most 8 control channels");
+  if (order != 1 && order != 2) return fail(QCH_ERR_VALUE, "order must be 1 or 2");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nn = N * N;
+  const int ncomm = (int)(K + K * (K - 1) / 2);
+  const double dt = (t_end - t_start) / (double)(S - 1);  // ControlGrid.dt, magnus.py:87-88
+  const double dt_int = (t_end - t_start) / (double)M;     // magnus.py:199
+  CoefArgs ca{d_sig, (int)K, S, M, (int)((S - 1) / M), dt};
+
+  DevBuf flags(st);
+  QCH_CUDA(flags.alloc(sizeof(unsigned long long) * 2));
+  unsigned long long* bad_u = flags.as<unsigned long long>();
+  unsigned long long* bad_norm = bad_u + 1;
+  QCH_CUDA(cudaMemsetAsync(bad_u, 0xff, sizeof(unsigned long long) * 2, st));
+  DevBuf comm(st);
+  if (order >= 2 && ncomm > 0) {
+    QCH_CUDA(comm.alloc(sizeof(double2) * nn * ncomm));
+    if (int rc = qch_magnus_commutators_c128(d_h0, d_hk, K, N, comm.p, stream)) return rc;
+  }
+
+  if (N <= 4) {
+    const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
+    DevBuf q(st);
+    QCH_CUDA(q.alloc(sizeof(double2) * nn * (M + nb)));
+    SmallArgs g;
+    g.ca = ca;
+    g.h0 = (const double2*)d_h0;
+    g.hk = (const double2*)d_hk;
+    g.comm = comm.as<double2>();
+    g.order = order;
+    g.dt_int = dt_int;
+    g.check = check;
+    g.props = (double2*)d_props;
+    g.qloc = q.as<double2>();
+    g.agg = q.as<double2>() + nn * M;
+    g.bad = bad_u;
+    int rc = QCH_OK;
+    switch (N) {
+      case 1: rc = evolve_small<1>(g, M, (const double2*)d_psi0, (double2*)d_traj, bad_norm, st); break;
+      case 2: rc = evolve_small<2>(g, M, (const double2*)d_psi0, (double2*)d_traj, bad_norm, st); break;
+      case 3: rc = evolve_small<3>(g, M, (const double2*)d_psi0, (double2*)d_traj, bad_norm, st); break;
+      default: rc = evolve_small<4>(g, M, (const double2*)d_psi0, (double2*)d_traj, bad_norm, st); break;
+    }
+    if (rc) return rc;
+  } else {
+    DevBuf coef(st);
+    QCH_CUDA(coef.alloc(sizeof(double) * M * (K + ncomm + 1)));
+    double* c1 = coef.as<double>();
+    double* c2 = c1 + M * K;
+    if (K > 0) {
+      if (int rc = qch_magnus_coefficients(d_sig, K, S, M, dt, order, c1, c2, stream)) return rc;
+    }
+    // chunk so that 5 matrices per interval stay within ~12 GiB
+    const size_t per = sizeof(double2) * (size_t)nn;
+    int64_t mb = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)((12ull << 30) / (5 * per))));
+    mb = std::min<int64_t>(mb, 4096);
+    DevBuf buf(st);
+    QCH_CUDA(buf.alloc(per * mb * 5 + sizeof(double2) * N + sizeof(int) * mb + sizeof(unsigned long long) * mb +
+                       sizeof(double) * 2 * mb + 64));
+    double2* hbar = buf.as<double2>();
+    double2* ubuf = hbar + nn * mb;
+    double2* work = ubuf + nn * mb;  // 3 * mb
+    double2* psi = work + 3 * nn * mb;
+    int* sarr = (int*)(psi + N);
+    unsigned long long* norms = (unsigned long long*)(sarr + mb + (mb & 1));
+    double* vbuf = (double*)(norms + mb);
+    QCH_CUDA(cudaMemcpyAsync(psi, d_psi0, sizeof(double2) * N, cudaMemcpyDeviceToDevice, st));
+    QCH_CUDA(cudaMemcpyAsync(d_traj, d_psi0, sizeof(double2) * N, cudaMemcpyDeviceToDevice, st));
+    DevBuf nrm(st);
+    QCH_CUDA(nrm.alloc(sizeof(double)));
+    QCH_CUDA(cudaMemsetAsync(nrm.p, 0, sizeof(double), st));
+    for (int64_t m0 = 0; m0 < M; m0 += mb) {
+      const int64_t cm = std::min<int64_t>(mb, M - m0);
+      if (int rc = qch_magnus_assemble_c128(d_h0, d_hk, comm.p, K, N, c1, c2, m0, cm, dt_int, order, hbar, stream))
+        return rc;
+      double2* u = d_props ? (double2*)d_props + m0 * nn : ubuf;
+      if (int rc = expm_generic(hbar, cm, (int)N, u, work, sarr, norms, st)) return rc;
+      if (check) {
+        if (int rc = validate_generic(u, cm, (int)N, work, vbuf, bad_u, st)) return rc;
+        // report in interval order: offset flagged index by m0 on the host side below
+        unsigned long long b = 0;
+        QCH_CUDA(cudaMemcpyAsync(&b, bad_u, sizeof b, cudaMemcpyDeviceToHost, st));
+        QCH_CUDA(cudaStreamSynchronize(st));
+        if (b != ~0ull) {
+          if (bad_index) *bad_index = (int64_t)b + m0;
+          return fail(QCH_ERR_NONFINITE, "propagator not unitary (interval " + std::to_string(b + m0) + ")");
+        }
+      }
+      double2* traj_rows = (double2*)d_traj + (m0 + 1) * N;
+      if (N < 512) {
+        size_t sm = sizeof(double2) * 2 * N;
+        chain_small_kernel<<<1, 256, sm, st>>>(u, (int)N, cm, psi, traj_rows, m0, bad_norm);
+        QCH_LAUNCH_CHECK("chain_small_kernel");
+        note_launch(1);
+      } else {
+        for (int64_t m = 0; m < cm; ++m) {
+          double2* y = traj_rows + m * N;
+          const double2* x = (m == 0) ? psi : traj_rows + (m - 1) * N;
+          gemv_kernel<<<(int)((N + 7) / 8), 256, 0, st>>>(u + m * nn, (int)N, x, y, nrm.as<double>());
+          norm_check_kernel<<<1, 1, 0, st>>>(nrm.as<double>(), m0 + m, bad_norm);
+          note_launch(2);
+        }
+        QCH_LAUNCH_CHECK("gemv_kernel");
+        QCH_CUDA(cudaMemcpyAsync(psi, traj_rows + (cm - 1) * N, sizeof(double2) * N, cudaMemcpyDeviceToDevice, st));
+      }
+    }
+  }
+  if (check) {
+    if (int rc = report_bad(bad_u, bad_index, QCH_ERR_NONFINITE, "propagator not unitary", st)) return rc;
+  }
+  return report_bad(bad_norm, bad_index, QCH_ERR_NORM_DRIFT, "state norm drifted", st);
+}

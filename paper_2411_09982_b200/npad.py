@@ -1,0 +1,376 @@
+"""NPAD: iterative exact block diagonalisation by Givens rotations, on the GPU.
+
+Drop-in for the reference module (npad.py:1-354): same dataclasses, same
+functions, same signatures and errors.  Every numerical step runs in
+libqcheff's sm_100a kernels:
+
+* ``givens_rotation_matrix``   -> qch_givens_params_c128   (npad.py:101-123)
+* ``unitary_transformation``   -> qch_npad_apply_rotations_c128 (npad.py:131-145, 235-241)
+* ``eliminate_couplings``      -> ONE launch for all disjoint pairs (npad.py:274-297)
+* ``npad_run``                 -> the whole greedy loop on the device (npad.py:300-354)
+
+New API (the parameter-sweep unit of the north star):
+* ``npad_run_batch``           -> one persistent block per operator
+* ``npad_sweep_transmon``      -> builds the sweep Hamiltonians on the device
+
+Rotation convention (reference docstring, npad.py:1-17): the coupling
+``H[j, i] = g e^{i phi}``, ``delta = (H[i,i] - H[j,j]) / 2``,
+``r = hypot(delta, g)``, ``cos t = |delta|/r``, ``sin t = sign(delta) g/r``,
+``cos(t/2) = sqrt((1 + cos t)/2)``, ``sin(t/2) = sin t / (2 cos(t/2))``.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, replace
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import IndexOutOfRange, OverlappingPairs, ZeroCoupling
+from .operators import HermitianOperator
+
+SPARSE_FILL_DROP = 1e-15  # npad.py:33 (sparse path; operators are densified here)
+UNITARY_CHECK_EVERY = 100  # npad.py:36
+UNITARY_DRIFT_TOL = 1e-10  # npad.py:37
+
+
+@dataclass(frozen=True)
+class GivensRotation:
+    """Two-level unitary on span{|i>, |j>}, i < j (npad.py:40-78).
+
+    Block ``[[c, s e^{-i phase}], [-s e^{i phase}, c]]`` with ``c = cos_half``
+    and ``s = sin_half`` (signed).
+    """
+
+    i: int
+    j: int
+    cos_half: float
+    sin_half: float
+    phase: float
+    degenerate: bool = False
+
+    def __post_init__(self):
+        if not (0 <= self.i < self.j):
+            raise IndexOutOfRange(f"need 0 <= i < j, got ({self.i}, {self.j})")
+        residual = abs(self.cos_half**2 + self.sin_half**2 - 1.0)
+        if residual > 1e-14:
+            raise ValueError(f"rotation parameters not normalized: |c^2+s^2-1| = {residual:.2e}")
+
+    def embedded(self) -> np.ndarray:
+        c = self.cos_half
+        se = self.sin_half * np.exp(1j * self.phase)
+        return np.array([[c, np.conj(se)], [-se, c]], dtype=np.complex128)
+
+    def as_matrix(self, dim: int) -> np.ndarray:
+        if self.j >= dim:
+            raise IndexOutOfRange(f"rotation indices ({self.i}, {self.j}) exceed dim {dim}")
+        u = np.eye(dim, dtype=np.complex128)
+        b = self.embedded()
+        u[self.i, self.i], u[self.i, self.j] = b[0, 0], b[0, 1]
+        u[self.j, self.i], u[self.j, self.j] = b[1, 0], b[1, 1]
+        return u
+
+
+@dataclass
+class NPADState:
+    """Operator under iteration plus bookkeeping (npad.py:81-98).
+
+    ``accumulated_unitary`` (when tracked) satisfies
+    ``current = U @ initial @ U^dag``.
+    """
+
+    current: HermitianOperator
+    applied: int = 0
+    accumulated_unitary: np.ndarray | None = None
+    converged: bool = True
+
+    @classmethod
+    def from_operator(cls, op: HermitianOperator, *, track_unitary: bool = False) -> "NPADState":
+        u = np.eye(op.dim, dtype=np.complex128) if track_unitary else None
+        return cls(current=op, accumulated_unitary=u)
+
+
+# -- device helpers -------------------------------------------------------------
+
+def _params_from_rotations(rots: Sequence[GivensRotation]) -> np.ndarray:
+    """Host (c, s) block parameters of given rotations in the kernel layout.
+    s = -sin_half * exp(1j*phase) exactly as _block_params (npad.py:126-128)."""
+    out = np.zeros((len(rots), 8), dtype=np.float64)
+    for k, rot in enumerate(rots):
+        s = -rot.sin_half * np.exp(1j * rot.phase)
+        out[k] = (rot.cos_half, rot.sin_half, rot.phase, float(rot.degenerate), s.real, s.imag, 0.0, 0.0)
+    return out
+
+
+def _device_params(op: HermitianOperator, pairs: Sequence[tuple[int, int]]):
+    """(pairs tensor, params tensor, host params, status) for index pairs."""
+    t = _lib.require_cuda()
+    dev = op.device_tensor()
+    n = len(pairs)
+    d_pairs = _lib.to_device(np.asarray(pairs, dtype=np.int64).reshape(n, 2))
+    d_params = t.empty((n, 8), dtype=t.float64, device="cuda")
+    d_status = t.empty(n, dtype=t.int32, device="cuda")
+    _lib.call(
+        "qch_givens_params_c128", _lib.dptr(dev), op.dim, _lib.dptr(d_pairs), n, _lib.dptr(d_params),
+        _lib.dptr(d_status), _lib.stream_ptr(),
+    )
+    return d_pairs, d_params, _lib.to_host(d_params), _lib.to_host(d_status)
+
+
+def _check_pair(op: HermitianOperator, i: int, j: int) -> None:
+    if not (0 <= i < j < op.dim):
+        raise IndexOutOfRange(f"need 0 <= i < j < {op.dim}, got ({i}, {j})")
+
+
+def _rotation_from_row(i: int, j: int, row: np.ndarray) -> GivensRotation:
+    return GivensRotation(int(i), int(j), float(row[0]), float(row[1]), float(row[2]), degenerate=bool(row[3] != 0.0))
+
+
+def _nonherm(dev) -> int:
+    t = _lib.torch()
+    flag = t.zeros(1, dtype=t.int32, device="cuda")
+    _lib.call("qch_hermitian_exact_c128", _lib.dptr(dev), int(dev.shape[0]), _lib.dptr(flag), _lib.stream_ptr())
+    return int(flag.item())
+
+
+def _apply(op: HermitianOperator, d_pairs, d_params, n_pairs: int, u_host):
+    """Copy op's matrix on the device, apply the rotations; returns the new
+    operator and the updated accumulated unitary (host) if given."""
+    dev = op.device_tensor()
+    out = dev.clone()
+    herm = 0 if _nonherm(out) else 1
+    d_u = _lib.to_device(u_host) if u_host is not None else None
+    _lib.call(
+        "qch_npad_apply_rotations_c128", _lib.dptr(out), op.dim, _lib.dptr(d_pairs), _lib.dptr(d_params), n_pairs,
+        herm, _lib.dptr(d_u), _lib.stream_ptr(),
+    )
+    new_u = _lib.to_host(d_u) if d_u is not None else None
+    return HermitianOperator._from_device(out), new_u, d_u
+
+
+def _audit(d_u, applied: int, dim: int) -> None:
+    """UnitarityDrift audit of npad.py:254-259 on the device."""
+    from .errors import UnitarityDrift
+
+    t = _lib.torch()
+    out = t.zeros(1, dtype=t.float64, device="cuda")
+    _lib.call("qch_unitarity_defect_c128", _lib.dptr(d_u), 1, dim, _lib.dptr(out), _lib.stream_ptr())
+    drift = float(out.item())
+    if drift > UNITARY_DRIFT_TOL * dim:
+        raise UnitarityDrift(f"accumulated unitary drift {drift:.3e} after {applied} rotations")
+
+
+# -- reference API -----------------------------------------------------------------
+
+def givens_rotation_matrix(op: HermitianOperator, i: int, j: int) -> GivensRotation:
+    """Rotation zeroing the (i, j) coupling of ``op`` (npad.py:101-123).
+
+    ZeroCoupling when H[j, i] == 0; a degenerate pair (delta == 0) is flagged.
+    """
+    _check_pair(op, i, j)
+    _, _, params, status = _device_params(op, [(i, j)])
+    if status[0] != 0:
+        raise ZeroCoupling(f"entry ({j}, {i}) is zero; nothing to eliminate")
+    return _rotation_from_row(i, j, params[0])
+
+
+def unitary_transformation(op: HermitianOperator, rot: GivensRotation) -> HermitianOperator:
+    """U H U^dag for one rotation; only rows/columns i, j change (npad.py:235-241)."""
+    if rot.j >= op.dim:
+        raise IndexOutOfRange(f"rotation indices ({rot.i}, {rot.j}) exceed dim {op.dim}")
+    d_pairs = _lib.to_device(np.array([[rot.i, rot.j]], dtype=np.int64))
+    d_params = _lib.to_device(_params_from_rotations([rot]))
+    new_op, _, _ = _apply(op, d_pairs, d_params, 1, None)
+    return new_op
+
+
+def eliminate_coupling(state: NPADState, i: int, j: int) -> NPADState:
+    """Zero one coupling (npad.py:262-271)."""
+    return eliminate_couplings(state, [(i, j)])
+
+
+def eliminate_couplings(state: NPADState, pairs: Sequence[tuple[int, int]]) -> NPADState:
+    """Zero several index-disjoint couplings with rotations all built from the
+    same input operator, applied in list order — one fused launch
+    (npad.py:274-297)."""
+    pairs = [(int(a), int(b)) for a, b in pairs]
+    if not pairs:
+        return state
+    flat = [k for pair in pairs for k in pair]
+    if len(set(flat)) != len(flat):
+        raise OverlappingPairs(f"index pairs share an index: {pairs}")
+    op = state.current
+    for i, j in pairs:
+        _check_pair(op, i, j)
+    d_pairs, d_params, _, status = _device_params(op, pairs)
+    bad = np.flatnonzero(status)
+    if bad.size:
+        i, j = pairs[int(bad[0])]
+        raise ZeroCoupling(f"entry ({j}, {i}) is zero; nothing to eliminate")
+    new_op, new_u, d_u = _apply(op, d_pairs, d_params, len(pairs), state.accumulated_unitary)
+    applied = state.applied + len(pairs)
+    if d_u is not None:
+        # audit whenever a multiple of UNITARY_CHECK_EVERY was reached
+        if applied // UNITARY_CHECK_EVERY > state.applied // UNITARY_CHECK_EVERY:
+            _audit(d_u, applied, op.dim)
+    return replace(state, current=new_op, applied=applied, accumulated_unitary=new_u)
+
+
+def _target_tensor(target, dim: int):
+    if target is None:
+        return None, 0
+    tset = sorted(frozenset(int(k) for k in target))
+    if tset and (max(tset) >= dim or min(tset) < 0):
+        raise IndexOutOfRange("target indices exceed operator dimension")
+    arr = np.asarray(tset, dtype=np.int32)
+    if arr.size == 0:
+        arr = np.zeros(1, dtype=np.int32)  # valid pointer, n_target = 0
+        return _lib.to_device(arr), 0
+    return _lib.to_device(arr), len(tset)
+
+
+def _npad_run_device(op, target, tol, max_iter, track_unitary, pivot_cap=0):
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    if max_iter is None:
+        max_iter = 20 * op.dim * op.dim
+    t = _lib.require_cuda()
+    d_target, n_target = _target_tensor(target, op.dim)
+    threshold = tol * op.max_abs()
+    work = op.device_tensor().clone()
+    d_u = t.eye(op.dim, dtype=t.complex128, device="cuda") if track_unitary else None
+    d_piv = t.full((max(pivot_cap, 1), 2), -1, dtype=t.int32, device="cuda") if pivot_cap > 0 else None
+    applied = ctypes.c_int64(0)
+    conv = ctypes.c_int(0)
+    _lib.call(
+        "qch_npad_run_dense_c128", _lib.dptr(work), op.dim, _lib.dptr(d_target), n_target, float(threshold),
+        int(max_iter), _lib.dptr(d_u), _lib.dptr(d_piv), int(pivot_cap), ctypes.byref(applied), ctypes.byref(conv),
+        _lib.stream_ptr(),
+    )
+    state = NPADState(
+        current=HermitianOperator._from_device(work),
+        applied=int(applied.value),
+        accumulated_unitary=_lib.to_host(d_u) if d_u is not None else None,
+        converged=bool(conv.value),
+    )
+    pivots = None
+    if d_piv is not None:
+        pivots = _lib.to_host(d_piv)[: min(state.applied, pivot_cap)]
+    return state, pivots
+
+
+def npad_run(
+    op: HermitianOperator,
+    target: Iterable[int] | None = None,
+    *,
+    tol: float,
+    max_iter: int | None = None,
+    track_unitary: bool = False,
+) -> NPADState:
+    """Eliminate the largest remaining coupling until convergence (npad.py:320-354).
+
+    ``target=None`` drives toward a full diagonal; a set of indices decouples
+    that subspace (only couplings with exactly one endpoint inside count).
+    Converged when every relevant magnitude is below ``tol * max|op|``;
+    reaching ``max_iter`` (default ``20 * dim**2``) returns
+    ``converged=False``.  The entire greedy chain runs on the device.
+    """
+    state, _ = _npad_run_device(op, target, tol, max_iter, track_unitary)
+    return state
+
+
+def npad_run_logged(op, target=None, *, tol, max_iter=None, track_unitary=False, pivot_cap=None):
+    """``npad_run`` plus the (i, j) pivot sequence (int32 array, one row per
+    rotation) — the parity harness's view of the greedy order."""
+    if pivot_cap is None:
+        pivot_cap = max_iter if max_iter is not None else 20 * op.dim * op.dim
+    return _npad_run_device(op, target, tol, max_iter, track_unitary, pivot_cap=int(pivot_cap))
+
+
+# -- new API: batched sweeps ----------------------------------------------------------
+
+@dataclass
+class BatchResult:
+    """Result of a batched npad_run: device-resident final operators
+    (batch, n, n), rotation counts and convergence flags."""
+
+    matrices: object  # CUDA tensor (batch, n, n) complex128
+    applied: np.ndarray
+    converged: np.ndarray
+
+    def operator(self, b: int) -> HermitianOperator:
+        return HermitianOperator._from_device(self.matrices[b])
+
+    def diagonals(self) -> np.ndarray:
+        return _lib.to_host(self.matrices.diagonal(dim1=1, dim2=2).real.contiguous())
+
+
+def _run_batch_inplace(mats, target, tol, max_iter, max_abs_dev=None, sync=True):
+    t = _lib.require_cuda()
+    b, n = int(mats.shape[0]), int(mats.shape[1])
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    if max_iter is None:
+        max_iter = 20 * n * n
+    d_target, n_target = _target_tensor(target, n)
+    if max_abs_dev is None:
+        max_abs_dev = t.empty(b, dtype=t.float64, device="cuda")
+        for k in range(b):
+            _lib.call("qch_max_abs_c128", _lib.dptr(mats[k]), n * n, _lib.dptr(max_abs_dev[k:k + 1]), _lib.stream_ptr())
+    thr = max_abs_dev * float(tol)
+    applied = t.empty(b, dtype=t.int64, device="cuda")
+    conv = t.empty(b, dtype=t.int32, device="cuda")
+    _lib.call(
+        "qch_npad_run_batch_c128", _lib.dptr(mats), b, n, _lib.dptr(d_target), n_target, _lib.dptr(thr),
+        int(max_iter), _lib.dptr(applied), _lib.dptr(conv), _lib.stream_ptr(),
+    )
+    return applied, conv
+
+
+def npad_run_batch(ops: Sequence[HermitianOperator], target=None, *, tol: float, max_iter: int | None = None,
+                   devices: Sequence[int] | None = None) -> BatchResult:
+    """``npad_run`` over independent operators of one dimension, one
+    persistent block per operator (new API; per-point results equal
+    ``npad_run`` on each operator).  Operators must be exactly Hermitian
+    (H[x,y] == conj(H[y,x]) bitwise), as the builders produce."""
+    t = _lib.require_cuda()
+    ops = list(ops)
+    if not ops:
+        raise ValueError("need at least one operator")
+    n = ops[0].dim
+    mats = t.stack([op.device_tensor() for op in ops]).contiguous()
+    nonherm = any(_nonherm(mats[k]) for k in range(len(ops)))
+    if nonherm:
+        raise ValueError("npad_run_batch needs exactly Hermitian operators; use npad_run per operator")
+    max_abs = t.tensor([op.max_abs() for op in ops], dtype=t.float64, device="cuda")
+    applied, conv = _run_batch_inplace(mats, target, tol, max_iter, max_abs)
+    return BatchResult(mats, _lib.to_host(applied), _lib.to_host(conv).astype(bool))
+
+
+def build_transmon_resonator_batch(params: np.ndarray, n_q: int, n_r: int):
+    """Device-built transmon (x) resonator Hamiltonians, one per row of
+    ``params`` = (omega_q, alpha, omega_r, g).  Same matrix as
+    models.transmon_resonator_hamiltonian."""
+    t = _lib.require_cuda()
+    params = np.ascontiguousarray(params, dtype=np.float64).reshape(-1, 4)
+    b = params.shape[0]
+    n = n_q * n_r
+    mats = t.empty((b, n, n), dtype=t.complex128, device="cuda")
+    d_prm = _lib.to_device(params)
+    _lib.call("qch_build_transmon_resonator_c128", _lib.dptr(mats), b, n_q, n_r, _lib.dptr(d_prm), _lib.stream_ptr())
+    return mats
+
+
+def npad_sweep_transmon(params: np.ndarray, n_q: int, n_r: int, target=None, *, tol: float,
+                        max_iter: int | None = None) -> BatchResult:
+    """Parameter sweep of config 4: build every (omega_q, alpha, omega_r, g)
+    point on the device and run the batched greedy NPAD (new API)."""
+    t = _lib.require_cuda()
+    mats = build_transmon_resonator_batch(params, n_q, n_r)
+    n = n_q * n_r
+    max_abs = t.empty(mats.shape[0], dtype=t.float64, device="cuda")
+    for k in range(mats.shape[0]):
+        _lib.call("qch_max_abs_c128", _lib.dptr(mats[k]), n * n, _lib.dptr(max_abs[k:k + 1]), _lib.stream_ptr())
+    applied, conv = _run_batch_inplace(mats, target, tol, max_iter, max_abs)
+    return BatchResult(mats, _lib.to_host(applied), _lib.to_host(conv).astype(bool))

@@ -1,0 +1,146 @@
+"""Magnus / expm on the GPU vs the oracle and the reference's golden vectors.
+Bar: 1e-10 relative (Frobenius) on matrices and trajectories."""
+import numpy as np
+import pytest
+
+from conftest import rel_fro
+from oracle import expm_oracle, magnus_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def E():
+    import paper_2411_09982_b200 as eff
+
+    return eff
+
+
+def _ch(E, drift, controls):
+    return E.ControlledHamiltonian(E.HermitianOperator(drift), [E.HermitianOperator(c) for c in controls])
+
+
+def test_expm_vs_reference_golden(E, golden):
+    g = golden("expm")
+    for key in [k for k in g if k.startswith("h")]:
+        u = E.expm_unitary(g[key]).entries
+        assert rel_fro(u, g["u" + key[1:]]) <= 1e-12, key
+
+
+def test_expm_batch_and_validate(E):
+    rng = np.random.default_rng(0)
+    hs = []
+    for n in (3, 3, 3, 17, 17):
+        a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        hs.append((a + a.conj().T) * 0.8)
+    props = E.expm_batch(hs)
+    for h, p in zip(hs, props):
+        assert rel_fro(p.entries, expm_oracle.expm_minus_i(h)) <= 1e-12
+        assert p.unitarity_defect() <= 1e-12
+    bad = np.full((3, 3), np.nan)
+    with pytest.raises(E.NonFinite):
+        E.expm_batch([hs[0], bad])
+    with pytest.raises(E.NonFinite):
+        E.UnitaryPropagator(2 * np.eye(3, dtype=complex)).validate()
+
+
+@pytest.mark.parametrize("case", ["magnus_transmon_m2000", "magnus_spin6_m20"])
+def test_evolve_order1_vs_reference_golden(E, golden, case):
+    g = golden(case)
+    t0, t1 = g["t"]
+    m = int(g["m"])
+    ch = _ch(E, g["drift"], g["controls"])
+    grid = E.ControlGrid(t0, t1, g["signals"])
+    np.testing.assert_array_equal(E.magnus_coefficients(grid, m), g["coeffs"])
+    traj = E.evolve(ch, grid, m, g["psi0"])
+    assert rel_fro(traj.amplitudes, g["traj"]) <= 1e-10
+    if "hbar_head" in g:
+        iv = E.magnus_intervals(ch, grid, m)
+        hb = np.stack([iv.effective_hams[k].data for k in range(16)])
+        assert rel_fro(hb, g["hbar_head"]) <= 1e-14
+        _, props = E.evolve(ch, grid, m, g["psi0"], return_propagators=True)
+        assert rel_fro(np.stack([p.entries for p in props[:16]]), g["u_head"]) <= 1e-12
+
+
+@pytest.mark.parametrize("m", [1, 7, 300, 1000])
+def test_evolve_order2_transmon_vs_oracle(E, m):
+    ch, grid = E.driven_transmon(3, intervals=m, sub=4)
+    d0 = ch.drift.data
+    ctr = np.stack([c.data for c in ch.controls])
+    psi0 = np.array([1, 0, 0], dtype=complex)
+    ref = magnus_oracle.evolve(d0, ctr, grid.signals, grid.t_start, grid.t_end, m, psi0, order=2)
+    got = E.evolve(ch, grid, m, psi0, order=2)
+    assert rel_fro(got.amplitudes, ref) <= 1e-10
+    c2 = E.magnus_coefficients_second_order(grid, m)
+    np.testing.assert_array_equal(c2, magnus_oracle.second_order_coefficients(grid.signals, grid.t_start, grid.t_end, m))
+
+
+def test_evolve_order2_spin_chain_vs_oracle(E, golden):
+    g = golden("magnus_spin6_m20")
+    t0, t1 = g["t"]
+    ch = _ch(E, g["drift"], g["controls"])
+    grid = E.ControlGrid(t0, t1, g["signals"])
+    ref = magnus_oracle.evolve(g["drift"], g["controls"], g["signals"], t0, t1, 20, g["psi0"], order=2)
+    got = E.evolve(ch, grid, 20, g["psi0"], order=2)
+    assert rel_fro(got.amplitudes, ref) <= 1e-10
+    iv = E.magnus_intervals(ch, grid, 20, order=2)
+    hb = magnus_oracle.effective_hamiltonians(g["drift"], g["controls"], g["signals"], t0, t1, 20, order=2)
+    assert rel_fro(iv.effective_hams.to_numpy(), hb) <= 1e-13
+
+
+def test_evolve_large_dim_heisenberg_vs_oracle(E):
+    # dim 256 (L = 8) exercises the DMMA Taylor path and the chain kernel
+    ch = E.heisenberg_chain_hamiltonians(8)
+    grid = E.synthetic_transfer_pulse(2.0, 4 * 8 + 1, seed=7)
+    psi0 = np.zeros(256, dtype=complex)
+    psi0[0] = 1
+    d0 = ch.drift.to_dense()
+    ctr = np.stack([c.to_dense() for c in ch.controls])
+    for order in (1, 2):
+        ref = magnus_oracle.evolve(d0, ctr, grid.signals, grid.t_start, grid.t_end, 4, psi0, order=order)
+        got = E.evolve(ch, grid, 4, psi0, order=order)
+        assert rel_fro(got.amplitudes, ref) <= 1e-10
+
+
+def test_constant_hamiltonian_exactness(E):
+    # SPEC AC5: time-independent evolution == eigendecomposition, any M
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4))
+    h = (a + a.conj().T) / 2
+    ch = E.ControlledHamiltonian(E.HermitianOperator(h))
+    psi0 = np.array([1, 0, 0, 0], dtype=complex)
+    w, v = np.linalg.eigh(h)
+    exact = v @ (np.exp(-1j * w * 2.0) * (v.conj().T @ psi0))
+    for m in (1, 10, 100):
+        grid = E.ControlGrid(0.0, 2.0, samples=m + 1)
+        traj = E.evolve(ch, grid, m, psi0)
+        assert np.linalg.norm(traj.amplitudes[-1] - exact) <= 1e-10
+
+
+def test_magnus_errors(E):
+    ch, grid = E.driven_transmon(3, intervals=10, sub=4)
+    with pytest.raises(E.GridMismatch):
+        E.magnus_coefficients(grid, 7)
+    with pytest.raises(E.GridMismatch):
+        E.evolve(ch, grid, 0, np.array([1, 0, 0], dtype=complex))
+    with pytest.raises(E.DimensionMismatch):
+        E.evolve(ch, grid, 10, np.array([1, 0], dtype=complex))
+    with pytest.raises(ValueError):
+        E.evolve(ch, grid, 10, np.array([1, 1, 0], dtype=complex))
+    with pytest.raises(E.DimensionMismatch):
+        E.assemble_effective_hams(ch, np.zeros((10, 3)), 0.1)
+
+
+def test_zgemm_dmma_vs_numpy(E):
+    import torch
+    from paper_2411_09982_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    for m, n, k, b in [(64, 64, 64, 1), (100, 37, 129, 3), (1, 1, 1, 2), (257, 130, 65, 1)]:
+        a = rng.standard_normal((b, m, k)) + 1j * rng.standard_normal((b, m, k))
+        bb = rng.standard_normal((b, k, n)) + 1j * rng.standard_normal((b, k, n))
+        da, db = _lib.to_device(a), _lib.to_device(bb)
+        dc = torch.empty((b, m, n), dtype=torch.complex128, device="cuda")
+        _lib.call("qch_zgemm_batched", _lib.dptr(da), _lib.dptr(db), _lib.dptr(dc), m, n, k, b, m * k, k * n, m * n,
+                  _lib.stream_ptr())
+        assert rel_fro(dc.cpu().numpy(), a @ bb) <= 1e-14

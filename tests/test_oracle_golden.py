@@ -1,0 +1,58 @@
+"""The CPU oracle (oracle/) against golden vectors produced by the reference
+itself (oracle/gen_golden.py).  Bit-exact: same numpy operations, same host."""
+import numpy as np
+import pytest
+
+from oracle import expm_oracle, magnus_oracle, npad_oracle
+
+
+@pytest.mark.parametrize("runner", [npad_oracle.run_full_scan, npad_oracle.run_incremental])
+@pytest.mark.parametrize("case", ["npad_tr3x20_full", "npad_rand24_full_u", "npad_tr4x30_sub", "npad_tr4x60_k150"])
+def test_npad_oracle_bit_exact(golden, runner, case):
+    g = golden(case)
+    target = g["target"].tolist() if "target" in g else None
+    max_iter = int(g["max_iter"]) if "max_iter" in g else None
+    out = runner(g["h"], target, tol=float(g["tol"]), max_iter=max_iter, track_unitary="u" in g)
+    assert out["applied"] == int(g["applied"])
+    assert out["converged"] == bool(g["converged"])
+    np.testing.assert_array_equal(out["pivots"], g["pivots"])
+    np.testing.assert_array_equal(out["h"], g["final"])
+    if "u" in g:
+        np.testing.assert_array_equal(out["u"], g["u"])
+
+
+def test_eliminate_pairs_oracle(golden):
+    g = golden("npad_jc_pairs")
+    h, u = npad_oracle.eliminate_pairs(g["h"], [tuple(p) for p in g["pairs"]], np.eye(g["h"].shape[0]))
+    np.testing.assert_array_equal(h, g["final"])
+    np.testing.assert_array_equal(u, g["u"])
+
+
+def test_givens_oracle(golden):
+    g = golden("givens_2x2")
+    for k in range(0, 1000, 7):
+        c, sh, ph, deg = npad_oracle.rotation_scalars(g["mats"][k], 0, 1)
+        assert (c, sh, ph, float(deg)) == tuple(g["params"][k])
+        h = g["mats"][k].copy()
+        npad_oracle.rotate(h, 0, 1, c, npad_oracle.block_s(sh, ph))
+        np.testing.assert_array_equal(h, g["after"][k])
+
+
+def test_expm_oracle(golden):
+    g = golden("expm")
+    for key in [k for k in g if k.startswith("h")]:
+        np.testing.assert_array_equal(expm_oracle.expm_minus_i(g[key]), g["u" + key[1:]])
+
+
+@pytest.mark.parametrize("case", ["magnus_transmon_m2000", "magnus_spin6_m20"])
+def test_magnus_oracle(golden, case):
+    g = golden(case)
+    t0, t1 = g["t"]
+    m = int(g["m"])
+    c = magnus_oracle.first_order_coefficients(g["signals"], t0, t1, m)
+    np.testing.assert_array_equal(c, g["coeffs"])
+    traj = magnus_oracle.evolve(g["drift"], g["controls"], g["signals"], t0, t1, m, g["psi0"])
+    np.testing.assert_array_equal(traj, g["traj"])
+    if "hbar_head" in g:
+        hb = magnus_oracle.effective_hamiltonians(g["drift"], g["controls"], g["signals"], t0, t1, m)
+        np.testing.assert_array_equal(hb[:16], g["hbar_head"])
