@@ -1,0 +1,609 @@
+#!/usr/bin/env python
+"""bench.py — qCH_eff hot paths on B200 (libqcheff, sm_100a).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--secondary all|none|npad60,npad4096,sweep,magnus4096]
+
+Headline (BASELINE.json metric, configs[1]): Magnus time coarse-graining of a
+driven 3-level transmon, 10^5 intervals per GPU, SECOND order, intervals/s.
+N > 1 GPUs: weak scaling — every rank owns 10^5 contiguous intervals of one
+global evolution; the ranks all-gather their block products (NCCL) for the
+ordered product.  Secondary lines (N = 1, rank 0): NPAD configs 1, 3, 4 and
+Magnus config 5 (sampled), each with its own roofline.
+
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events
+on the launching stream (L2 flushed between steps by writing a 256 MiB
+buffer, outside the events); barrier + synchronize around the timed region;
+max over ranks.  ``e2e`` repeats the step through the public API from pinned
+host buffers (H2D of the inputs + D2H of the trajectory inside the timing).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
+METRIC = BASELINE["metric"]
+M_PER_GPU = 100_000
+SUB = 4
+T_PER_GPU = 100.0
+
+
+# ---------------------------------------------------------------- helpers --
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6545.6), "MEASURED_PEAKS.json"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        self.tmp.flush()
+        rows = []
+        try:
+            for line in Path(self.tmp.name).read_text().splitlines():
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        loaded = [v for v in sm if v > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+class L2Flusher:
+    def __init__(self, torch):
+        self.buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def __call__(self):
+        self.buf.fill_(1.0)
+
+
+def time_steps(torch, fn, steps, flush, world):
+    """Per-step CUDA-event timing (current stream); returns list of ms."""
+    import torch.distributed as dist
+
+    out = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for _ in range(steps):
+        flush()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        out.append(s.elapsed_time(e))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    return out
+
+
+def max_over_ranks(torch, value, world):
+    if world == 1:
+        return value
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def fp64_peaks(torch, lib_mod):
+    """Live FP64 probes (DFMA pipe, DMMA tensor pipe) -> TFLOP/s."""
+    import ctypes
+
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    res = {}
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    for kind, name, iters in ((0, "dfma", 2000), (1, "dmma", 4000)):
+        fl = ctypes.c_double(0)
+        best = 0.0
+        for _ in range(4):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            lib_mod.load().qch_peak_kernel(kind, sms * 8, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(fl),
+                                           lib_mod.stream_ptr())
+            e.record()
+            torch.cuda.synchronize()
+            best = max(best, fl.value / (s.elapsed_time(e) * 1e-3) / 1e12)
+        res[name] = best
+    # cuBLAS zgemm (library reference point for the DMMA path)
+    a = torch.randn(4096, 4096, dtype=torch.complex128, device="cuda")
+    b = torch.randn(4096, 4096, dtype=torch.complex128, device="cuda")
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(3):
+        torch.matmul(a, b)
+    e.record()
+    torch.cuda.synchronize()
+    res["cublas_zgemm"] = 3 * 8 * 4096**3 / (s.elapsed_time(e) * 1e-3) / 1e12
+    del a, b
+    return res
+
+
+def traffic_from_profiles(kernel: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        v = d.get(kernel)
+        if isinstance(v, dict):
+            return v.get("bytes_per_launch")
+    return None
+
+
+# ------------------------------------------------------- headline: Magnus --
+
+def magnus_inputs(eff, world, rank):
+    m = M_PER_GPU * world
+    ch, grid = eff.driven_transmon(3, intervals=m, sub=SUB, t_final=T_PER_GPU * world)
+    psi0 = np.array([1, 0, 0], dtype=np.complex128)
+    return ch, grid, m, psi0
+
+
+# Algorithmic FP64 flops per interval of the fused interval kernel (N=3, K=2,
+# order 2): 17 complex N^3 GEMMs (8N^3 each) + 18 scale/add passes (4N^2) of
+# the Taylor series (expm.py:66-68) + assembly of 1 + K + K(K+1)/2 operator
+# terms (4N^2 each: real*complex + add) + second-order coefficients (~14*sub*K^2).
+def magnus_flops_per_interval(n=3, k=2, sub=SUB):
+    ncomm = k + k * (k - 1) // 2
+    return 17 * 8 * n**3 + 18 * 4 * n * n + (1 + k + ncomm) * 4 * n * n + 14 * sub * k * k
+
+
+def cpu_magnus_sample(eff_models, n_int):
+    """Oracle (numpy port of the reference, + 2nd order) on a bounded sample."""
+    from oracle import magnus_oracle
+
+    ch, grid = eff_models.driven_transmon(3, intervals=n_int, sub=SUB, t_final=T_PER_GPU * n_int / M_PER_GPU)
+    d0 = ch.drift.data
+    ctr = np.stack([c.data for c in ch.controls])
+    psi0 = np.array([1, 0, 0], dtype=complex)
+    t0 = time.perf_counter()
+    magnus_oracle.evolve(d0, ctr, grid.signals, grid.t_start, grid.t_end, n_int, psi0, order=2)
+    dt = time.perf_counter() - t0
+    return n_int / dt, dt
+
+
+def run_headline(torch, eff, lib, args, world, rank, local):
+    from paper_2411_09982_b200 import magnus as mg
+    from paper_2411_09982_b200 import sharding
+
+    ch, grid, m, psi0 = magnus_inputs(eff, world, rank)
+    psi0_dev = lib.to_device(psi0)
+    flush = L2Flusher(torch)
+
+    if world == 1:
+        def step():
+            mg.evolve_device(ch, grid, m, psi0_dev, check=False, order=2)
+    else:
+        def step():
+            sharding.evolve_sharded(ch, grid, m, psi0, order=2, check=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    lib.profile_read(reset=True)
+    lib.profile_enable(True)
+    n0 = lib.launch_count()
+    with ClockSampler(local) as clk:
+        ms = time_steps(torch, step, args.steps, flush, world)
+    launches = lib.launch_count() - n0
+    lib.profile_enable(False)
+    prof = lib.profile_read(reset=True)
+    total_ms = max_over_ranks(torch, sum(ms), world)
+    per_step = total_ms / args.steps
+    value = M_PER_GPU * world / (per_step * 1e-3)
+
+    # e2e through the public API from pinned host buffers
+    sig_pinned = torch.empty(grid.signals.shape, dtype=torch.float64).pin_memory()
+    sig_pinned.numpy()[:] = grid.signals
+    ops = [ch.drift.data] + [c.data for c in ch.controls]
+
+    def e2e_step():
+        chh = eff.ControlledHamiltonian(eff.HermitianOperator(ops[0], validate=False),
+                                        [eff.HermitianOperator(o, validate=False) for o in ops[1:]])
+        gh = eff.ControlGrid(grid.t_start, grid.t_end, sig_pinned.numpy())
+        if world == 1:
+            tr = eff.evolve(chh, gh, m, psi0, order=2, check=False)
+            return tr.amplitudes
+        res = sharding.evolve_sharded(chh, gh, m, psi0, order=2, check=False)
+        return res.trajectory.cpu().numpy()
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = time_steps(torch, e2e_step, max(1, min(args.steps, 5)), flush, world)
+    e2e_per = max_over_ranks(torch, sum(e2e_ms), world) / len(e2e_ms)
+    h2d = grid.signals.nbytes // world + sum(o.nbytes for o in ops) + psi0.nbytes
+    d2h = (M_PER_GPU + 1) * 3 * 16
+
+    k1 = prof.get("magnus_small_k1")
+    roof = None
+    if k1:
+        k1_ms = k1[0] / k1[1]
+        fl = magnus_flops_per_interval() * M_PER_GPU
+        roof = {"kernel": "magnus_small_k1", "launch_ms": k1_ms, "flops_per_launch": fl,
+                "kernel_share_of_step": k1_ms / per_step}
+    return dict(value=value, per_step=per_step, ms=ms, launches=launches // args.steps, clocks=clk.summary(),
+                e2e=(M_PER_GPU * world / (e2e_per * 1e-3), h2d, d2h), roof=roof, m=m)
+
+
+# -------------------------------------------------------------- secondaries --
+
+def sec_npad60(torch, eff, lib, args, peaks):
+    from oracle import npad_oracle
+
+    h = eff.transmon_resonator_hamiltonian(3, 20).data
+    op = eff.HermitianOperator(h)
+    op.device_tensor()
+    op.max_abs()
+    res = {}
+
+    def step():
+        res["st"] = eff.npad_run(op, tol=1e-12)
+
+    for _ in range(3):
+        step()
+    lib.profile_read(reset=True)
+    lib.profile_enable(True)
+    ms = time_steps(torch, step, 10, lambda: None, 1)
+    lib.profile_enable(False)
+    prof = lib.profile_read(reset=True)
+    rot = res["st"].applied
+    per = sum(ms) / len(ms)
+    kms = prof["npad_run_kernel"][0] / prof["npad_run_kernel"][1]
+    t0 = time.perf_counter()
+    ref = npad_oracle.run_full_scan(h, tol=1e-12)
+    cpu = ref["applied"] / (time.perf_counter() - t0)
+    return {"workload": "config 1: NPAD transmon3 x resonator20 (dim 60), full diagonal, tol 1e-12",
+            "metric": "NPAD rotations/s", "unit": "rotations/s", "value": rot / (per * 1e-3),
+            "rotations": rot, "ms_per_solve": per, "us_per_rotation_kernel": kms * 1e3 / rot,
+            "roofline": {"bound": "latency", "note": "serial greedy chain; matrix resident in shared memory",
+                         "achieved": 96 * 60 * rot / (kms * 1e-3) / 1e9, "peak": peaks[0], "unit": "GB/s",
+                         "frac": 96 * 60 * rot / (kms * 1e-3) / 1e9 / peaks[0]},
+            "cpu_baseline": {"value": cpu, "unit": "rotations/s", "cores": 1, "kind": "port",
+                             "sample": "full solve (1022 rotations), oracle run_full_scan (reference algorithm)"}}
+
+
+def sec_npad4096(torch, eff, lib, args, peaks, rotations=None):
+    from oracle import npad_oracle
+
+    n_q, n_r = 4, 1024
+    h = eff.transmon_resonator_hamiltonian(n_q, n_r).data
+    op = eff.HermitianOperator(h, validate=False)
+    op.device_tensor()
+    op.max_abs()
+    res = {}
+    mi = rotations
+
+    def step():
+        res["st"] = eff.npad_run(op, tol=1e-12, max_iter=mi)
+
+    step()
+    lib.profile_read(reset=True)
+    lib.profile_enable(True)
+    ms = time_steps(torch, step, 2, L2Flusher(torch), 1)
+    lib.profile_enable(False)
+    prof = lib.profile_read(reset=True)
+    st = res["st"]
+    per = sum(ms) / len(ms)
+    kms = prof["npad_run_kernel"][0] / prof["npad_run_kernel"][1]
+    n = n_q * n_r
+    ach = 96 * n * st.applied / (kms * 1e-3) / 1e9
+    t0 = time.perf_counter()
+    ref = npad_oracle.run_full_scan(h, tol=1e-12, max_iter=3)
+    cpu = 3 / (time.perf_counter() - t0)
+    return {"workload": f"config 3: NPAD transmon4 x resonator1024 (dim 4096) dense complex128, full diagonal, "
+                        f"tol 1e-12, {'max_iter=' + str(mi) if mi else 'to convergence'}",
+            "metric": "NPAD rotations/s", "unit": "rotations/s", "value": st.applied / (per * 1e-3),
+            "rotations": st.applied, "converged": st.converged, "ms_per_solve": per,
+            "us_per_rotation_kernel": kms * 1e3 / st.applied,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks[0], "unit": "GB/s", "frac": ach / peaks[0],
+                         "bytes_per_rotation": 96 * n, "note": "single greedy chain: latency-bound (see DESIGN.md)",
+                         "traffic": traffic_from_profiles("npad_run_kernel_4096")},
+            "cpu_baseline": {"value": cpu, "unit": "rotations/s", "cores": 1, "kind": "port",
+                             "sample": "3 rotations of the same operator, oracle run_full_scan"}}
+
+
+def sec_sweep(torch, eff, lib, args, peaks, n_points=1024):
+    from oracle import npad_oracle
+
+    n_q, n_r = 4, 256
+    n = n_q * n_r
+    side = int(round(n_points ** 0.5))
+    pts = eff.sweep_points(side, n_points // side)
+    tgt = eff.sweep_target(n_r)
+    from paper_2411_09982_b200 import npad as npd
+
+    state = {}
+
+    def rebuild():
+        state["mats"] = npd.build_transmon_resonator_batch(pts, n_q, n_r)
+        mx = torch.empty(pts.shape[0], dtype=torch.float64, device="cuda")
+        for k in range(pts.shape[0]):
+            lib.call("qch_max_abs_c128", lib.dptr(state["mats"][k]), n * n, lib.dptr(mx[k:k + 1]), lib.stream_ptr())
+        state["mx"] = mx
+
+    def step():
+        state["out"] = npd._run_batch_inplace(state["mats"], tgt, 1e-12, None, state["mx"])
+
+    rebuild()
+    step()
+    tot = []
+    lib.profile_read(reset=True)
+    lib.profile_enable(True)
+    for _ in range(2):
+        rebuild()  # fresh operators; writes 16 GiB => L2 flushed
+        tot += time_steps(torch, step, 1, lambda: None, 1)
+    lib.profile_enable(False)
+    prof = lib.profile_read(reset=True)
+    applied = state["out"][0].cpu().numpy()
+    conv = state["out"][1].cpu().numpy()
+    rot = int(applied.sum())
+    per = sum(tot) / len(tot)
+    kms = prof["npad_run_kernel"][0] / prof["npad_run_kernel"][1]
+    ach = 96 * n * rot / (kms * 1e-3) / 1e9
+    # CPU: reference algorithm on 2 sweep points
+    t0 = time.perf_counter()
+    crot = 0
+    for row in pts[:2]:
+        h = eff.transmon_resonator_hamiltonian(n_q, n_r, omega_q=row[0], alpha=row[1], omega_r=row[2], g=row[3]).data
+        crot += npad_oracle.run_full_scan(h, tgt, tol=1e-12, max_iter=60)["applied"]
+    cpu = crot / (time.perf_counter() - t0)
+    return {"workload": f"config 4: NPAD sweep {pts.shape[0]} (g, Delta) points, transmon4 x resonator256 (dim 1024),"
+                        f" subspace target 10 levels, tol 1e-12, one GPU",
+            "metric": "NPAD rotations/s", "unit": "rotations/s", "value": rot / (per * 1e-3), "rotations": rot,
+            "all_converged": bool(conv.all()), "ms_per_sweep": per,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks[0], "unit": "GB/s", "frac": ach / peaks[0],
+                         "bytes_per_rotation": 96 * n, "traffic": traffic_from_profiles("npad_run_kernel_sweep")},
+            "cpu_baseline": {"value": cpu, "unit": "rotations/s", "cores": 1, "kind": "port",
+                             "sample": "first 60 rotations of 2 sweep points, oracle run_full_scan"}}
+
+
+def sec_magnus4096(torch, eff, lib, args, fp64, n_int=2):
+    from paper_2411_09982_b200 import magnus as mg
+
+    L = 12
+    ch = eff.heisenberg_chain_hamiltonians(L)
+    full = eff.synthetic_transfer_pulse(25.0, 4096 * 8 + 1, seed=7)
+    grid = eff.ControlGrid(0.0, 25.0 * n_int / 4096, full.signals[:, :n_int * 8 + 1])
+    psi0 = np.zeros(1 << L, dtype=complex)
+    psi0[0] = 1
+    d_psi = lib.to_device(psi0)
+    ch.device_operators()
+
+    def step():
+        mg.evolve_device(ch, grid, n_int, d_psi, check=False, order=2)
+
+    step()
+    lib.profile_read(reset=True)
+    lib.profile_enable(True)
+    ms = time_steps(torch, step, 1, lambda: None, 1)
+    lib.profile_enable(False)
+    prof = lib.profile_read(reset=True)
+    per = sum(ms) / len(ms)
+    n = 1 << L
+    tay = prof.get("zgemm_taylor")
+    fl = 17 * 8 * n**3
+    ach = fl * n_int / (tay[0] * 1e-3) / 1e12 if tay else None
+    return {"workload": f"config 5: Magnus 12-spin Heisenberg chain (dim 4096), order 2, sample of {n_int} of 4096 "
+                        f"intervals, one GPU",
+            "metric": "Magnus intervals/s", "unit": "intervals/s", "value": n_int / (per * 1e-3),
+            "ms_per_interval": per / n_int,
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": fp64.get("dmma"), "unit": "TFLOP/s",
+                         "frac": (ach / fp64["dmma"]) if ach and fp64.get("dmma") else None,
+                         "peak_kind": "FP64 DMMA (mma.sync f64) measured live; cuBLAS zgemm "
+                                      f"{fp64.get('cublas_zgemm', 0):.1f} TFLOP/s for reference",
+                         "flops_per_interval": fl, "kernel": "zgemm_taylor",
+                         "traffic": traffic_from_profiles("zgemm_taylor")},
+            "cpu_baseline": {"value": 1.0 / 36.7, "unit": "intervals/s", "cores": 8, "kind": "port",
+                             "sample": "SURVEY.md §8(d) measurement (one _expm_minus_i at N=4096 = 36.7 s, 8-core "
+                                       "OpenBLAS); not re-timed here (42 h full run)"}}
+
+
+# --------------------------------------------------------------- reference --
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU algorithm (oracle port of
+    effham.magnus.evolve + the 2nd-order restatement) on the host cores, the
+    headline config's metric, bounded sample per step; rank 0 only."""
+    if rank != 0:
+        return
+    from concurrent.futures import ProcessPoolExecutor
+
+    from paper_2411_09982_b200 import models as eff_models
+
+    cores = os.cpu_count() or 1
+    chunk = 20000
+    per_step = chunk * cores
+    ex = ProcessPoolExecutor(max_workers=cores)
+    list(ex.map(_ref_chunk, [200] * cores))  # spawn + import outside the timing
+
+    def one_step():
+        t0 = time.perf_counter()
+        list(ex.map(_ref_chunk, [chunk] * cores))
+        return time.perf_counter() - t0
+
+    for _ in range(max(1, args.warmup)):
+        one_step()
+    ts = [one_step() for _ in range(args.steps)]
+    ex.shutdown()
+    per = sum(ts) / len(ts)
+    value = per_step / per
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "intervals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
+            "config": {"workload": "config 2: Magnus driven 3-level transmon, order 2, 1e5 intervals "
+                                   "(CPU: bounded sample per step)", "order": 2, "dim": 3, "sub": SUB},
+            "cpu_baseline": {"value": value, "unit": "intervals/s", "cores": cores, "kind": "port",
+                             "sample": f"{cores} processes x {chunk} intervals per step (oracle/magnus_oracle.evolve,"
+                                       f" numpy restatement of effham.magnus.evolve + 2nd-order term)"},
+            "e2e": {"value": value, "unit": "intervals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _ref_chunk(n_int):
+    sys.path.insert(0, str(ROOT))
+    from paper_2411_09982_b200 import models as eff_models
+
+    return cpu_magnus_sample(eff_models, n_int)[0]
+
+
+# -------------------------------------------------------------------- main --
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--secondary", default="all")
+    ap.add_argument("--npad4096-rotations", type=int, default=0, help="0 = run to convergence")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2411_09982_b200 as eff
+    from paper_2411_09982_b200 import _lib as lib
+
+    lib.load(build_if_missing=False)
+    hbm_peak, hbm_src = measured_peaks()
+    fp64 = fp64_peaks(torch, lib)
+    head = run_headline(torch, eff, lib, args, world, rank, local)
+
+    secondary = []
+    if rank == 0 and world == 1 and args.secondary != "none":
+        want = {"npad60", "npad4096", "sweep", "magnus4096"} if args.secondary == "all" else set(
+            args.secondary.split(","))
+        peaks = (hbm_peak, hbm_src)
+        if "npad60" in want:
+            secondary.append(sec_npad60(torch, eff, lib, args, peaks))
+        if "npad4096" in want:
+            secondary.append(sec_npad4096(torch, eff, lib, args, peaks, args.npad4096_rotations or None))
+        if "sweep" in want:
+            secondary.append(sec_sweep(torch, eff, lib, args, peaks))
+        if "magnus4096" in want:
+            secondary.append(sec_magnus4096(torch, eff, lib, args, fp64))
+
+    if rank == 0:
+        cpu_v, cpu_t = cpu_magnus_sample(__import__("paper_2411_09982_b200.models", fromlist=["x"]), 60000)
+        roof = head["roof"]
+        achieved = roof["flops_per_launch"] / (roof["launch_ms"] * 1e-3) / 1e12 if roof else None
+        line = {
+            "metric": METRIC,
+            "value": head["value"],
+            "unit": "intervals/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": head["per_step"],
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64 (complex128)",
+            "data": "synthetic (driven transmon, SURVEY.md §8(d) config 2)",
+            "config": {"workload": "config 2: Magnus time coarse-graining, driven 3-level transmon, 1e5 intervals per "
+                                   "GPU, 2nd order, sub=4 samples/interval, check=False (as experiments.py:369)",
+                       "intervals_total": head["m"], "order": 2, "dim": 3, "controls": 2,
+                       "parallelism": f"interval-sharded x{world}" if world > 1 else "single GPU",
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+            "e2e": {"value": head["e2e"][0], "unit": "intervals/s", "h2d_bytes_per_step": head["e2e"][1],
+                    "d2h_bytes_per_step": head["e2e"][2]},
+            "gpu_launches": head["launches"],
+            "clocks": head["clocks"],
+            "roofline": {"bound": "fp64", "kernel": "magnus_small_k1", "achieved": achieved,
+                         "peak": fp64["dfma"], "unit": "TFLOP/s",
+                         "frac": (achieved / fp64["dfma"]) if achieved else None,
+                         "traffic": traffic_from_profiles("magnus_small_k1"),
+                         "peak_kind": "FP64 FMA pipe, measured live by bench.py (DFMA probe); MEASURED_PEAKS.json "
+                                      "has no FP64 entry. Per-interval 3x3 expm is FP64-FMA work, not tensor work",
+                         "flops_per_launch": roof["flops_per_launch"] if roof else None,
+                         "kernel_share_of_step": roof["kernel_share_of_step"] if roof else None},
+            "cpu_baseline": {"value": cpu_v, "unit": "intervals/s", "cores": 1, "kind": "port",
+                             "sample": f"60000 intervals of the same configuration ({cpu_t:.1f} s), "
+                                       "oracle/magnus_oracle.evolve order 2"},
+            "fp64_peaks_tflops": fp64,
+            "hbm_peak": {"gbs": hbm_peak, "source": hbm_src},
+            "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

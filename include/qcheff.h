@@ -160,6 +160,34 @@ int qch_unitarity_defect_c128(const void* d_u, int64_t batch, int64_t n, double*
 int qch_zgemm_batched(const void* d_a, const void* d_b, void* d_c, int64_t m, int64_t n, int64_t k,
                       int64_t batch, int64_t stride_a, int64_t stride_b, int64_t stride_c, void* stream);
 
+/* ------------------------------------------------ multi-GPU Magnus ------- */
+
+/* Interval sharding, N <= 4.  Workspace bytes for M local
+ * intervals. */
+int64_t qch_magnus_shard_workspace_bytes(int64_t N, int64_t M);
+/* Local intervals of one rank: coefficients from the local signal slice
+ * (K, S) with grid spacing dt and interval length dt_int, propagators, local
+ * prefix products; writes the block product B = U_last...U_first to d_block
+ * (N,N) — the tensor the ranks all-gather. */
+int qch_magnus_shard_prepare_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                                  const double* d_sig, int64_t S, double dt, double dt_int, int64_t M, int order,
+                                  int check, void* d_work, void* d_block, void* stream);
+/* psi_start = B_{rank-1} ... B_0 psi0 from the gathered blocks (world, N, N). */
+int qch_magnus_apply_prefix_c128(const void* d_blocks, int64_t N, int64_t rank, const void* d_psi0,
+                                 void* d_psi_start, void* stream);
+/* Local trajectory (M+1, N) from psi_start; NormDrift / NonFinite checks. */
+int qch_magnus_shard_finish_c128(int64_t N, int64_t M, void* d_work, const void* d_psi_start, void* d_traj,
+                                 int check, int64_t* bad_index, void* stream);
+
+/* ------------------------------------------------ measurement ------------ */
+
+/* FP64 peak probes: kind 0 = DFMA pipe, kind 1 = DMMA (mma.sync f64).
+ * *flops receives the launch's flop count (caller times it). */
+int qch_peak_kernel(int kind, int blocks, int iters, double* d_sink, double* flops, void* stream);
+/* CUDA-event timing of the hot kernels on their launching stream. */
+void qch_profile_enable(int on);
+int qch_profile_read(double* total_ms, int64_t* counts, char* names_buf, int64_t buf_len, int cap, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,17 @@ PROTOTYPES = {
         [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int, c_void_p,
          c_void_p, c_void_p, c_int, P_int64, c_void_p],
     ),
+    "qch_magnus_shard_workspace_bytes": (c_int64, [c_int64, c_int64]),
+    "qch_magnus_shard_prepare_c128": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int, c_int,
+         c_void_p, c_void_p, c_void_p],
+    ),
+    "qch_magnus_apply_prefix_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
+    "qch_magnus_shard_finish_c128": (c_int, [c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int, P_int64, c_void_p]),
+    "qch_peak_kernel": (c_int, [c_int, c_int, c_int, c_void_p, ctypes.POINTER(c_double), c_void_p]),
+    "qch_profile_enable": (None, [c_int]),
+    "qch_profile_read": (c_int, [c_void_p, c_void_p, ctypes.c_char_p, c_int64, c_int, c_int]),
     "qch_zgemm_batched": (
         c_int,
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p],
@@ -129,6 +140,23 @@ def call(name: str, *args) -> None:
 
 def launch_count() -> int:
     return int(load().qch_launch_count())
+
+
+def profile_enable(on: bool) -> None:
+    load().qch_profile_enable(1 if on else 0)
+
+
+def profile_read(reset: bool = True) -> dict:
+    """{kernel name: (total_ms, launches)} recorded since the last reset."""
+    lib = load()
+    cap = 64
+    tot = (c_double * cap)()
+    cnt = (c_int64 * cap)()
+    buf = ctypes.create_string_buffer(8192)
+    k = lib.qch_profile_read(ctypes.cast(tot, c_void_p), ctypes.cast(cnt, c_void_p), buf, len(buf), cap,
+                             1 if reset else 0)
+    names = buf.raw.split(b"\0")
+    return {names[i].decode(): (float(tot[i]), int(cnt[i])) for i in range(min(k, cap))}
 
 
 # -- device plumbing (torch owns memory and streams) ---------------------------

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kScanThreads) magnus_small_k1(SmallArgs g) {
 
 // exclusive scan of block aggregates: E_0 = I, E_b = A_{b-1} ... A_0 (in place)
 template <int N>
-__global__ void __launch_bounds__(1024) scan_aggregates_kernel(double2* agg, int64_t nb) {
+__global__ void __launch_bounds__(1024) scan_aggregates_kernel(double2* agg, int64_t nb, double2* total) {
   extern __shared__ __align__(16) double2 ssm[];
   Mat<N> carry = mat_eye<N>();
   for (int64_t base = 0; base < nb; base += blockDim.x) {
@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(1024) scan_aggregates_kernel(double2* agg, int
     if (b < nb) st_mat<N>(agg + b * N * N, e);
     carry = mat_mul<N>(last, carry);
   }
+  if (total != nullptr && threadIdx.x == 0) st_mat<N>(total, carry);
 }
 
 template <int N>
@@ -857,24 +858,40 @@ extern "C" int qch_validate_unitary_batch_c128(const void* d_u, int64_t batch, i
 }
 
 template <int N>
-static int evolve_small(const SmallArgs& base, int64_t M, const double2* psi0, double2* traj,
-                        unsigned long long* bad_norm, cudaStream_t st) {
+static int small_prepare(const SmallArgs& base, int64_t M, double2* total, cudaStream_t st) {
   const int K = base.ca.K;
   const int ncomm = K + K * (K - 1) / 2;
   const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
   size_t smem1 = sizeof(double2) * ((size_t)(1 + K + ncomm) * N * N + (size_t)kScanThreads * N * N);
   QCH_CUDA(cudaFuncSetAttribute(magnus_small_k1<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+  void* pr = prof_begin("magnus_small_k1", st);
   magnus_small_k1<N><<<(unsigned)nb, kScanThreads, smem1, st>>>(base);
+  prof_end(pr, st);
   QCH_LAUNCH_CHECK("magnus_small_k1");
   int t2 = (int)std::min<int64_t>(1024, std::max<int64_t>(32, ((nb + 31) / 32) * 32));
   size_t smem2 = sizeof(double2) * (size_t)t2 * N * N;
   QCH_CUDA(cudaFuncSetAttribute(scan_aggregates_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-  scan_aggregates_kernel<N><<<1, t2, smem2, st>>>(base.agg, nb);
+  scan_aggregates_kernel<N><<<1, t2, smem2, st>>>(base.agg, nb, total);
   QCH_LAUNCH_CHECK("scan_aggregates_kernel");
+  note_launch(2);
+  return QCH_OK;
+}
+
+template <int N>
+static int small_finish(const SmallArgs& base, int64_t M, const double2* psi0, double2* traj,
+                        unsigned long long* bad_norm, cudaStream_t st) {
+  const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
   magnus_small_k3<N><<<(unsigned)nb, kScanThreads, 0, st>>>(base.qloc, base.agg, psi0, M, traj, bad_norm);
   QCH_LAUNCH_CHECK("magnus_small_k3");
-  note_launch(3);
+  note_launch(1);
   return QCH_OK;
+}
+
+template <int N>
+static int evolve_small(const SmallArgs& base, int64_t M, const double2* psi0, double2* traj,
+                        unsigned long long* bad_norm, cudaStream_t st) {
+  if (int rc = small_prepare<N>(base, M, nullptr, st)) return rc;
+  return small_finish<N>(base, M, psi0, traj, bad_norm, st);
 }
 
 extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, int64_t K, int64_t N, const double* d_sig,
@@ -993,6 +1010,107 @@ extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, int64_
   }
   if (check) {
     if (int rc = report_bad(bad_u, bad_index, QCH_ERR_NONFINITE, "propagator not unitary", st)) return rc;
+  }
+  return report_bad(bad_norm, bad_index, QCH_ERR_NORM_DRIFT, "state norm drifted", st);
+}
+
+// ---------------------------------------------------------------------------
+// Interval sharding across GPUs: each rank owns a
+// contiguous block of intervals, computes its block product B_r, the ranks
+// all-gather the B's (NCCL), each rank applies B_{r-1}...B_0 to psi0 and
+// finishes its local trajectory.  Workspace layout (caller-allocated,
+// qch_magnus_shard_workspace_bytes): qloc (M,N,N) | agg (nb,N,N) | flags.
+extern "C" int64_t qch_magnus_shard_workspace_bytes(int64_t N, int64_t M) {
+  const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
+  return (int64_t)sizeof(double2) * N * N * (M + nb) + 64;
+}
+
+static SmallArgs shard_args(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                            const double* d_sig, int64_t S, double dt, double dt_int, int64_t M, int order, int check,
+                            void* d_work) {
+  SmallArgs g;
+  g.ca = CoefArgs{d_sig, (int)K, S, M, (int)((S - 1) / M), dt};
+  g.h0 = (const double2*)d_h0;
+  g.hk = (const double2*)d_hk;
+  g.comm = (const double2*)d_comm;
+  g.order = order;
+  g.dt_int = dt_int;
+  g.check = check;
+  g.props = nullptr;
+  g.qloc = (double2*)d_work;
+  const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
+  g.agg = g.qloc + N * N * M;
+  g.bad = (unsigned long long*)(g.agg + N * N * nb);
+  return g;
+}
+
+extern "C" int qch_magnus_shard_prepare_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K,
+                                             int64_t N, const double* d_sig, int64_t S, double dt, double dt_int,
+                                             int64_t M, int order, int check, void* d_work, void* d_block,
+                                             void* stream) {
+  if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "sharded Magnus prepare: N <= 4");
+  if (M < 1 || (S - 1) % M) return fail(QCH_ERR_GRID, "interval count does not divide the local sample steps");
+  cudaStream_t st = (cudaStream_t)stream;
+  SmallArgs g = shard_args(d_h0, d_hk, d_comm, K, N, d_sig, S, dt, dt_int, M, order, check, d_work);
+  QCH_CUDA(cudaMemsetAsync(g.bad, 0xff, 2 * sizeof(unsigned long long), st));
+  switch (N) {
+    case 1: return small_prepare<1>(g, M, (double2*)d_block, st);
+    case 2: return small_prepare<2>(g, M, (double2*)d_block, st);
+    case 3: return small_prepare<3>(g, M, (double2*)d_block, st);
+    default: return small_prepare<4>(g, M, (double2*)d_block, st);
+  }
+}
+
+// psi_start = B_{rank-1} ... B_0 psi0   (blocks: (world, N, N))
+__global__ void apply_prefix_kernel(const double2* __restrict__ blocks, int n, int rank, const double2* __restrict__ psi0,
+                                    double2* __restrict__ out) {
+  extern __shared__ __align__(16) double2 pv[];
+  double2* cur = pv;
+  double2* nxt = pv + n;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) cur[r] = psi0[r];
+  __syncthreads();
+  for (int b = 0; b < rank; ++b) {
+    const double2* m = blocks + (int64_t)b * n * n;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      cplx acc = mkc(0, 0);
+      for (int c = 0; c < n; ++c) acc = cadd(acc, np_cmul(d2c(m[(int64_t)r * n + c]), d2c(cur[c])));
+      nxt[r] = c2d(acc);
+    }
+    __syncthreads();
+    double2* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  for (int r = threadIdx.x; r < n; r += blockDim.x) out[r] = cur[r];
+}
+
+extern "C" int qch_magnus_apply_prefix_c128(const void* d_blocks, int64_t N, int64_t rank, const void* d_psi0,
+                                            void* d_psi_start, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  apply_prefix_kernel<<<1, 128, sizeof(double2) * 2 * N, st>>>((const double2*)d_blocks, (int)N, (int)rank,
+                                                              (const double2*)d_psi0, (double2*)d_psi_start);
+  QCH_LAUNCH_CHECK("apply_prefix_kernel");
+  note_launch(1);
+  return QCH_OK;
+}
+
+extern "C" int qch_magnus_shard_finish_c128(int64_t N, int64_t M, void* d_work, const void* d_psi_start,
+                                            void* d_traj, int check, int64_t* bad_index, void* stream) {
+  if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "sharded Magnus finish: N <= 4");
+  cudaStream_t st = (cudaStream_t)stream;
+  SmallArgs g = shard_args(nullptr, nullptr, nullptr, 0, N, nullptr, M + 1, 0.0, 0.0, M, 1, check, d_work);
+  unsigned long long* bad_u = g.bad;
+  unsigned long long* bad_norm = g.bad + 1;
+  int rc;
+  switch (N) {
+    case 1: rc = small_finish<1>(g, M, (const double2*)d_psi_start, (double2*)d_traj, bad_norm, st); break;
+    case 2: rc = small_finish<2>(g, M, (const double2*)d_psi_start, (double2*)d_traj, bad_norm, st); break;
+    case 3: rc = small_finish<3>(g, M, (const double2*)d_psi_start, (double2*)d_traj, bad_norm, st); break;
+    default: rc = small_finish<4>(g, M, (const double2*)d_psi_start, (double2*)d_traj, bad_norm, st); break;
+  }
+  if (rc) return rc;
+  if (check) {
+    if (int r2 = report_bad(bad_u, bad_index, QCH_ERR_NONFINITE, "propagator not unitary", st)) return r2;
   }
   return report_bad(bad_norm, bad_index, QCH_ERR_NORM_DRIFT, "state norm drifted", st);
 }

@@ -768,7 +768,9 @@ int npad_launch(NpadJob* d_jobs, int njobs, NpadCommon cm, int pref_threads, cud
     return fail(QCH_ERR_UNSUPPORTED, "npad: dimension " + std::to_string(cm.n) + " needs " + std::to_string(smem) +
                                          " B of shared memory (max " + std::to_string(max_smem_optin()) + ")");
   QCH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* pr = prof_begin("npad_run_kernel", st);
   k<<<njobs, threads, smem, st>>>(d_jobs, cm);
+  prof_end(pr, st);
   QCH_LAUNCH_CHECK("npad_run_kernel");
   note_launch(1);
   return QCH_OK;

@@ -31,6 +31,8 @@ int cuda_status(cudaError_t e, const char* what);
 
 // number of SMs of the current device (cached)
 void note_launch(int k);
+void* prof_begin(const char* name, cudaStream_t st);
+void prof_end(void* h, cudaStream_t st);
 int sm_count();
 int max_smem_optin();
 

@@ -228,7 +228,9 @@ static int zgemm_launch(const ZgemmArgs& g, int64_t batch, cudaStream_t st) {
     if (h.o) h.o += done * g.sc;
     if (h.acc) h.acc += done;
     dim3 grid((g.n + BN - 1) / BN, (g.m + BM - 1) / BM, (unsigned)nb);
+    void* pr = prof_begin(MODE == ZG_TAYLOR ? "zgemm_taylor" : (MODE == ZG_STORE ? "zgemm" : "zgemm_defect"), st);
     zgemm_kernel<MODE, BH><<<grid, 128, smem, st>>>(h);
+    prof_end(pr, st);
     QCH_LAUNCH_CHECK("zgemm_kernel");
     note_launch(1);
     done += nb;
