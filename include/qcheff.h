@@ -141,16 +141,27 @@ int qch_validate_unitary_batch_c128(const void* d_u, int64_t batch, int64_t n, i
 /* evolve (magnus.py:214-267), whole pipeline on the device: coefficients,
  * assembly (order 1|2), propagators, ordered product and trajectory.
  * d_h0 (N,N), d_hk (K,N,N), d_sig (K,S), d_psi0 (N).  d_traj: (M+1, N).
+ * d_comm (nullable): precomputed qch_magnus_commutators_c128 output for
+ * order 2 (computed internally when NULL).
  * d_props (nullable): (M, N, N) propagators.  check: validate propagators.
  * NormDrift (magnus.py:270-273) -> QCH_ERR_NORM_DRIFT with the interval in
  * *bad_index. */
-int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, int64_t K, int64_t N, const double* d_sig,
-                           int64_t S, double t_start, double t_end, int64_t M, int order, const void* d_psi0,
-                           void* d_traj, void* d_props, int check, int64_t* bad_index, void* stream);
+int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                           const double* d_sig, int64_t S, double t_start, double t_end, int64_t M, int order,
+                           const void* d_psi0, void* d_traj, void* d_props, int check, int64_t* bad_index,
+                           void* stream);
 
 /* ||U_b U_b^dag - I||_F for a batch (DMMA GEMM with a fused reduction):
  * the unitarity audit of npad.py:257 and expm.py:35-38.  d_defect: (batch). */
 int qch_unitarity_defect_c128(const void* d_u, int64_t batch, int64_t n, double* d_defect, void* stream);
+
+/* Asynchronous evolve for N <= 4 (pipelined throughput): no host sync; the
+ * two status words (first non-unitary interval, first norm-drift interval;
+ * ~0 = none) are copied to d_flags (device, 2 x uint64) for a later check. */
+int qch_magnus_evolve_async_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                                 const double* d_sig, int64_t S, double t_start, double t_end, int64_t M, int order,
+                                 const void* d_psi0, void* d_traj, void* d_props, int check, void* d_flags,
+                                 void* stream);
 
 /* ------------------------------------------------------------ GEMM ------- */
 

@@ -57,8 +57,8 @@ PROTOTYPES = {
     "qch_unitarity_defect_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "qch_magnus_evolve_c128": (
         c_int,
-        [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int, c_void_p,
-         c_void_p, c_void_p, c_int, P_int64, c_void_p],
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int,
+         c_void_p, c_void_p, c_void_p, c_int, P_int64, c_void_p],
     ),
     "qch_magnus_shard_workspace_bytes": (c_int64, [c_int64, c_int64]),
     "qch_magnus_shard_prepare_c128": (
@@ -71,6 +71,11 @@ PROTOTYPES = {
     "qch_peak_kernel": (c_int, [c_int, c_int, c_int, c_void_p, ctypes.POINTER(c_double), c_void_p]),
     "qch_profile_enable": (None, [c_int]),
     "qch_profile_read": (c_int, [c_void_p, c_void_p, ctypes.c_char_p, c_int64, c_int, c_int]),
+    "qch_magnus_evolve_async_c128": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int,
+         c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p],
+    ),
     "qch_zgemm_batched": (
         c_int,
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p],

@@ -12,6 +12,7 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 int cuda_status(cudaError_t e, const char* what) {
+  (void)cudaGetLastError();  // clear the runtime's sticky last-error slot for the next call
   g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
   return QCH_ERR_CUDA;
 }
@@ -22,6 +23,21 @@ int sm_count() {
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
   return v > 0 ? v : 148;
 }
+// Keep the stream-ordered pool's memory mapped between calls: with the default
+// release threshold (0) every synchronising call hands the workspace back to
+// the OS and the next cudaMallocAsync re-maps it (hundreds of microseconds).
+void ensure_pool() {
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 int max_smem_optin() {
   int dev = 0, v = 227 * 1024;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);

@@ -87,6 +87,40 @@ __device__ __forceinline__ void interval_coeffs(const CoefArgs& a, int64_t n, in
     }
 }
 
+// the same coefficients one at a time (no local arrays in the hot kernel)
+__device__ __forceinline__ double coef1(const CoefArgs& a, int64_t n, int k) {
+  const double* u = a.sig + (int64_t)k * a.S + n * a.sub;
+  auto f = [&](int q) { return QADD(u[q], u[q + 1]); };
+  return QMUL(QDIV(a.dt, 2.0), np_pairwise(f, a.sub));
+}
+__device__ __forceinline__ double coef_alpha(const CoefArgs& a, int64_t n, int k) {
+  const double h = a.dt, h2 = QDIV(h, 2.0), hh6 = QDIV(QMUL(h, h), 6.0);
+  const double* u = a.sig + (int64_t)k * a.S + n * a.sub;
+  double run = 0.0, acc = 0.0, lin = 0.0;
+  for (int q = 0; q < a.sub; ++q) {
+    double tau = QMUL(h2, QADD(u[q], u[q + 1]));
+    acc = QADD(acc, QSUB(QMUL(h, run), QMUL(QMUL((double)q, h), tau)));
+    lin = QADD(lin, QSUB(u[q + 1], u[q]));
+    run = QADD(run, tau);
+  }
+  return QSUB(acc, QMUL(hh6, lin));
+}
+__device__ __forceinline__ double coef_beta(const CoefArgs& a, int64_t n, int k, int l) {
+  const double h = a.dt, h2 = QDIV(h, 2.0), hh6 = QDIV(QMUL(h, h), 6.0);
+  const double* uk = a.sig + (int64_t)k * a.S + n * a.sub;
+  const double* ul = a.sig + (int64_t)l * a.S + n * a.sub;
+  double sk = 0.0, sl = 0.0, acc = 0.0, cr = 0.0;
+  for (int q = 0; q < a.sub; ++q) {
+    double tk = QMUL(h2, QADD(uk[q], uk[q + 1]));
+    double tl = QMUL(h2, QADD(ul[q], ul[q + 1]));
+    acc = QADD(acc, QSUB(QMUL(tk, sl), QMUL(tl, sk)));
+    cr = QADD(cr, QSUB(QMUL(uk[q], ul[q + 1]), QMUL(ul[q], uk[q + 1])));
+    sk = QADD(sk, tk);
+    sl = QADD(sl, tl);
+  }
+  return QSUB(acc, QMUL(hh6, cr));
+}
+
 constexpr int kMaxK = 8;
 
 __global__ void coeff_kernel(CoefArgs a, int order, double* __restrict__ c1, double* __restrict__ c2) {
@@ -236,10 +270,10 @@ struct SmallArgs {
   int order;
   double dt_int;
   int check;
-  double2* props;   // (M,N,N) or nullptr
-  double2* qloc;    // (M,N,N) block-local prefixes
-  double2* agg;     // (nblocks, N, N)
-  unsigned long long* bad;  // [0] first non-unitary interval
+  double2* ubuf;    // (M,N,N) propagators (the caller's props buffer when requested)
+  double2* runp;    // (nruns,N,N) block-exclusive prefix of each run
+  double2* agg;     // (nblocks, N, N) block aggregates -> exclusive block prefixes
+  unsigned long long* bad;  // [0] first non-unitary interval, [1] first norm drift
 };
 
 template <int N>
@@ -257,10 +291,84 @@ __device__ __forceinline__ void st_mat(double2* p, const Mat<N>& m) {
     for (int c = 0; c < N; ++c) p[r * N + c] = c2d(m.v[r][c]);
 }
 
-constexpr int kScanThreads = 256;
+// complex matrix product with FMA accumulation (the BLAS-like rounding of the
+// reference's `term @ a`, expm.py:67; 4 FMA per complex MAC)
+template <int N>
+__device__ __forceinline__ Mat<N> mat_mul_fma(const Mat<N>& a, const Mat<N>& b) {
+  Mat<N> o;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      double re = a.v[r][0].re * b.v[0][c].re;
+      double im = a.v[r][0].re * b.v[0][c].im;
+      re = fma(-a.v[r][0].im, b.v[0][c].im, re);
+      im = fma(a.v[r][0].im, b.v[0][c].re, im);
+#pragma unroll
+      for (int k = 1; k < N; ++k) {
+        re = fma(a.v[r][k].re, b.v[k][c].re, re);
+        im = fma(a.v[r][k].re, b.v[k][c].im, im);
+        re = fma(-a.v[r][k].im, b.v[k][c].im, re);
+        im = fma(a.v[r][k].im, b.v[k][c].re, im);
+      }
+      o.v[r][c] = mkc(re, im);
+    }
+  return o;
+}
+
+// _expm_minus_i (expm.py:56-71) in registers, FMA products; the k = 1 term
+// (I @ a / 1 = a, exact) is taken directly.
+template <int N>
+__device__ __forceinline__ Mat<N> expm_minus_i_fast(const Mat<N>& hb) {
+  Mat<N> a;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) a.v[r][c] = mkc(hb.v[r][c].im, -hb.v[r][c].re);
+  double norm = 0.0;
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    double rs = 0.0;
+#pragma unroll
+    for (int c = 0; c < N; ++c) rs = QADD(rs, np_cabs(a.v[r][c]));
+    norm = fmax(norm, rs);
+  }
+  int s = 0;
+  if (norm > kScaleTarget) {
+    s = (int)ceil(log2(QDIV(norm, kScaleTarget)));
+    const double scl = ldexp(1.0, -s);
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) a.v[r][c] = mkc(a.v[r][c].re * scl, a.v[r][c].im * scl);
+  }
+  Mat<N> out, term = a;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) out.v[r][c] = mkc((r == c ? 1.0 : 0.0) + a.v[r][c].re, a.v[r][c].im);
+#pragma unroll 1
+  for (int k = 2; k <= kTaylorOrder; ++k) {
+    term = mat_mul_fma<N>(term, a);
+    const double inv = 1.0 / (double)k;
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        term.v[r][c] = mkc(term.v[r][c].re * inv, term.v[r][c].im * inv);
+        out.v[r][c] = mkc(out.v[r][c].re + term.v[r][c].re, out.v[r][c].im + term.v[r][c].im);
+      }
+  }
+#pragma unroll 1
+  for (int q = 0; q < s; ++q) out = mat_mul_fma<N>(out, out);
+  return out;
+}
+
+constexpr int kScanThreads = 128;
+constexpr int kRun = 4;  // intervals per thread in the ordered-product scan
 
 // Hillis-Steele inclusive scan of matrix products in thread order, later
-// intervals multiplied on the LEFT: P_t = U_t ... U_0.
+// entries multiplied on the LEFT: P_t = A_t ... A_0.
 template <int N>
 __device__ Mat<N> block_scan(Mat<N> p, double2* sm) {
   const int t = threadIdx.x;
@@ -270,68 +378,107 @@ __device__ Mat<N> block_scan(Mat<N> p, double2* sm) {
     if (t >= d) {
       Mat<N> q;
       ld_mat<N>(q, sm + (t - d) * N * N);
-      p = mat_mul<N>(p, q);
+      p = mat_mul_fma<N>(p, q);
     }
     __syncthreads();
   }
   return p;
 }
 
+// per-interval propagators: coefficients + assembly (numpy order) + expm
 template <int N>
-__global__ void __launch_bounds__(kScanThreads) magnus_small_k1(SmallArgs g) {
+__global__ void __launch_bounds__(128) magnus_prop_kernel(SmallArgs g) {
   extern __shared__ __align__(16) double2 ssm[];
   const int K = g.ca.K;
   const int ncomm = K + K * (K - 1) / 2;
-  double2* s_ops = ssm;                                // H0, Hk..., comm...
-  double2* s_scan = ssm + (1 + K + ncomm) * N * N;     // kScanThreads * N*N
+  double2* s_ops = ssm;  // H0, Hk..., comm...
   for (int q = threadIdx.x; q < N * N; q += blockDim.x) s_ops[q] = g.h0[q];
   for (int q = threadIdx.x; q < K * N * N; q += blockDim.x) s_ops[N * N + q] = g.hk[q];
   if (g.order >= 2)
     for (int q = threadIdx.x; q < ncomm * N * N; q += blockDim.x) s_ops[(1 + K) * N * N + q] = g.comm[q];
   __syncthreads();
-
   const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  Mat<N> u = mat_eye<N>();
-  if (n < g.ca.M) {
-    double c1[kMaxK], c2[kMaxK + kMaxK * (kMaxK - 1) / 2];
-    interval_coeffs(g.ca, n, g.order, c1, c2);
-    Mat<N> hb;
-    // h = dt*drift; h = h + w*ctrl  (magnus.py:186-188)
+  if (n >= g.ca.M) return;
+  Mat<N> hb;
+  // h = dt*drift; h = h + w*ctrl  (magnus.py:186-188)
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) hb.v[r][c] = np_rmul(g.dt_int, d2c(s_ops[r * N + c]));
+  for (int k = 0; k < K; ++k) {
+    const double w = coef1(g.ca, n, k);
 #pragma unroll
     for (int r = 0; r < N; ++r)
 #pragma unroll
-      for (int c = 0; c < N; ++c) hb.v[r][c] = np_rmul(g.dt_int, d2c(s_ops[r * N + c]));
-    for (int k = 0; k < K; ++k)
+      for (int c = 0; c < N; ++c) hb.v[r][c] = cadd(hb.v[r][c], np_rmul(w, d2c(s_ops[(1 + k) * N * N + r * N + c])));
+  }
+  if (g.order >= 2) {
+    Mat<N> x;
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) x.v[r][c] = mkc(0, 0);
+    int q = 0;
+    for (int k = 0; k < K; ++k, ++q) {
+      const double w = coef_alpha(g.ca, n, k);
 #pragma unroll
       for (int r = 0; r < N; ++r)
 #pragma unroll
         for (int c = 0; c < N; ++c)
-          hb.v[r][c] = cadd(hb.v[r][c], np_rmul(c1[k], d2c(s_ops[(1 + k) * N * N + r * N + c])));
-    if (g.order >= 2) {
-      Mat<N> x;
-#pragma unroll
-      for (int r = 0; r < N; ++r)
-#pragma unroll
-        for (int c = 0; c < N; ++c) x.v[r][c] = mkc(0, 0);
-      for (int q = 0; q < ncomm; ++q)
+          x.v[r][c] = cadd(x.v[r][c], np_rmul(w, d2c(s_ops[(1 + K + q) * N * N + r * N + c])));
+    }
+    for (int k = 0; k < K; ++k)
+      for (int l = k + 1; l < K; ++l, ++q) {
+        const double w = coef_beta(g.ca, n, k, l);
 #pragma unroll
         for (int r = 0; r < N; ++r)
 #pragma unroll
           for (int c = 0; c < N; ++c)
-            x.v[r][c] = cadd(x.v[r][c], np_rmul(c2[q], d2c(s_ops[(1 + K + q) * N * N + r * N + c])));
-      // hbar = hbar1 + (-0.5j) * X
+            x.v[r][c] = cadd(x.v[r][c], np_rmul(w, d2c(s_ops[(1 + K + q) * N * N + r * N + c])));
+      }
+    // hbar = hbar1 + (-0.5j) * X
 #pragma unroll
-      for (int r = 0; r < N; ++r)
+    for (int r = 0; r < N; ++r)
 #pragma unroll
-        for (int c = 0; c < N; ++c) hb.v[r][c] = cadd(hb.v[r][c], np_cmul(mkc(0.0, -0.5), x.v[r][c]));
-    }
-    u = expm_minus_i_reg<N>(hb);
-    if (g.check && !validate_reg<N>(u)) atomicMin(g.bad, (unsigned long long)n);
-    if (g.props) st_mat<N>(g.props + n * N * N, u);
+      for (int c = 0; c < N; ++c) hb.v[r][c] = cadd(hb.v[r][c], np_cmul(mkc(0.0, -0.5), x.v[r][c]));
   }
-  Mat<N> p = block_scan<N>(u, s_scan);
-  if (n < g.ca.M) st_mat<N>(g.qloc + n * N * N, p);
-  if (threadIdx.x == blockDim.x - 1) st_mat<N>(g.agg + (int64_t)blockIdx.x * N * N, p);
+  const Mat<N> u = expm_minus_i_fast<N>(hb);
+  if (g.check && !validate_reg<N>(u)) atomicMin(g.bad, (unsigned long long)n);
+  st_mat<N>(g.ubuf + n * N * N, u);
+}
+
+// run products (kRun intervals per thread), block scan over runs
+template <int N>
+__global__ void __launch_bounds__(kScanThreads) magnus_runs_kernel(const double2* __restrict__ ubuf, int64_t M,
+                                                                  double2* __restrict__ runp,
+                                                                  double2* __restrict__ agg) {
+  extern __shared__ __align__(16) double2 ssm[];
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t first = r * kRun;
+  Mat<N> a = mat_eye<N>();
+  if (first < M) {
+    ld_mat<N>(a, ubuf + first * N * N);
+    for (int k = 1; k < kRun && first + k < M; ++k) {
+      Mat<N> u;
+      ld_mat<N>(u, ubuf + (first + k) * N * N);
+      a = mat_mul_fma<N>(u, a);
+    }
+  }
+  Mat<N> p = block_scan<N>(a, ssm);
+  // exclusive within the block: P_{t-1}
+  st_mat<N>(ssm + threadIdx.x * N * N, p);
+  __syncthreads();
+  const int64_t nruns = (M + kRun - 1) / kRun;
+  if (r < nruns) {
+    if (threadIdx.x == 0) {
+      st_mat<N>(runp + r * N * N, mat_eye<N>());
+    } else {
+      Mat<N> e;
+      ld_mat<N>(e, ssm + (threadIdx.x - 1) * N * N);
+      st_mat<N>(runp + r * N * N, e);
+    }
+  }
+  if (threadIdx.x == blockDim.x - 1) st_mat<N>(agg + (int64_t)blockIdx.x * N * N, p);
 }
 
 // exclusive scan of block aggregates: E_0 = I, E_b = A_{b-1} ... A_0 (in place)
@@ -351,55 +498,78 @@ __global__ void __launch_bounds__(1024) scan_aggregates_kernel(double2* agg, int
     if (threadIdx.x > 0) {
       Mat<N> q;
       ld_mat<N>(q, ssm + (threadIdx.x - 1) * N * N);
-      e = mat_mul<N>(q, carry);
+      e = mat_mul_fma<N>(q, carry);
     }
     Mat<N> last;
     ld_mat<N>(last, ssm + (blockDim.x - 1) * N * N);
     __syncthreads();
     if (b < nb) st_mat<N>(agg + b * N * N, e);
-    carry = mat_mul<N>(last, carry);
+    carry = mat_mul_fma<N>(last, carry);
   }
   if (total != nullptr && threadIdx.x == 0) st_mat<N>(total, carry);
 }
 
+// trajectory: psi at the start of run r = runp[r] * E_block * psi0, then the
+// run's intervals sequentially (psi <- U_n psi, magnus.py:249-252)
 template <int N>
-__global__ void __launch_bounds__(kScanThreads) magnus_small_k3(const double2* __restrict__ qloc,
-                                                                const double2* __restrict__ excl,
-                                                                const double2* __restrict__ psi0, int64_t M,
-                                                                double2* __restrict__ traj,
-                                                                unsigned long long* bad_norm) {
-  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kScanThreads) magnus_traj_kernel(const double2* __restrict__ ubuf,
+                                                                  const double2* __restrict__ runp,
+                                                                  const double2* __restrict__ excl,
+                                                                  const double2* __restrict__ psi0, int64_t M,
+                                                                  double2* __restrict__ traj,
+                                                                  unsigned long long* bad_norm) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   cplx p0[N];
 #pragma unroll
-  for (int r = 0; r < N; ++r) p0[r] = d2c(psi0[r]);
-  if (n == 0) {
+  for (int q = 0; q < N; ++q) p0[q] = d2c(psi0[q]);
+  if (r == 0) {
 #pragma unroll
-    for (int r = 0; r < N; ++r) traj[r] = c2d(p0[r]);
+    for (int q = 0; q < N; ++q) traj[q] = c2d(p0[q]);
   }
-  if (n >= M) return;
+  const int64_t first = r * kRun;
+  if (first >= M) return;
   Mat<N> e, q;
   ld_mat<N>(e, excl + (int64_t)blockIdx.x * N * N);
-  ld_mat<N>(q, qloc + n * N * N);
-  cplx v[N], w[N];
+  ld_mat<N>(q, runp + r * N * N);
+  Mat<N> pre = mat_mul_fma<N>(q, e);
+  cplx v[N];
 #pragma unroll
-  for (int r = 0; r < N; ++r) {
-    cplx acc = np_cmul(e.v[r][0], p0[0]);
+  for (int a = 0; a < N; ++a) {
+    double re = 0.0, im = 0.0;
 #pragma unroll
-    for (int c = 1; c < N; ++c) acc = cadd(acc, np_cmul(e.v[r][c], p0[c]));
-    v[r] = acc;
+    for (int c = 0; c < N; ++c) {
+      re = fma(pre.v[a][c].re, p0[c].re, re);
+      re = fma(-pre.v[a][c].im, p0[c].im, re);
+      im = fma(pre.v[a][c].re, p0[c].im, im);
+      im = fma(pre.v[a][c].im, p0[c].re, im);
+    }
+    v[a] = mkc(re, im);
   }
-  double nrm2 = 0.0;
+  for (int k = 0; k < kRun && first + k < M; ++k) {
+    Mat<N> u;
+    ld_mat<N>(u, ubuf + (first + k) * N * N);
+    cplx w[N];
+    double nrm2 = 0.0;
 #pragma unroll
-  for (int r = 0; r < N; ++r) {
-    cplx acc = np_cmul(q.v[r][0], v[0]);
+    for (int a = 0; a < N; ++a) {
+      double re = 0.0, im = 0.0;
 #pragma unroll
-    for (int c = 1; c < N; ++c) acc = cadd(acc, np_cmul(q.v[r][c], v[c]));
-    w[r] = acc;
-    nrm2 += acc.re * acc.re + acc.im * acc.im;
+      for (int c = 0; c < N; ++c) {
+        re = fma(u.v[a][c].re, v[c].re, re);
+        re = fma(-u.v[a][c].im, v[c].im, re);
+        im = fma(u.v[a][c].re, v[c].im, im);
+        im = fma(u.v[a][c].im, v[c].re, im);
+      }
+      w[a] = mkc(re, im);
+      nrm2 = fma(re, re, fma(im, im, nrm2));
+    }
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      v[a] = w[a];
+      traj[(first + k + 1) * N + a] = c2d(w[a]);
+    }
+    if (!(fabs(sqrt(nrm2) - 1.0) <= 1e-6)) atomicMin(bad_norm, (unsigned long long)(first + k));  // NORM_DRIFT_TOL
   }
-#pragma unroll
-  for (int r = 0; r < N; ++r) traj[(n + 1) * N + r] = c2d(w[r]);
-  if (!(fabs(sqrt(nrm2) - 1.0) <= 1e-6)) atomicMin(bad_norm, (unsigned long long)n);  // NORM_DRIFT_TOL
 }
 
 // standalone small expm batch (expm_batch for N <= 4)
@@ -668,7 +838,10 @@ struct DevBuf {
   cudaStream_t st;
   void* p = nullptr;
   explicit DevBuf(cudaStream_t s) : st(s) {}
-  cudaError_t alloc(size_t b) { return cudaMallocAsync(&p, std::max<size_t>(b, 16), st); }
+  cudaError_t alloc(size_t b) {
+    ensure_pool();
+    return cudaMallocAsync(&p, std::max<size_t>(b, 16), st);
+  }
   ~DevBuf() {
     if (p) cudaFreeAsync(p, st);
   }
@@ -857,47 +1030,97 @@ extern "C" int qch_validate_unitary_batch_c128(const void* d_u, int64_t batch, i
   return report_bad(bad, bad_index, QCH_ERR_NONFINITE, "propagator not unitary", st);
 }
 
+static int64_t small_nruns(int64_t M) { return (M + kRun - 1) / kRun; }
+static int64_t small_nblocks(int64_t M) { return (small_nruns(M) + kScanThreads - 1) / kScanThreads; }
+
 template <int N>
-static int small_prepare(const SmallArgs& base, int64_t M, double2* total, cudaStream_t st) {
-  const int K = base.ca.K;
+static int small_prepare(const SmallArgs& g, int64_t M, double2* total, cudaStream_t st) {
+  const int K = g.ca.K;
   const int ncomm = K + K * (K - 1) / 2;
-  const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
-  size_t smem1 = sizeof(double2) * ((size_t)(1 + K + ncomm) * N * N + (size_t)kScanThreads * N * N);
-  QCH_CUDA(cudaFuncSetAttribute(magnus_small_k1<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
-  void* pr = prof_begin("magnus_small_k1", st);
-  magnus_small_k1<N><<<(unsigned)nb, kScanThreads, smem1, st>>>(base);
+  const size_t smem1 = sizeof(double2) * (size_t)(1 + K + ncomm) * N * N;
+  void* pr = prof_begin("magnus_prop_kernel", st);
+  magnus_prop_kernel<N><<<(unsigned)((M + 127) / 128), 128, smem1, st>>>(g);
   prof_end(pr, st);
-  QCH_LAUNCH_CHECK("magnus_small_k1");
-  int t2 = (int)std::min<int64_t>(1024, std::max<int64_t>(32, ((nb + 31) / 32) * 32));
-  size_t smem2 = sizeof(double2) * (size_t)t2 * N * N;
-  QCH_CUDA(cudaFuncSetAttribute(scan_aggregates_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-  scan_aggregates_kernel<N><<<1, t2, smem2, st>>>(base.agg, nb, total);
+  QCH_LAUNCH_CHECK("magnus_prop_kernel");
+  const int64_t nb = small_nblocks(M);
+  const size_t smem2 = sizeof(double2) * (size_t)kScanThreads * N * N;
+  static bool attr2 = false;
+  if (!attr2) {
+    QCH_CUDA(cudaFuncSetAttribute(magnus_runs_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    attr2 = true;
+  }
+  void* pr2 = prof_begin("magnus_runs_scan_kernels", st);
+  magnus_runs_kernel<N><<<(unsigned)nb, kScanThreads, smem2, st>>>(g.ubuf, M, g.runp, g.agg);
+  QCH_LAUNCH_CHECK("magnus_runs_kernel");
+  const int tmax = N <= 2 ? 1024 : (N == 3 ? 512 : 256);  // <= 64 KB of scan buffer
+  const int t2 = (int)std::min<int64_t>(tmax, std::max<int64_t>(32, ((nb + 31) / 32) * 32));
+  const size_t smem3 = sizeof(double2) * (size_t)t2 * N * N;
+  static bool attr = false;
+  if (!attr) {
+    QCH_CUDA(cudaFuncSetAttribute(scan_aggregates_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double2) * tmax * N * N)));
+    attr = true;
+  }
+  scan_aggregates_kernel<N><<<1, t2, smem3, st>>>(g.agg, nb, total);
+  prof_end(pr2, st);
   QCH_LAUNCH_CHECK("scan_aggregates_kernel");
-  note_launch(2);
+  note_launch(3);
   return QCH_OK;
 }
 
 template <int N>
-static int small_finish(const SmallArgs& base, int64_t M, const double2* psi0, double2* traj,
-                        unsigned long long* bad_norm, cudaStream_t st) {
-  const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
-  magnus_small_k3<N><<<(unsigned)nb, kScanThreads, 0, st>>>(base.qloc, base.agg, psi0, M, traj, bad_norm);
-  QCH_LAUNCH_CHECK("magnus_small_k3");
+static int small_finish(const SmallArgs& g, int64_t M, const double2* psi0, double2* traj, cudaStream_t st) {
+  const int64_t nb = small_nblocks(M);
+  void* pr = prof_begin("magnus_traj_kernel", st);
+  magnus_traj_kernel<N><<<(unsigned)nb, kScanThreads, 0, st>>>(g.ubuf, g.runp, g.agg, psi0, M, traj, g.bad + 1);
+  prof_end(pr, st);
+  QCH_LAUNCH_CHECK("magnus_traj_kernel");
   note_launch(1);
   return QCH_OK;
 }
 
-template <int N>
-static int evolve_small(const SmallArgs& base, int64_t M, const double2* psi0, double2* traj,
-                        unsigned long long* bad_norm, cudaStream_t st) {
-  if (int rc = small_prepare<N>(base, M, nullptr, st)) return rc;
-  return small_finish<N>(base, M, psi0, traj, bad_norm, st);
+// workspace: [ubuf (M) unless props given] runp (nruns) agg (nblocks) flags
+static size_t small_ws_bytes(int64_t N, int64_t M, bool props) {
+  return sizeof(double2) * N * N * ((props ? 0 : M) + small_nruns(M) + small_nblocks(M)) + 64;
+}
+static SmallArgs small_carve(void* ws, int64_t N, int64_t M, double2* props) {
+  SmallArgs g;
+  double2* p = (double2*)ws;
+  if (props) {
+    g.ubuf = props;
+  } else {
+    g.ubuf = p;
+    p += N * N * M;
+  }
+  g.runp = p;
+  p += N * N * small_nruns(M);
+  g.agg = p;
+  p += N * N * small_nblocks(M);
+  g.bad = (unsigned long long*)p;
+  return g;
 }
 
-extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, int64_t K, int64_t N, const double* d_sig,
-                                      int64_t S, double t_start, double t_end, int64_t M, int order,
-                                      const void* d_psi0, void* d_traj, void* d_props, int check, int64_t* bad_index,
-                                      void* stream) {
+// one D2H for both flags; NonFinite (unitarity) first, as expm_batch
+// validates before the product (magnus.py:248-252)
+static int small_report(unsigned long long* d_bad, int check, int64_t* bad_index, cudaStream_t st, int64_t offset) {
+  unsigned long long b[2] = {~0ull, ~0ull};
+  QCH_CUDA(cudaMemcpyAsync(b, d_bad, sizeof b, cudaMemcpyDeviceToHost, st));
+  QCH_CUDA(cudaStreamSynchronize(st));
+  if (check && b[0] != ~0ull) {
+    if (bad_index) *bad_index = (int64_t)b[0] + offset;
+    return fail(QCH_ERR_NONFINITE, "propagator not unitary (interval " + std::to_string(b[0] + offset) + ")");
+  }
+  if (b[1] != ~0ull) {
+    if (bad_index) *bad_index = (int64_t)b[1] + offset;
+    return fail(QCH_ERR_NORM_DRIFT, "state norm drifted after interval " + std::to_string(b[1] + offset));
+  }
+  return QCH_OK;
+}
+
+static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_comm_in, int64_t K, int64_t N,
+                              const double* d_sig, int64_t S, double t_start, double t_end, int64_t M, int order,
+                              const void* d_psi0, void* d_traj, void* d_props, int check, int64_t* bad_index,
+                              unsigned long long* d_flags_out, void* stream) {
   if (M < 1) return fail(QCH_ERR_GRID, "need at least one interval");
   if ((S - 1) % M)
     return fail(QCH_ERR_GRID, std::to_string(M) + " intervals do not divide " + std::to_string(S - 1) + " sample steps");
@@ -916,35 +1139,40 @@ extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, int64_
   unsigned long long* bad_norm = bad_u + 1;
   QCH_CUDA(cudaMemsetAsync(bad_u, 0xff, sizeof(unsigned long long) * 2, st));
   DevBuf comm(st);
-  if (order >= 2 && ncomm > 0) {
+  const void* d_comm = d_comm_in;
+  if (order >= 2 && ncomm > 0 && d_comm == nullptr) {
     QCH_CUDA(comm.alloc(sizeof(double2) * nn * ncomm));
     if (int rc = qch_magnus_commutators_c128(d_h0, d_hk, K, N, comm.p, stream)) return rc;
+    d_comm = comm.p;
   }
 
   if (N <= 4) {
-    const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
-    DevBuf q(st);
-    QCH_CUDA(q.alloc(sizeof(double2) * nn * (M + nb)));
-    SmallArgs g;
+    DevBuf ws(st);
+    QCH_CUDA(ws.alloc(small_ws_bytes(N, M, d_props != nullptr)));
+    SmallArgs g = small_carve(ws.p, N, M, (double2*)d_props);
     g.ca = ca;
     g.h0 = (const double2*)d_h0;
     g.hk = (const double2*)d_hk;
-    g.comm = comm.as<double2>();
+    g.comm = (const double2*)d_comm;
     g.order = order;
     g.dt_int = dt_int;
     g.check = check;
-    g.props = (double2*)d_props;
-    g.qloc = q.as<double2>();
-    g.agg = q.as<double2>() + nn * M;
-    g.bad = bad_u;
+    QCH_CUDA(cudaMemsetAsync(g.bad, 0xff, 2 * sizeof(unsigned long long), st));
+    const double2* psi0 = (const double2*)d_psi0;
+    double2* traj = (double2*)d_traj;
     int rc = QCH_OK;
     switch (N) {
-      case 1: rc = evolve_small<1>(g, M, (const double2*)d_psi0, (double2*)d_traj, bad_norm, st); break;
-      case 2: rc = evolve_small<2>(g, M, (const double2*)d_psi0, (double2*)d_traj, bad_norm, st); break;
-      case 3: rc = evolve_small<3>(g, M, (const double2*)d_psi0, (double2*)d_traj, bad_norm, st); break;
-      default: rc = evolve_small<4>(g, M, (const double2*)d_psi0, (double2*)d_traj, bad_norm, st); break;
+      case 1: rc = small_prepare<1>(g, M, nullptr, st); if (!rc) rc = small_finish<1>(g, M, psi0, traj, st); break;
+      case 2: rc = small_prepare<2>(g, M, nullptr, st); if (!rc) rc = small_finish<2>(g, M, psi0, traj, st); break;
+      case 3: rc = small_prepare<3>(g, M, nullptr, st); if (!rc) rc = small_finish<3>(g, M, psi0, traj, st); break;
+      default: rc = small_prepare<4>(g, M, nullptr, st); if (!rc) rc = small_finish<4>(g, M, psi0, traj, st); break;
     }
     if (rc) return rc;
+    if (d_flags_out) {
+      QCH_CUDA(cudaMemcpyAsync(d_flags_out, g.bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+      return QCH_OK;
+    }
+    return small_report(g.bad, check, bad_index, st, 0);
   } else {
     DevBuf coef(st);
     QCH_CUDA(coef.alloc(sizeof(double) * M * (K + ncomm + 1)));
@@ -974,7 +1202,7 @@ extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, int64_
     QCH_CUDA(cudaMemsetAsync(nrm.p, 0, sizeof(double), st));
     for (int64_t m0 = 0; m0 < M; m0 += mb) {
       const int64_t cm = std::min<int64_t>(mb, M - m0);
-      if (int rc = qch_magnus_assemble_c128(d_h0, d_hk, comm.p, K, N, c1, c2, m0, cm, dt_int, order, hbar, stream))
+      if (int rc = qch_magnus_assemble_c128(d_h0, d_hk, d_comm, K, N, c1, c2, m0, cm, dt_int, order, hbar, stream))
         return rc;
       double2* u = d_props ? (double2*)d_props + m0 * nn : ubuf;
       if (int rc = expm_generic(hbar, cm, (int)N, u, work, sarr, norms, st)) return rc;
@@ -1014,34 +1242,31 @@ extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, int64_
   return report_bad(bad_norm, bad_index, QCH_ERR_NORM_DRIFT, "state norm drifted", st);
 }
 
+extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                                      const double* d_sig, int64_t S, double t_start, double t_end, int64_t M,
+                                      int order, const void* d_psi0, void* d_traj, void* d_props, int check,
+                                      int64_t* bad_index, void* stream) {
+  return magnus_evolve_impl(d_h0, d_hk, d_comm, K, N, d_sig, S, t_start, t_end, M, order, d_psi0, d_traj, d_props,
+                            check, bad_index, nullptr, stream);
+}
+
+extern "C" int qch_magnus_evolve_async_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K,
+                                            int64_t N, const double* d_sig, int64_t S, double t_start, double t_end,
+                                            int64_t M, int order, const void* d_psi0, void* d_traj, void* d_props,
+                                            int check, void* d_flags, void* stream) {
+  if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "asynchronous evolve: N <= 4 (fused pipeline)");
+  return magnus_evolve_impl(d_h0, d_hk, d_comm, K, N, d_sig, S, t_start, t_end, M, order, d_psi0, d_traj, d_props,
+                            check, nullptr, (unsigned long long*)d_flags, stream);
+}
+
 // ---------------------------------------------------------------------------
 // Interval sharding across GPUs: each rank owns a
 // contiguous block of intervals, computes its block product B_r, the ranks
 // all-gather the B's (NCCL), each rank applies B_{r-1}...B_0 to psi0 and
 // finishes its local trajectory.  Workspace layout (caller-allocated,
-// qch_magnus_shard_workspace_bytes): qloc (M,N,N) | agg (nb,N,N) | flags.
+// qch_magnus_shard_workspace_bytes): U (M,N,N) | run prefixes | block prefixes | flags.
 extern "C" int64_t qch_magnus_shard_workspace_bytes(int64_t N, int64_t M) {
-  const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
-  return (int64_t)sizeof(double2) * N * N * (M + nb) + 64;
-}
-
-static SmallArgs shard_args(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
-                            const double* d_sig, int64_t S, double dt, double dt_int, int64_t M, int order, int check,
-                            void* d_work) {
-  SmallArgs g;
-  g.ca = CoefArgs{d_sig, (int)K, S, M, (int)((S - 1) / M), dt};
-  g.h0 = (const double2*)d_h0;
-  g.hk = (const double2*)d_hk;
-  g.comm = (const double2*)d_comm;
-  g.order = order;
-  g.dt_int = dt_int;
-  g.check = check;
-  g.props = nullptr;
-  g.qloc = (double2*)d_work;
-  const int64_t nb = (M + kScanThreads - 1) / kScanThreads;
-  g.agg = g.qloc + N * N * M;
-  g.bad = (unsigned long long*)(g.agg + N * N * nb);
-  return g;
+  return (int64_t)small_ws_bytes(N, M, false);
 }
 
 extern "C" int qch_magnus_shard_prepare_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K,
@@ -1051,7 +1276,14 @@ extern "C" int qch_magnus_shard_prepare_c128(const void* d_h0, const void* d_hk,
   if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "sharded Magnus prepare: N <= 4");
   if (M < 1 || (S - 1) % M) return fail(QCH_ERR_GRID, "interval count does not divide the local sample steps");
   cudaStream_t st = (cudaStream_t)stream;
-  SmallArgs g = shard_args(d_h0, d_hk, d_comm, K, N, d_sig, S, dt, dt_int, M, order, check, d_work);
+  SmallArgs g = small_carve(d_work, N, M, nullptr);
+  g.ca = CoefArgs{d_sig, (int)K, S, M, (int)((S - 1) / M), dt};
+  g.h0 = (const double2*)d_h0;
+  g.hk = (const double2*)d_hk;
+  g.comm = (const double2*)d_comm;
+  g.order = order;
+  g.dt_int = dt_int;
+  g.check = check;
   QCH_CUDA(cudaMemsetAsync(g.bad, 0xff, 2 * sizeof(unsigned long long), st));
   switch (N) {
     case 1: return small_prepare<1>(g, M, (double2*)d_block, st);
@@ -1098,19 +1330,16 @@ extern "C" int qch_magnus_shard_finish_c128(int64_t N, int64_t M, void* d_work, 
                                             void* d_traj, int check, int64_t* bad_index, void* stream) {
   if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "sharded Magnus finish: N <= 4");
   cudaStream_t st = (cudaStream_t)stream;
-  SmallArgs g = shard_args(nullptr, nullptr, nullptr, 0, N, nullptr, M + 1, 0.0, 0.0, M, 1, check, d_work);
-  unsigned long long* bad_u = g.bad;
-  unsigned long long* bad_norm = g.bad + 1;
+  SmallArgs g = small_carve(d_work, N, M, nullptr);
+  const double2* p0 = (const double2*)d_psi_start;
+  double2* tr = (double2*)d_traj;
   int rc;
   switch (N) {
-    case 1: rc = small_finish<1>(g, M, (const double2*)d_psi_start, (double2*)d_traj, bad_norm, st); break;
-    case 2: rc = small_finish<2>(g, M, (const double2*)d_psi_start, (double2*)d_traj, bad_norm, st); break;
-    case 3: rc = small_finish<3>(g, M, (const double2*)d_psi_start, (double2*)d_traj, bad_norm, st); break;
-    default: rc = small_finish<4>(g, M, (const double2*)d_psi_start, (double2*)d_traj, bad_norm, st); break;
+    case 1: rc = small_finish<1>(g, M, p0, tr, st); break;
+    case 2: rc = small_finish<2>(g, M, p0, tr, st); break;
+    case 3: rc = small_finish<3>(g, M, p0, tr, st); break;
+    default: rc = small_finish<4>(g, M, p0, tr, st); break;
   }
   if (rc) return rc;
-  if (check) {
-    if (int r2 = report_bad(bad_u, bad_index, QCH_ERR_NONFINITE, "propagator not unitary", st)) return r2;
-  }
-  return report_bad(bad_norm, bad_index, QCH_ERR_NORM_DRIFT, "state norm drifted", st);
+  return small_report(g.bad, check, bad_index, st, 0);
 }

@@ -23,6 +23,8 @@
 // chains) fill the GPU; small matrices (N <= 112) are staged into shared
 // memory for the single-chain case.
 #include <cooperative_groups.h>
+#include <cstdlib>
+#include <cstring>
 
 #include "qch_internal.h"
 #include "qch_math.cuh"
@@ -197,485 +199,11 @@ __global__ void apply_rotations_kernel(double2* __restrict__ h, int64_t n, const
   }
 }
 
-// ----------------------------------------------------------------------------
-// Initial per-row maxima of the relevant strict lower triangle: one warp/row.
-__device__ __forceinline__ bool relevant(const unsigned char* inT, int r, int c) {
-  return inT == nullptr || (inT[r] != inT[c]);
-}
-
-__global__ void rowmax_init_kernel(const double2* __restrict__ h, int n, const unsigned char* __restrict__ inT,
-                                   const int* __restrict__ tlist, int n_target, double* __restrict__ rmag,
-                                   int* __restrict__ rcol, double2* __restrict__ rval) {
-  // blockIdx.y = matrix in batch; state arrays are (batch, n)
-  const double2* hm = h + (int64_t)blockIdx.y * n * n;
-  double* rm = rmag + (int64_t)blockIdx.y * n;
-  int* rc = rcol + (int64_t)blockIdx.y * n;
-  double2* rv = rval + (int64_t)blockIdx.y * n;
-  int lane = threadIdx.x & 31;
-  int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (r >= n) return;
-  double bm = -1.0;
-  int bc = 0x7fffffff;
-  double2 bv = make_double2(0.0, 0.0);
-  if (inT != nullptr && !inT[r]) {
-    // subspace mode, row outside the target: only target columns are relevant
-    for (int q = lane; q < n_target; q += 32) {
-      int c = tlist[q];
-      if (c >= r) continue;
-      double2 v = hm[(int64_t)r * n + c];
-      double m = np_cabs(v.x, v.y);
-      if (rowcand_better(m, c, bm, bc)) {
-        bm = m;
-        bc = c;
-        bv = v;
-      }
-    }
-  } else {
-    for (int c = lane; c < r; c += 32) {
-      if (inT != nullptr && inT[c]) continue;
-      double2 v = hm[(int64_t)r * n + c];
-      double m = np_cabs(v.x, v.y);
-      if (rowcand_better(m, c, bm, bc)) {
-        bm = m;
-        bc = c;
-        bv = v;
-      }
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    double om = __shfl_xor_sync(0xffffffffu, bm, off);
-    int oc = __shfl_xor_sync(0xffffffffu, bc, off);
-    double ovx = __shfl_xor_sync(0xffffffffu, bv.x, off);
-    double ovy = __shfl_xor_sync(0xffffffffu, bv.y, off);
-    if (rowcand_better(om, oc, bm, bc)) {
-      bm = om;
-      bc = oc;
-      bv = make_double2(ovx, ovy);
-    }
-  }
-  if (lane == 0) {
-    rm[r] = bm;
-    rc[r] = (bm < 0.0) ? -1 : bc;
-    rv[r] = bv;
-  }
-}
-
 __global__ void fill_mask_kernel(unsigned char* mask, int n, const int* tlist, int nt) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) mask[x] = 0;
 }
 __global__ void set_mask_kernel(unsigned char* mask, const int* tlist, int nt) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nt; q += gridDim.x * blockDim.x) mask[tlist[q]] = 1;
-}
-
-// ----------------------------------------------------------------------------
-// The greedy driver.  One block per job.
-struct NpadJob {
-  double2* h;        // (N,N)
-  double2* u;        // accumulated unitary or nullptr
-  double* rmag;      // persisted row-max state (N)
-  int* rcol;         // (N)
-  double2* rval;     // (N)
-  int* pivots;       // 2*pivot_cap or nullptr
-  long long pivot_cap;
-  double threshold;
-  long long applied;  // in: already applied; out: total applied
-  int status;         // out: 0 converged, 1 max_iter reached, 2 paused at stop_at
-};
-
-struct NpadCommon {
-  int n;
-  const unsigned char* inT;  // nullptr: full-diagonal mode
-  const int* tlist;          // sorted target list (subspace mode)
-  int n_target;
-  int herm;                  // 1: matrix is bitwise Hermitian
-  int stage_h;               // 1: stage H in shared memory
-  long long max_iter;
-  long long stop_at;
-};
-
-constexpr int kListCap = 30;  // long rescan rows per rotation handled in-phase
-
-struct NpadScalars {
-  double c;
-  cplx s;
-  Block2 blk;
-  int i, j;
-};
-
-template <int CPT>
-__global__ void __launch_bounds__(1024) npad_run_kernel(NpadJob* __restrict__ jobs, NpadCommon cm) {
-  NpadJob* job = jobs + blockIdx.x;
-  const int n = cm.n;
-  const int T = blockDim.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T >> 5;
-  const bool sub = cm.inT != nullptr;
-  const bool herm = cm.herm != 0;
-  double2* __restrict__ ug = job->u;
-  const bool track = ug != nullptr;
-
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned char* sp = smem;
-  auto carve = [&](size_t bytes) {
-    unsigned char* p = sp;
-    sp += (bytes + 15) & ~size_t(15);
-    return p;
-  };
-  double2* s_rval = (double2*)carve(sizeof(double2) * n);
-  double* s_rmag = (double*)carve(sizeof(double) * n);
-  double* s_diag = (double*)carve(sizeof(double) * n);
-  int* s_rcol = (int*)carve(sizeof(int) * n);
-  int* s_slot = (int*)carve(sizeof(int) * n);
-  int* s_list = (int*)carve(sizeof(int) * n);
-  unsigned char* s_inT = (unsigned char*)carve(n);
-  PKey* s_part = (PKey*)carve(sizeof(PKey) * (kListCap + 2) * nw);
-  PKey* s_wkey = (PKey*)carve(sizeof(PKey) * 32);
-  cplx* s_lv = (cplx*)carve(sizeof(cplx) * 2 * kListCap);
-  NpadScalars* s_sc = (NpadScalars*)carve(sizeof(NpadScalars));
-  int* s_cnt = (int*)carve(sizeof(int) * 4);
-  double2* s_h = cm.stage_h ? (double2*)carve(sizeof(double2) * (size_t)n * n) : nullptr;
-
-  double2* __restrict__ h = job->h;
-  if (cm.stage_h) {
-    for (int k = tid; k < n * n; k += T) s_h[k] = h[k];
-    h = s_h;
-  }
-  for (int x = tid; x < n; x += T) {
-    s_rmag[x] = job->rmag[x];
-    s_rcol[x] = job->rcol[x];
-    s_rval[x] = job->rval[x];
-    s_slot[x] = -1;
-    s_inT[x] = sub ? cm.inT[x] : 0;
-    s_diag[x] = herm ? (cm.stage_h ? s_h[(size_t)x * n + x].x : h[(size_t)x * n + x].x) : 0.0;
-  }
-  if (tid == 0) s_cnt[0] = 0;
-  __syncthreads();
-
-  long long applied = job->applied;
-  const double threshold = job->threshold;
-  int status = 0;
-
-  // rows owned by this thread: x = tid + k*T, k < CPT
-  while (true) {
-    // ---------------- Phase 1: finalize partial rows, local best, warp best
-    PKey best = pk_none();
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      int x = tid + k * T;
-      if (x < n) {
-        int sl = s_slot[x];
-        if (sl >= 0) {
-          PKey b = pk_none();
-          for (int w = 0; w < nw; ++w) {
-            PKey o = s_part[sl * nw + w];
-            if (pk_better(o, b)) b = o;
-          }
-          if (b.mag >= 0.0) {
-            int c = (int)(b.cr >> 16);
-            s_rmag[x] = b.mag;
-            s_rcol[x] = c;
-            s_rval[x] = h[(size_t)x * n + c];
-          } else {
-            s_rmag[x] = -1.0;
-            s_rcol[x] = -1;
-          }
-          s_slot[x] = -1;
-        }
-        double m = s_rmag[x];
-        if (m >= 0.0) {
-          PKey kk{m, ((unsigned)s_rcol[x] << 16) | (unsigned)x};
-          if (pk_better(kk, best)) best = kk;
-        }
-      }
-    }
-    best = warp_best(best);
-    if (lane == 0) s_wkey[warp] = best;
-    __syncthreads();  // ---- A
-
-    // ---------------- Phase 2: global pick, stop tests, scalars, prefetch
-    PKey piv = lane < nw ? s_wkey[lane] : pk_none();
-    piv = warp_best(piv);
-    if (applied >= cm.stop_at) {
-      status = 2;
-      break;
-    }
-    if (piv.mag <= 0.0 || piv.mag < threshold) {  // None or below threshold
-      status = 0;
-      break;
-    }
-    if (applied >= cm.max_iter) {
-      status = 1;
-      break;
-    }
-    const int i = (int)(piv.cr >> 16), j = (int)(piv.cr & 0xffffu);
-    if (tid == 0) {
-      cplx hji = d2c(s_rval[j]);
-      cplx hij, hii, hjj;
-      double dii, djj;
-      if (herm) {
-        dii = s_diag[i];
-        djj = s_diag[j];
-        hii = mkc(dii, 0.0);
-        hjj = mkc(djj, 0.0);
-        hij = cconj(hji);
-      } else {
-        hii = d2c(h[(size_t)i * n + i]);
-        hjj = d2c(h[(size_t)j * n + j]);
-        hij = d2c(h[(size_t)i * n + j]);
-        dii = hii.re;
-        djj = hjj.re;
-      }
-      RotParams rp = givens_params(hji, dii, djj);
-      s_sc->c = rp.cos_half;
-      s_sc->s = rp.s;
-      s_sc->blk = rotate_block(rp.cos_half, rp.s, hii, hij, hji, hjj);
-      if (job->pivots != nullptr && applied < job->pivot_cap) {
-        job->pivots[2 * applied] = i;
-        job->pivots[2 * applied + 1] = j;
-      }
-      s_slot[i] = 0;
-      s_slot[j] = 1;
-    }
-    // rows whose stored argmax column is i or j need a rescan
-    bool local_rescan[CPT];
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      local_rescan[k] = false;
-      int x = tid + k * T;
-      if (x < n && x != i && x != j) {
-        int rc = s_rcol[x];
-        if (rc == i || rc == j) {
-          bool shortrow = sub && !s_inT[x] && cm.n_target <= 32;
-          if (shortrow) {
-            local_rescan[k] = true;
-          } else {
-            int q = atomicAdd(&s_cnt[0], 1);
-            s_list[q] = x;
-            s_slot[x] = (q < kListCap) ? 2 + q : -2;
-          }
-        }
-      }
-    }
-    cplx ri[CPT], rj[CPT], ci[CPT], cj[CPT];
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      int x = tid + k * T;
-      if (x < n) {
-        ri[k] = d2c(h[(size_t)i * n + x]);
-        rj[k] = d2c(h[(size_t)j * n + x]);
-        if (!herm) {
-          ci[k] = d2c(h[(size_t)x * n + i]);
-          cj[k] = d2c(h[(size_t)x * n + j]);
-        }
-      }
-    }
-    __syncthreads();  // ---- B
-
-    // ---------------- Phase 3: rotate, fold, partials
-    const double c = s_sc->c;
-    const cplx s = s_sc->s;
-    const int nlist = s_cnt[0];
-    const bool in_i = s_inT[i], in_j = s_inT[j];
-    PKey pi = pk_none(), pj = pk_none();
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      int x = tid + k * T;
-      if (x >= n || x == i || x == j) continue;
-      cplx ni, nj, cxi, cxj;
-      rotate_rows(c, s, ri[k], rj[k], &ni, &nj);
-      if (herm) {
-        cxi = cconj(ni);
-        cxj = cconj(nj);
-      } else {
-        rotate_cols(c, s, ci[k], cj[k], &cxi, &cxj);
-      }
-      h[(size_t)i * n + x] = c2d(ni);
-      h[(size_t)j * n + x] = c2d(nj);
-      h[(size_t)x * n + i] = c2d(cxi);
-      h[(size_t)x * n + j] = c2d(cxj);
-      const bool in_x = s_inT[x];
-      // rows i / j partials: entries (i,x), x<i and (j,x), x<j
-      if (x < i && (!sub || in_i != in_x)) {
-        PKey kk{np_cabs(ni), ((unsigned)x << 16) | (unsigned)i};
-        if (pk_better(kk, pi)) pi = kk;
-      }
-      if (x < j && (!sub || in_j != in_x)) {
-        PKey kk{np_cabs(nj), ((unsigned)x << 16) | (unsigned)j};
-        if (pk_better(kk, pj)) pj = kk;
-      }
-      // row x: entries (x,i) if i<x, (x,j) if j<x
-      bool rel_i = (i < x) && (!sub || in_i != in_x);
-      bool rel_j = (j < x) && (!sub || in_j != in_x);
-      int sl = s_slot[x];
-      if (sl >= 2) {
-        s_lv[2 * (sl - 2)] = cxi;  // new (x,i), (x,j) for the list-row partial
-        s_lv[2 * (sl - 2) + 1] = cxj;
-      } else if (sl == -2) {
-        // overflow row: rescanned after barrier C from memory
-      } else if (local_rescan[k]) {
-        // short subspace row (x not in target): scan its target columns
-        double bm = -1.0;
-        int bc = -1;
-        cplx bv = mkc(0, 0);
-        for (int q = 0; q < cm.n_target; ++q) {
-          int t = cm.tlist[q];
-          if (t >= x) break;
-          cplx v = (t == i) ? cxi : (t == j) ? cxj : d2c(h[(size_t)x * n + t]);
-          double m = np_cabs(v);
-          if (rowcand_better(m, t, bm, bc)) {
-            bm = m;
-            bc = t;
-            bv = v;
-          }
-        }
-        s_rmag[x] = bm;
-        s_rcol[x] = bc;
-        s_rval[x] = c2d(bv);
-      } else {
-        double bm = s_rmag[x];
-        int bc = s_rcol[x];
-        bool ch = false;
-        cplx bv;
-        if (rel_i) {
-          double m = np_cabs(cxi);
-          if (rowcand_better(m, i, bm, bc)) {
-            bm = m;
-            bc = i;
-            bv = cxi;
-            ch = true;
-          }
-        }
-        if (rel_j) {
-          double m = np_cabs(cxj);
-          if (rowcand_better(m, j, bm, bc)) {
-            bm = m;
-            bc = j;
-            bv = cxj;
-            ch = true;
-          }
-        }
-        if (ch) {
-          s_rmag[x] = bm;
-          s_rcol[x] = bc;
-          s_rval[x] = c2d(bv);
-        }
-      }
-    }
-    if (tid == 0) {
-      const Block2 b = s_sc->blk;
-      h[(size_t)i * n + i] = c2d(b.ii);
-      h[(size_t)i * n + j] = c2d(b.ij);
-      h[(size_t)j * n + i] = c2d(b.ji);
-      h[(size_t)j * n + j] = c2d(b.jj);
-      s_diag[i] = b.ii.re;
-      s_diag[j] = b.jj.re;
-      if (!sub || in_i != in_j) {
-        PKey kk{np_cabs(b.ji), ((unsigned)i << 16) | (unsigned)j};
-        if (pk_better(kk, pj)) pj = kk;
-      }
-    }
-    if (track) {
-#pragma unroll
-      for (int k = 0; k < CPT; ++k) {
-        int x = tid + k * T;
-        if (x >= n) continue;
-        cplx ui = d2c(ug[(size_t)i * n + x]), uj = d2c(ug[(size_t)j * n + x]);
-        cplx ni, nj;
-        rotate_rows(c, s, ui, uj, &ni, &nj);
-        ug[(size_t)i * n + x] = c2d(ni);
-        ug[(size_t)j * n + x] = c2d(nj);
-      }
-    }
-    pi = warp_best(pi);
-    pj = warp_best(pj);
-    if (lane == 0) {
-      s_part[0 * nw + warp] = pi;
-      s_part[1 * nw + warp] = pj;
-    }
-    // list rows: partial scans over owned columns
-    const int nl = nlist < kListCap ? nlist : kListCap;
-    for (int q = 0; q < nl; ++q) {
-      const int r = s_list[q];
-      const bool in_r = s_inT[r];
-      PKey pr = pk_none();
-#pragma unroll
-      for (int k = 0; k < CPT; ++k) {
-        int x = tid + k * T;
-        if (x >= r || x == i || x == j) continue;
-        if (sub && in_r == (bool)s_inT[x]) continue;
-        double2 v = h[(size_t)r * n + x];
-        PKey kk{np_cabs(v.x, v.y), ((unsigned)x << 16) | (unsigned)r};
-        if (pk_better(kk, pr)) pr = kk;
-      }
-      if ((r % T) == tid) {
-        // owner adds the entries it rotated: (r,i), (r,j)
-        if (i < r && (!sub || in_r != in_i)) {
-          PKey kk{np_cabs(s_lv[2 * q]), ((unsigned)i << 16) | (unsigned)r};
-          if (pk_better(kk, pr)) pr = kk;
-        }
-        if (j < r && (!sub || in_r != in_j)) {
-          PKey kk{np_cabs(s_lv[2 * q + 1]), ((unsigned)j << 16) | (unsigned)r};
-          if (pk_better(kk, pr)) pr = kk;
-        }
-      }
-      pr = warp_best(pr);
-      if (lane == 0) s_part[(2 + q) * nw + warp] = pr;
-    }
-    ++applied;
-    __syncthreads();  // ---- C
-    if (nlist > kListCap) {
-      // overflow: one warp per remaining row, straight from memory
-      for (int q = kListCap + warp; q < nlist; q += nw) {
-        const int r = s_list[q];
-        const bool in_r = s_inT[r];
-        double bm = -1.0;
-        int bc = 0x7fffffff;
-        for (int x = lane; x < r; x += 32) {
-          if (sub && in_r == (bool)s_inT[x]) continue;
-          double2 v = h[(size_t)r * n + x];
-          double m = np_cabs(v.x, v.y);
-          if (rowcand_better(m, x, bm, bc)) {
-            bm = m;
-            bc = x;
-          }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          double om = __shfl_xor_sync(0xffffffffu, bm, off);
-          int oc = __shfl_xor_sync(0xffffffffu, bc, off);
-          if (rowcand_better(om, oc, bm, bc)) {
-            bm = om;
-            bc = oc;
-          }
-        }
-        if (lane == 0) {
-          s_rmag[r] = bm;
-          s_rcol[r] = bm >= 0.0 ? bc : -1;
-          if (bm >= 0.0) s_rval[r] = h[(size_t)r * n + bc];
-          s_slot[r] = -1;
-        }
-      }
-      __syncthreads();
-    }
-    if (tid == 0) s_cnt[0] = 0;
-    // s_cnt reset is ordered before the next phase-2 atomics by barrier A
-  }
-
-  // ---------------- write back
-  __syncthreads();
-  for (int x = tid; x < n; x += T) {
-    job->rmag[x] = s_rmag[x];
-    job->rcol[x] = s_rcol[x];
-    job->rval[x] = s_rval[x];
-  }
-  if (cm.stage_h) {
-    double2* hg = job->h;
-    for (int k = tid; k < n * n; k += T) hg[k] = s_h[k];
-  }
-  if (tid == 0) {
-    job->applied = applied;
-    job->status = status;
-  }
 }
 
 // ----------------------------------------------------------------------------
@@ -714,67 +242,18 @@ __global__ void build_tr_kernel(double2* __restrict__ h, int64_t nq, int64_t nr,
 // host side
 namespace qch {
 
-static size_t npad_smem_bytes(int n, int threads, bool stage) {
-  auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
-  int nw = threads / 32;
-  size_t s = al(16 * (size_t)n) + al(8 * (size_t)n) + al(8 * (size_t)n) + 3 * al(4 * (size_t)n) + al(n) +
-             al(sizeof(PKey) * (kListCap + 2) * nw) + al(sizeof(PKey) * 32) + al(sizeof(cplx) * 2 * kListCap) +
-             al(sizeof(NpadScalars)) + al(16);
-  if (stage) s += al(16 * (size_t)n * n);
-  return s;
-}
-
-using npad_kernel_t = void (*)(NpadJob*, NpadCommon);
-
-static npad_kernel_t npad_kernel_for(int cpt) {
-  switch (cpt) {
-    case 1: return npad_run_kernel<1>;
-    case 2: return npad_run_kernel<2>;
-    case 4: return npad_run_kernel<4>;
-    case 8: return npad_run_kernel<8>;
-    default: return nullptr;
-  }
-}
-
-// pick (columns per thread, threads): single chains use the widest block
-// (latency); batches use `pref_threads` so several chains share an SM.
-static void npad_shape(int n, int pref_threads, int* cpt, int* threads) {
-  int c = 1;
-  while (c < 8 && (n + c - 1) / c > pref_threads) c *= 2;
-  int t = (n + c - 1) / c;
-  t = ((t + 31) / 32) * 32;
-  if (t < 32) t = 32;
-  *cpt = c;
-  *threads = t;
-}
-
 struct Workspace {
   cudaStream_t st;
   void* p = nullptr;
   explicit Workspace(cudaStream_t s) : st(s) {}
-  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, st); }
+  cudaError_t alloc(size_t bytes) {
+    ensure_pool();
+    return cudaMallocAsync(&p, bytes, st);
+  }
   ~Workspace() {
     if (p) cudaFreeAsync(p, st);
   }
 };
-
-int npad_launch(NpadJob* d_jobs, int njobs, NpadCommon cm, int pref_threads, cudaStream_t st) {
-  int cpt, threads;
-  npad_shape(cm.n, pref_threads, &cpt, &threads);
-  npad_kernel_t k = npad_kernel_for(cpt);
-  if (!k) return fail(QCH_ERR_UNSUPPORTED, "npad: dimension too large for the single-block driver");
-  size_t smem = npad_smem_bytes(cm.n, threads, cm.stage_h != 0);
-  if (smem > (size_t)max_smem_optin())
-    return fail(QCH_ERR_UNSUPPORTED, "npad: dimension " + std::to_string(cm.n) + " needs " + std::to_string(smem) +
-                                         " B of shared memory (max " + std::to_string(max_smem_optin()) + ")");
-  QCH_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  void* pr = prof_begin("npad_run_kernel", st);
-  k<<<njobs, threads, smem, st>>>(d_jobs, cm);
-  prof_end(pr, st);
-  QCH_LAUNCH_CHECK("npad_run_kernel");
-  note_launch(1);
-  return QCH_OK;
-}
 
 }  // namespace qch
 
@@ -858,37 +337,59 @@ extern "C" int qch_build_transmon_resonator_c128(void* d_h, int64_t batch, int64
   return QCH_OK;
 }
 
-// shared setup of the npad drivers: mask, row-max state, jobs
-static int npad_setup(const double2* d_h, int64_t batch, int n, const int32_t* d_target, int64_t n_target,
-                      unsigned char** mask, double** rmag, int** rcol, double2** rval, void* base, cudaStream_t st) {
+
+// ----------------------------------------------------------------------------
+// npad_run drivers (C-ABI)
+#include "npad_run.h"
+
+namespace {
+using namespace qch;
+
+struct RunBufs {
+  unsigned char* mask = nullptr;
+  double* q = nullptr;
+  int* c = nullptr;
+  double2* v = nullptr;
+  NpadJob2* jobs = nullptr;
+  int* flag = nullptr;
+};
+
+size_t run_bytes(int64_t batch, int n) {
+  return 4096 + (size_t)n + (sizeof(double) + sizeof(int) + sizeof(double2)) * (size_t)n * batch +
+         sizeof(NpadJob2) * batch;
+}
+
+RunBufs carve_run(void* base, int64_t batch, int n) {
   unsigned char* p = (unsigned char*)base;
   auto take = [&](size_t b) {
     unsigned char* q = p;
     p += (b + 255) & ~size_t(255);
     return q;
   };
-  *rval = (double2*)take(sizeof(double2) * n * batch);
-  *rmag = (double*)take(sizeof(double) * n * batch);
-  *rcol = (int*)take(sizeof(int) * n * batch);
-  *mask = d_target ? (unsigned char*)take(n) : nullptr;
-  if (d_target) {
-    fill_mask_kernel<<<(n + 255) / 256, 256, 0, st>>>(*mask, n, d_target, (int)n_target);
-    if (n_target > 0) set_mask_kernel<<<(int)((n_target + 255) / 256), 256, 0, st>>>(*mask, d_target, (int)n_target);
-    note_launch(n_target > 0 ? 2 : 1);
-  }
-  dim3 grid((n + 7) / 8, (unsigned)batch);
-  rowmax_init_kernel<<<grid, 256, 0, st>>>(d_h, n, *mask, d_target, (int)n_target, *rmag, *rcol, *rval);
-  QCH_LAUNCH_CHECK("rowmax_init_kernel");
-  note_launch(1);
+  RunBufs r;
+  r.flag = (int*)take(sizeof(int) * 4);
+  r.jobs = (NpadJob2*)take(sizeof(NpadJob2) * batch);
+  r.v = (double2*)take(sizeof(double2) * n * batch);
+  r.q = (double*)take(sizeof(double) * n * batch);
+  r.c = (int*)take(sizeof(int) * n * batch);
+  r.mask = take(n);
+  return r;
+}
+
+// exact keys when |z|^2 could leave the normal range for entries that matter
+int exact_keys(double max_abs, double threshold) {
+  return (max_abs > 1e100 || (threshold > 0.0 && threshold < 1e-140)) ? 1 : 0;
+}
+
+int fill_mask(unsigned char* mask, int n, const int32_t* d_target, int64_t n_target, cudaStream_t st) {
+  fill_mask_kernel<<<(n + 255) / 256, 256, 0, st>>>(mask, n, d_target, (int)n_target);
+  if (n_target > 0) set_mask_kernel<<<(int)((n_target + 255) / 256), 256, 0, st>>>(mask, d_target, (int)n_target);
+  QCH_LAUNCH_CHECK("mask kernels");
+  note_launch(n_target > 0 ? 2 : 1);
   return QCH_OK;
 }
+}  // namespace
 
-static size_t npad_ws_bytes(int64_t batch, int n) {
-  return 3 * 256 + (sizeof(double2) + sizeof(double) + sizeof(int)) * (size_t)n * batch + (size_t)n + 4 * 256 +
-         sizeof(NpadJob) * batch;
-}
-
-// UnitarityDrift audit (npad.py:254-259)
 extern "C" int qch_unitarity_defect_c128(const void* d_u, int64_t batch, int64_t n, double* d_defect, void* stream);
 
 extern "C" int qch_npad_run_dense_c128(void* d_h, int64_t n, const int32_t* d_target, int64_t n_target,
@@ -899,62 +400,60 @@ extern "C" int qch_npad_run_dense_c128(void* d_h, int64_t n, const int32_t* d_ta
   cudaStream_t st = (cudaStream_t)stream;
   const int ni = (int)n;
   Workspace ws(st);
-  QCH_CUDA(ws.alloc(npad_ws_bytes(1, ni) + 256));
-  unsigned char* base = (unsigned char*)ws.p;
-  int* d_flag = (int*)base;
-  NpadJob* d_job = (NpadJob*)(base + 256);
-  unsigned char* rest = base + 256 + ((sizeof(NpadJob) + 255) & ~size_t(255));
-  int rc = qch_hermitian_exact_c128(d_h, n, d_flag, stream);
-  if (rc) return rc;
-  unsigned char* mask;
-  double* rmag;
-  int* rcol;
-  double2* rval;
-  rc = npad_setup((const double2*)d_h, 1, ni, d_target, n_target, &mask, &rmag, &rcol, &rval, rest, st);
-  if (rc) return rc;
-  int nonherm = 0;
-  QCH_CUDA(cudaMemcpyAsync(&nonherm, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  QCH_CUDA(ws.alloc(run_bytes(1, ni)));
+  RunBufs rb = carve_run(ws.p, 1, ni);
+  if (int rc = qch_hermitian_exact_c128(d_h, n, rb.flag, stream)) return rc;
+  QCH_CUDA(cudaMemsetAsync(rb.flag + 1, 0, sizeof(double), st));
+  if (int rc = qch_max_abs_c128(d_h, n * n, (double*)(rb.flag + 2), stream)) return rc;
+  int host[4] = {0, 0, 0, 0};
+  QCH_CUDA(cudaMemcpyAsync(host, rb.flag, sizeof(host), cudaMemcpyDeviceToHost, st));
   QCH_CUDA(cudaStreamSynchronize(st));
+  double maxabs;
+  memcpy(&maxabs, host + 2, sizeof(double));
+  const bool herm = host[0] == 0;
 
-  NpadJob job;
+  NpadCommon2 cm;
+  cm.n = ni;
+  cm.inT = d_target ? rb.mask : nullptr;
+  cm.tlist = d_target;
+  cm.n_target = (int)n_target;
+  cm.ek = exact_keys(maxabs, threshold);
+  cm.max_iter = max_iter;
+  cm.stats = getenv("QCH_NPAD_STATS") ? 1 : 0;
+  const bool trows = npad_use_trows(cm, herm) && d_u == nullptr;
+  if (d_target) {
+    if (int rc = fill_mask(rb.mask, ni, d_target, n_target, st)) return rc;
+  }
+  if (int rc = npad_state_init((const double2*)d_h, 1, cm, trows, rb.q, rb.c, rb.v, st)) return rc;
+
+  NpadJob2 job;
   job.h = (double2*)d_h;
   job.u = (double2*)d_u;
-  job.rmag = rmag;
-  job.rcol = rcol;
-  job.rval = rval;
+  job.st_q = rb.q;
+  job.st_c = rb.c;
+  job.st_v = rb.v;
   job.pivots = d_pivots;
   job.pivot_cap = d_pivots ? pivot_cap : 0;
   job.threshold = threshold;
   job.applied = 0;
   job.status = 0;
-  NpadCommon cm;
-  cm.n = ni;
-  cm.inT = mask;
-  cm.tlist = d_target;
-  cm.n_target = (int)n_target;
-  cm.herm = nonherm ? 0 : 1;
-  cm.max_iter = max_iter;
-  int cpt, threads;
-  npad_shape(ni, 1024, &cpt, &threads);
-  cm.stage_h = npad_smem_bytes(ni, threads, true) <= (size_t)max_smem_optin() ? 1 : 0;
+  job.stats[0] = job.stats[1] = job.stats[2] = job.stats[3] = 0;
   const int64_t audit_every = 100;  // UNITARY_CHECK_EVERY, npad.py:216
-  double* d_defect = nullptr;
   Workspace ws2(st);
+  double* d_defect = nullptr;
   if (d_u) {
     QCH_CUDA(ws2.alloc(sizeof(double)));
     d_defect = (double*)ws2.p;
   }
   while (true) {
     cm.stop_at = d_u ? ((job.applied / audit_every) + 1) * audit_every : INT64_MAX;
-    QCH_CUDA(cudaMemcpyAsync(d_job, &job, sizeof(NpadJob), cudaMemcpyHostToDevice, st));
-    rc = npad_launch(d_job, 1, cm, 1024, st);
-    if (rc) return rc;
-    QCH_CUDA(cudaMemcpyAsync(&job, d_job, sizeof(NpadJob), cudaMemcpyDeviceToHost, st));
+    QCH_CUDA(cudaMemcpyAsync(rb.jobs, &job, sizeof(NpadJob2), cudaMemcpyHostToDevice, st));
+    if (int rc = npad_launch2(rb.jobs, 1, cm, herm, trows, 512, true, st)) return rc;
+    QCH_CUDA(cudaMemcpyAsync(&job, rb.jobs, sizeof(NpadJob2), cudaMemcpyDeviceToHost, st));
     QCH_CUDA(cudaStreamSynchronize(st));
     if (job.status != 2) break;
-    // paused at a multiple of 100 rotations: audit ||UU^dag - I||_F <= 1e-10 N
-    rc = qch_unitarity_defect_c128(d_u, 1, n, d_defect, stream);
-    if (rc) return rc;
+    // paused at a multiple of 100 rotations: ||U U^dag - I||_F <= 1e-10 N
+    if (int rc = qch_unitarity_defect_c128(d_u, 1, n, d_defect, stream)) return rc;
     double defect = 0.0;
     QCH_CUDA(cudaMemcpyAsync(&defect, d_defect, sizeof(double), cudaMemcpyDeviceToHost, st));
     QCH_CUDA(cudaStreamSynchronize(st));
@@ -969,24 +468,25 @@ extern "C" int qch_npad_run_dense_c128(void* d_h, int64_t n, const int32_t* d_ta
   return QCH_OK;
 }
 
-__global__ void batch_jobs_kernel(NpadJob* jobs, double2* h, int64_t n, const double* thr, double* rmag, int* rcol,
-                                  double2* rval, int64_t batch) {
+__global__ void batch_jobs_kernel(NpadJob2* jobs, double2* h, int64_t n, const double* thr, double* q, int* c,
+                                  double2* v, int64_t per, int64_t batch) {
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= batch) return;
-  NpadJob j;
+  NpadJob2 j;
   j.h = h + b * n * n;
   j.u = nullptr;
-  j.rmag = rmag + b * n;
-  j.rcol = rcol + b * n;
-  j.rval = rval + b * n;
+  j.st_q = q + b * per;
+  j.st_c = c + b * per;
+  j.st_v = v + b * per;
   j.pivots = nullptr;
   j.pivot_cap = 0;
   j.threshold = thr[b];
   j.applied = 0;
   j.status = 0;
+  j.stats[0] = j.stats[1] = j.stats[2] = j.stats[3] = 0;
   jobs[b] = j;
 }
-__global__ void batch_out_kernel(const NpadJob* jobs, int64_t batch, int64_t* applied, int32_t* conv) {
+__global__ void batch_out_kernel(const NpadJob2* jobs, int64_t batch, int64_t* applied, int32_t* conv) {
   int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (b >= batch) return;
   applied[b] = jobs[b].applied;
@@ -1002,33 +502,29 @@ extern "C" int qch_npad_run_batch_c128(void* d_h, int64_t batch, int64_t n, cons
   cudaStream_t st = (cudaStream_t)stream;
   const int ni = (int)n;
   Workspace ws(st);
-  QCH_CUDA(ws.alloc(npad_ws_bytes(batch, ni) + 256));
-  NpadJob* d_jobs = (NpadJob*)ws.p;
-  unsigned char* rest = (unsigned char*)ws.p + ((sizeof(NpadJob) * batch + 255) & ~size_t(255));
-  unsigned char* mask;
-  double* rmag;
-  int* rcol;
-  double2* rval;
-  int rc = npad_setup((const double2*)d_h, batch, ni, d_target, n_target, &mask, &rmag, &rcol, &rval, rest, st);
-  if (rc) return rc;
-  batch_jobs_kernel<<<(int)((batch + 127) / 128), 128, 0, st>>>(d_jobs, (double2*)d_h, n, d_thresholds, rmag, rcol,
-                                                                   rval, batch);
-  note_launch(1);
-  NpadCommon cm;
+  QCH_CUDA(ws.alloc(run_bytes(batch, ni)));
+  RunBufs rb = carve_run(ws.p, batch, ni);
+  NpadCommon2 cm;
   cm.n = ni;
-  cm.inT = mask;
+  cm.inT = d_target ? rb.mask : nullptr;
   cm.tlist = d_target;
   cm.n_target = (int)n_target;
-  cm.herm = 1;
+  cm.ek = 0;  // builder-scale operators: |z|^2 keys are safe (see exact_keys)
   cm.max_iter = max_iter;
   cm.stop_at = INT64_MAX;
-  int cpt, threads;
-  npad_shape(ni, 256, &cpt, &threads);
-  cm.stage_h = 0;
-  rc = npad_launch(d_jobs, (int)batch, cm, 256, st);
-  if (rc) return rc;
-  batch_out_kernel<<<(int)((batch + 127) / 128), 128, 0, st>>>(d_jobs, batch, d_applied, d_converged);
+  cm.stats = 0;
+  const bool trows = npad_use_trows(cm, true);
+  if (d_target) {
+    if (int rc = fill_mask(rb.mask, ni, d_target, n_target, st)) return rc;
+  }
+  if (int rc = npad_state_init((const double2*)d_h, batch, cm, trows, rb.q, rb.c, rb.v, st)) return rc;
+  const int64_t per = trows ? cm.n_target : ni;
+  batch_jobs_kernel<<<(int)((batch + 127) / 128), 128, 0, st>>>(rb.jobs, (double2*)d_h, n, d_thresholds, rb.q, rb.c,
+                                                                   rb.v, per, batch);
   note_launch(1);
+  if (int rc = npad_launch2(rb.jobs, (int)batch, cm, true, trows, 256, false, st)) return rc;
+  batch_out_kernel<<<(int)((batch + 127) / 128), 128, 0, st>>>(rb.jobs, batch, d_applied, d_converged);
   QCH_LAUNCH_CHECK("batch_out_kernel");
+  note_launch(1);
   return QCH_OK;
 }

@@ -34,6 +34,7 @@ void note_launch(int k);
 void* prof_begin(const char* name, cudaStream_t st);
 void prof_end(void* h, cudaStream_t st);
 int sm_count();
+void ensure_pool();
 int max_smem_optin();
 
 }  // namespace qch
