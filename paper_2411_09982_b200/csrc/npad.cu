@@ -512,7 +512,7 @@ extern "C" int qch_npad_run_batch_c128(void* d_h, int64_t batch, int64_t n, cons
   cm.ek = 0;  // builder-scale operators: |z|^2 keys are safe (see exact_keys)
   cm.max_iter = max_iter;
   cm.stop_at = INT64_MAX;
-  cm.stats = 0;
+  cm.stats = getenv("QCH_NPAD_STATS") ? 1 : 0;
   const bool trows = npad_use_trows(cm, true);
   if (d_target) {
     if (int rc = fill_mask(rb.mask, ni, d_target, n_target, st)) return rc;

@@ -456,7 +456,9 @@ __global__ void __launch_bounds__(512) npad_trows_kernel(NpadJob2* __restrict__ 
   int status = 0;
   unsigned fin_mask = 0;  // T-rows with partial slots pending (uniform)
 
+  long long tc0 = 0, tc1 = 0, tc2 = 0, tc3 = 0;
   while (true) {
+    if (cm.stats && tid == 0) tc0 = clock64();
     // ---- Phase 1 (every warp redundantly): finalize pending T-rows, select
     Cand mine = cand_none();
     if (lane < nT) {
@@ -490,6 +492,7 @@ __global__ void __launch_bounds__(512) npad_trows_kernel(NpadJob2* __restrict__ 
       status = 1;
       break;
     }
+    if (cm.stats && tid == 0) tc1 = clock64();
     const int i = (int)(piv.cr >> 16), j = (int)(piv.cr & 0xffffu);
     const int kt = s_kof[i] >= 0 ? s_kof[i] : s_kof[j];
     const int t = cm.tlist[kt];
@@ -520,6 +523,7 @@ __global__ void __launch_bounds__(512) npad_trows_kernel(NpadJob2* __restrict__ 
       }
     }
     __syncthreads();  // ---------------------------------------------- B
+    if (cm.stats && tid == 0) tc2 = clock64();
 
     // ---- Phase 3
     const double c = s_sc->c;
@@ -607,7 +611,13 @@ __global__ void __launch_bounds__(512) npad_trows_kernel(NpadJob2* __restrict__ 
       }
     }
     fin_mask = resc | (1u << kt);
-    if (cm.stats && tid == 0) job->stats[0] += __popc(resc);
+    if (cm.stats && tid == 0) {
+      tc3 = clock64();
+      job->stats[0] += __popc(resc);
+      job->stats[1] += tc1 - tc0;
+      job->stats[2] += tc2 - tc1;
+      job->stats[3] += tc3 - tc2;
+    }
     ++applied;
     __syncthreads();  // ---------------------------------------------- C
   }
@@ -621,6 +631,10 @@ __global__ void __launch_bounds__(512) npad_trows_kernel(NpadJob2* __restrict__ 
   if (tid == 0) {
     job->applied = applied;
     job->status = status;
+    if (cm.stats && blockIdx.x < 4)
+      printf("trows[blk %d n=%d T=%d]: applied=%lld rescans=%lld cyc/rot: select=%lld prefetch+B=%lld update=%lld\n",
+             blockIdx.x, n, T, applied, job->stats[0], job->stats[1] / (applied ? applied : 1),
+             job->stats[2] / (applied ? applied : 1), job->stats[3] / (applied ? applied : 1));
   }
 }
 

@@ -30,10 +30,31 @@ def main():
             st = eff.npad_run(op, tol=1e-12, max_iter=arg or 2000)
         print("applied", st.applied)
     elif case == "sweep":
-        pts = eff.sweep_points(8, (arg or 64) // 8)
+        pts = eff.sweep_points(32, 32)[: (arg or 64)]
         for _ in range(2):
             res = npd.npad_sweep_transmon(pts, 4, 256, eff.sweep_target(256), tol=1e-12)
         print("rotations", int(res.applied.sum()))
+    elif case == "sweepscale":
+        # per-chain rotation latency vs number of concurrent chains
+        from paper_2411_09982_b200 import _lib as lib
+        allpts = eff.sweep_points(32, 32)
+        for p in (1, 8, 74, 148, 296, 592, 1024):
+            pts = allpts[:p]
+            mats = npd.build_transmon_resonator_batch(pts, 4, 256)
+            mx = torch.empty(p, dtype=torch.float64, device="cuda")
+            for k in range(p):
+                lib.call("qch_max_abs_c128", lib.dptr(mats[k]), 1024 * 1024, lib.dptr(mx[k:k + 1]), lib.stream_ptr())
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            ap, cv = npd._run_batch_inplace(mats, eff.sweep_target(256), 1e-12, None, mx)
+            s1.record()
+            torch.cuda.synchronize()
+            ms = s0.elapsed_time(s1)
+            rot = int(ap.sum().item())
+            mx_rot = int(ap.max().item())
+            print(f"points={p:5d} rotations={rot:7d} max_chain={mx_rot:4d} ms={ms:8.3f} "
+                  f"rot/s={rot / ms * 1e3:.3e} us/rot(longest chain)={ms * 1e3 / mx_rot:.2f}")
     elif case == "magnus2":
         m = arg or 100000
         ch, grid = eff.driven_transmon(3, intervals=m, sub=4)
