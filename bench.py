@@ -375,7 +375,7 @@ def sec_npad4096(torch, eff, lib, args, peaks, rotations=None):
             "us_per_rotation_kernel": kms * 1e3 / st.applied,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks[0], "unit": "GB/s", "frac": ach / peaks[0],
                          "bytes_per_rotation": 96 * n, "note": "single greedy chain: latency-bound (see DESIGN.md)",
-                         "traffic": traffic_from_profiles("npad_run_kernel_4096")},
+                         "traffic": traffic_from_profiles("npad_rows_kernel@npad4096")},
             "cpu_baseline": {"value": cpu, "unit": "rotations/s", "cores": 1, "kind": "port",
                              "sample": "3 rotations of the same operator, oracle run_full_scan"}}
 
@@ -430,7 +430,7 @@ def sec_sweep(torch, eff, lib, args, peaks, n_points=1024):
             "metric": "NPAD rotations/s", "unit": "rotations/s", "value": rot / (per * 1e-3), "rotations": rot,
             "all_converged": bool(conv.all()), "ms_per_sweep": per,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks[0], "unit": "GB/s", "frac": ach / peaks[0],
-                         "bytes_per_rotation": 96 * n, "traffic": traffic_from_profiles("npad_run_kernel_sweep")},
+                         "bytes_per_rotation": 96 * n, "traffic": traffic_from_profiles("npad_trows_kernel@sweep")},
             "cpu_baseline": {"value": cpu, "unit": "rotations/s", "cores": 1, "kind": "port",
                              "sample": "first 60 rotations of 2 sweep points, oracle run_full_scan"}}
 
@@ -470,7 +470,7 @@ def sec_magnus4096(torch, eff, lib, args, fp64, n_int=2):
                          "peak_kind": "FP64 DMMA (mma.sync f64) measured live; cuBLAS zgemm "
                                       f"{fp64.get('cublas_zgemm', 0):.1f} TFLOP/s for reference",
                          "flops_per_interval": fl, "kernel": "zgemm_taylor",
-                         "traffic": traffic_from_profiles("zgemm_taylor")},
+                         "traffic": traffic_from_profiles("zgemm_kernel@zgemm_taylor4096")},
             "cpu_baseline": {"value": 1.0 / 36.7, "unit": "intervals/s", "cores": 8, "kind": "port",
                              "sample": "SURVEY.md §8(d) measurement (one _expm_minus_i at N=4096 = 36.7 s, 8-core "
                                        "OpenBLAS); not re-timed here (42 h full run)"}}
@@ -598,7 +598,7 @@ def main():
             "roofline": {"bound": "fp64", "kernel": "magnus_prop_kernel", "achieved": achieved,
                          "peak": fp64["dfma"], "unit": "TFLOP/s",
                          "frac": (achieved / fp64["dfma"]) if achieved else None,
-                         "traffic": traffic_from_profiles("magnus_prop_kernel"),
+                         "traffic": traffic_from_profiles("magnus_prop_kernel@magnus2"),
                          "peak_kind": "FP64 FMA pipe, measured live by bench.py (DFMA probe); MEASURED_PEAKS.json "
                                       "has no FP64 entry. Per-interval 3x3 expm is FP64-FMA work, not tensor work",
                          "flops_per_launch": roof["flops_per_launch"] if roof else None,
