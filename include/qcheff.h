@@ -163,6 +163,18 @@ int qch_magnus_evolve_async_c128(const void* d_h0, const void* d_hk, const void*
                                  const void* d_psi0, void* d_traj, void* d_props, int check, void* d_flags,
                                  void* stream);
 
+/* evolve (magnus.py:214-267) with HOST buffers — the reference-facing call:
+ * h_h0 (N,N), h_hk (K,N,N), h_sig (K,S) row-major, h_psi0 (N) are read from
+ * host memory, the trajectory (M+1, N) is written to h_traj.  For N <= 4 the
+ * transfers are pipelined in chunks against the single-pass fused kernel
+ * (H2D of chunk c+1 || kernel on chunk c || D2H of chunk c-1); pinned host
+ * buffers give full overlap, pageable ones are staged by the driver.
+ * Synchronous.  Errors as qch_magnus_evolve_c128.  Not re-entrant on one
+ * device (shares the device's side streams). */
+int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, int64_t K, int64_t N, const double* h_sig,
+                                int64_t S, double t_start, double t_end, int64_t M, int order, const void* h_psi0,
+                                void* h_traj, int check, int64_t* bad_index, void* stream);
+
 /* ------------------------------------------------------------ GEMM ------- */
 
 /* Batched complex128 GEMM on the FP64 tensor pipe (DMMA, mma.sync f64):

@@ -76,6 +76,11 @@ PROTOTYPES = {
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int,
          c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p],
     ),
+    "qch_magnus_evolve_host_c128": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int, c_void_p,
+         c_void_p, c_int, P_int64, c_void_p],
+    ),
     "qch_zgemm_batched": (
         c_int,
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p],
@@ -172,14 +177,21 @@ def torch():
     return _t
 
 
+_cuda_ok = False
+
+
 def require_cuda():
+    global _cuda_ok
     t = torch()
+    if _cuda_ok:
+        return t
     if not t.cuda.is_available():
         raise RuntimeError(
             "paper_2411_09982_b200 needs a CUDA device: the hot paths run only in libqcheff's sm_100a kernels "
             "(there is no CPU fallback)"
         )
     load()
+    _cuda_ok = True
     return t
 
 
@@ -211,5 +223,31 @@ def to_device(array, dtype=None):
     return out.cuda(non_blocking=False).contiguous()
 
 
+PINNED_MIN_BYTES = 1 << 16
+
+
+def host_empty(shape, dtype=np.complex128) -> np.ndarray:
+    """Uninitialised numpy array in page-locked host memory (torch's caching
+    host allocator: freed blocks are reused, so steady-state calls do not
+    cudaHostAlloc).  DMA targets for the host-buffer C-ABI calls."""
+    t = torch()
+    tdt = {np.dtype(np.complex128): t.complex128, np.dtype(np.float64): t.float64}[np.dtype(dtype)]
+    return t.empty(tuple(shape), dtype=tdt, pin_memory=True).numpy()
+
+
 def to_host(tensor) -> np.ndarray:
-    return tensor.detach().cpu().numpy()
+    """Device tensor -> numpy.  Large results land in pinned memory (full-speed
+    DMA, no pageable staging copy)."""
+    tensor = tensor.detach()
+    if tensor.is_cuda and tensor.numel() * tensor.element_size() >= PINNED_MIN_BYTES:
+        t = torch()
+        out = t.empty(tensor.shape, dtype=tensor.dtype, pin_memory=True)
+        out.copy_(tensor, non_blocking=True)
+        t.cuda.current_stream().synchronize()
+        return out.numpy()
+    return tensor.cpu().numpy()
+
+
+def ptr(array: np.ndarray) -> c_void_p:
+    """Host address of a C-contiguous numpy array."""
+    return c_void_p(array.ctypes.data)

@@ -21,6 +21,7 @@
 
 #include "qch_internal.h"
 #include "qch_math.cuh"
+#include "magnus_small.cuh"
 
 namespace qch {
 
@@ -29,99 +30,8 @@ int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, i
 int zgemm_taylor(const double2* a, const double2* b, double2* t, double2* o, int n, int64_t batch, double inv_k,
                  cudaStream_t st);
 int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st);
-
-constexpr int kTaylorOrder = 18;     // expm.py:19
-constexpr double kScaleTarget = 0.5;  // expm.py:20
-
-// ----------------------------------------------------------------------------
-// Coefficients.  First order: magnus.py:164-168 (numpy pairwise sum of
-// (left+right) then * dt/2).  Second order: SURVEY.md Appendix B.
-struct CoefArgs {
-  const double* sig;  // (K, S)
-  int K;
-  int64_t S;
-  int64_t M;
-  int sub;
-  double dt;
-};
-
-__device__ __forceinline__ void interval_coeffs(const CoefArgs& a, int64_t n, int order, double* c1, double* c2) {
-  const int K = a.K, sub = a.sub;
-  const double h = a.dt;
-  for (int k = 0; k < K; ++k) {
-    const double* u = a.sig + (int64_t)k * a.S + n * sub;
-    auto f = [&](int q) { return QADD(u[q], u[q + 1]); };
-    c1[k] = QMUL(QDIV(h, 2.0), np_pairwise(f, sub));
-  }
-  if (order < 2) return;
-  const double hh6 = QDIV(QMUL(h, h), 6.0);
-  const double h2 = QDIV(h, 2.0);
-  // alpha_k = sum_a [h*S_k(a) - a*h*tau_ak] - (h^2/6) sum_a (u_{a+1} - u_a)
-  for (int k = 0; k < K; ++k) {
-    const double* u = a.sig + (int64_t)k * a.S + n * sub;
-    double run = 0.0, acc = 0.0, lin = 0.0;
-    for (int q = 0; q < sub; ++q) {
-      double tau = QMUL(h2, QADD(u[q], u[q + 1]));
-      acc = QADD(acc, QSUB(QMUL(h, run), QMUL(QMUL((double)q, h), tau)));
-      lin = QADD(lin, QSUB(u[q + 1], u[q]));
-      run = QADD(run, tau);
-    }
-    c2[k] = QSUB(acc, QMUL(hh6, lin));
-  }
-  // beta_kl = sum_a [tau_ak S_l(a) - tau_al S_k(a)] - (h^2/6) sum_a (u_k,a u_l,a+1 - u_l,a u_k,a+1)
-  int idx = K;
-  for (int k = 0; k < K; ++k)
-    for (int l = k + 1; l < K; ++l) {
-      const double* uk = a.sig + (int64_t)k * a.S + n * sub;
-      const double* ul = a.sig + (int64_t)l * a.S + n * sub;
-      double sk = 0.0, sl = 0.0, acc = 0.0, cr = 0.0;
-      for (int q = 0; q < sub; ++q) {
-        double tk = QMUL(h2, QADD(uk[q], uk[q + 1]));
-        double tl = QMUL(h2, QADD(ul[q], ul[q + 1]));
-        acc = QADD(acc, QSUB(QMUL(tk, sl), QMUL(tl, sk)));
-        cr = QADD(cr, QSUB(QMUL(uk[q], ul[q + 1]), QMUL(ul[q], uk[q + 1])));
-        sk = QADD(sk, tk);
-        sl = QADD(sl, tl);
-      }
-      c2[idx++] = QSUB(acc, QMUL(hh6, cr));
-    }
-}
-
-// the same coefficients one at a time (no local arrays in the hot kernel)
-__device__ __forceinline__ double coef1(const CoefArgs& a, int64_t n, int k) {
-  const double* u = a.sig + (int64_t)k * a.S + n * a.sub;
-  auto f = [&](int q) { return QADD(u[q], u[q + 1]); };
-  return QMUL(QDIV(a.dt, 2.0), np_pairwise(f, a.sub));
-}
-__device__ __forceinline__ double coef_alpha(const CoefArgs& a, int64_t n, int k) {
-  const double h = a.dt, h2 = QDIV(h, 2.0), hh6 = QDIV(QMUL(h, h), 6.0);
-  const double* u = a.sig + (int64_t)k * a.S + n * a.sub;
-  double run = 0.0, acc = 0.0, lin = 0.0;
-  for (int q = 0; q < a.sub; ++q) {
-    double tau = QMUL(h2, QADD(u[q], u[q + 1]));
-    acc = QADD(acc, QSUB(QMUL(h, run), QMUL(QMUL((double)q, h), tau)));
-    lin = QADD(lin, QSUB(u[q + 1], u[q]));
-    run = QADD(run, tau);
-  }
-  return QSUB(acc, QMUL(hh6, lin));
-}
-__device__ __forceinline__ double coef_beta(const CoefArgs& a, int64_t n, int k, int l) {
-  const double h = a.dt, h2 = QDIV(h, 2.0), hh6 = QDIV(QMUL(h, h), 6.0);
-  const double* uk = a.sig + (int64_t)k * a.S + n * a.sub;
-  const double* ul = a.sig + (int64_t)l * a.S + n * a.sub;
-  double sk = 0.0, sl = 0.0, acc = 0.0, cr = 0.0;
-  for (int q = 0; q < a.sub; ++q) {
-    double tk = QMUL(h2, QADD(uk[q], uk[q + 1]));
-    double tl = QMUL(h2, QADD(ul[q], ul[q + 1]));
-    acc = QADD(acc, QSUB(QMUL(tk, sl), QMUL(tl, sk)));
-    cr = QADD(cr, QSUB(QMUL(uk[q], ul[q + 1]), QMUL(ul[q], uk[q + 1])));
-    sk = QADD(sk, tk);
-    sl = QADD(sl, tl);
-  }
-  return QSUB(acc, QMUL(hh6, cr));
-}
-
-constexpr int kMaxK = 8;
+int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const double2* d_psi0, double2* d_traj,
+                        int64_t* bad_index, unsigned long long* d_flags_out, cudaStream_t st);
 
 __global__ void coeff_kernel(CoefArgs a, int order, double* __restrict__ c1, double* __restrict__ c2) {
   int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -133,235 +43,6 @@ __global__ void coeff_kernel(CoefArgs a, int order, double* __restrict__ c1, dou
     int nc = a.K + a.K * (a.K - 1) / 2;
     for (int k = 0; k < nc; ++k) c2[n * nc + k] = l2[k];
   }
-}
-
-// ----------------------------------------------------------------------------
-// small dense matrices in registers
-template <int N>
-struct Mat {
-  cplx v[N][N];
-};
-template <int N>
-__device__ __forceinline__ Mat<N> mat_eye() {
-  Mat<N> m;
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) m.v[r][c] = mkc(r == c ? 1.0 : 0.0, 0.0);
-  return m;
-}
-template <int N>
-__device__ __forceinline__ Mat<N> mat_mul(const Mat<N>& a, const Mat<N>& b) {
-  Mat<N> o;
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      cplx acc = np_cmul(a.v[r][0], b.v[0][c]);
-#pragma unroll
-      for (int k = 1; k < N; ++k) acc = cadd(acc, np_cmul(a.v[r][k], b.v[k][c]));
-      o.v[r][c] = acc;
-    }
-  return o;
-}
-template <int N>
-__device__ __forceinline__ cplx mat_det(const Mat<N>& m);
-template <>
-__device__ __forceinline__ cplx mat_det<1>(const Mat<1>& m) {
-  return m.v[0][0];
-}
-template <>
-__device__ __forceinline__ cplx mat_det<2>(const Mat<2>& m) {
-  return csub(np_cmul(m.v[0][0], m.v[1][1]), np_cmul(m.v[0][1], m.v[1][0]));
-}
-template <>
-__device__ __forceinline__ cplx mat_det<3>(const Mat<3>& m) {
-  cplx a = np_cmul(m.v[0][0], csub(np_cmul(m.v[1][1], m.v[2][2]), np_cmul(m.v[1][2], m.v[2][1])));
-  cplx b = np_cmul(m.v[0][1], csub(np_cmul(m.v[1][0], m.v[2][2]), np_cmul(m.v[1][2], m.v[2][0])));
-  cplx c = np_cmul(m.v[0][2], csub(np_cmul(m.v[1][0], m.v[2][1]), np_cmul(m.v[1][1], m.v[2][0])));
-  return cadd(csub(a, b), c);
-}
-template <>
-__device__ __forceinline__ cplx mat_det<4>(const Mat<4>& m) {
-  cplx acc = mkc(0, 0);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    Mat<3> s;
-#pragma unroll
-    for (int r = 1; r < 4; ++r) {
-      int cc = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (q != c) s.v[r - 1][cc++] = m.v[r][q];
-    }
-    cplx t = np_cmul(m.v[0][c], mat_det<3>(s));
-    acc = (c & 1) ? csub(acc, t) : cadd(acc, t);
-  }
-  return acc;
-}
-
-// _expm_minus_i (expm.py:56-71) on one register matrix (hbar -> U)
-template <int N>
-__device__ __forceinline__ Mat<N> expm_minus_i_reg(const Mat<N>& hb) {
-  Mat<N> a;
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) a.v[r][c] = mkc(hb.v[r][c].im, -hb.v[r][c].re);  // -1j * H, exact
-  double norm = 0.0;
-#pragma unroll
-  for (int r = 0; r < N; ++r) {
-    double rs = 0.0;  // numpy sequential sum for n < 8
-#pragma unroll
-    for (int c = 0; c < N; ++c) rs = QADD(rs, np_cabs(a.v[r][c]));
-    norm = fmax(norm, rs);
-  }
-  int s = 0;
-  if (norm > kScaleTarget) {
-    s = (int)ceil(log2(QDIV(norm, kScaleTarget)));
-    double scl = ldexp(1.0, -s);  // a / 2**s == a * 2**-s exactly
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-#pragma unroll
-      for (int c = 0; c < N; ++c) a.v[r][c] = mkc(QMUL(a.v[r][c].re, scl), QMUL(a.v[r][c].im, scl));
-  }
-  Mat<N> out = mat_eye<N>(), term = mat_eye<N>();
-  for (int k = 1; k <= kTaylorOrder; ++k) {
-    term = mat_mul<N>(term, a);
-    double inv = QDIV(1.0, (double)k);
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        term.v[r][c] = mkc(QMUL(term.v[r][c].re, inv), QMUL(term.v[r][c].im, inv));
-        out.v[r][c] = cadd(out.v[r][c], term.v[r][c]);
-      }
-  }
-  for (int q = 0; q < s; ++q) out = mat_mul<N>(out, out);
-  return out;
-}
-
-// UnitaryPropagator.validate (expm.py:40-47)
-template <int N>
-__device__ __forceinline__ bool validate_reg(const Mat<N>& u) {
-  double d2 = 0.0;
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      cplx acc = mkc(0, 0);
-#pragma unroll
-      for (int k = 0; k < N; ++k) acc = cadd(acc, np_cmul(u.v[r][k], cconj(u.v[c][k])));
-      double re = acc.re - (r == c ? 1.0 : 0.0);
-      d2 += re * re + acc.im * acc.im;
-    }
-  double defect = sqrt(d2);
-  if (!(defect <= 1e-10 * N)) return false;
-  cplx d = mat_det<N>(u);
-  double ad = hypot_cr(d.re, d.im);
-  return fabs(ad - 1.0) <= 1e-8;
-}
-
-struct SmallArgs {
-  CoefArgs ca;
-  const double2* h0;    // (N,N)
-  const double2* hk;    // (K,N,N)
-  const double2* comm;  // (K + K(K-1)/2, N, N) (order 2)
-  int order;
-  double dt_int;
-  int check;
-  double2* ubuf;    // (M,N,N) propagators (the caller's props buffer when requested)
-  double2* runp;    // (nruns,N,N) block-exclusive prefix of each run
-  double2* agg;     // (nblocks, N, N) block aggregates -> exclusive block prefixes
-  unsigned long long* bad;  // [0] first non-unitary interval, [1] first norm drift
-};
-
-template <int N>
-__device__ __forceinline__ void ld_mat(Mat<N>& m, const double2* p) {
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) m.v[r][c] = d2c(p[r * N + c]);
-}
-template <int N>
-__device__ __forceinline__ void st_mat(double2* p, const Mat<N>& m) {
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) p[r * N + c] = c2d(m.v[r][c]);
-}
-
-// complex matrix product with FMA accumulation (the BLAS-like rounding of the
-// reference's `term @ a`, expm.py:67; 4 FMA per complex MAC)
-template <int N>
-__device__ __forceinline__ Mat<N> mat_mul_fma(const Mat<N>& a, const Mat<N>& b) {
-  Mat<N> o;
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      double re = a.v[r][0].re * b.v[0][c].re;
-      double im = a.v[r][0].re * b.v[0][c].im;
-      re = fma(-a.v[r][0].im, b.v[0][c].im, re);
-      im = fma(a.v[r][0].im, b.v[0][c].re, im);
-#pragma unroll
-      for (int k = 1; k < N; ++k) {
-        re = fma(a.v[r][k].re, b.v[k][c].re, re);
-        im = fma(a.v[r][k].re, b.v[k][c].im, im);
-        re = fma(-a.v[r][k].im, b.v[k][c].im, re);
-        im = fma(a.v[r][k].im, b.v[k][c].re, im);
-      }
-      o.v[r][c] = mkc(re, im);
-    }
-  return o;
-}
-
-// _expm_minus_i (expm.py:56-71) in registers, FMA products; the k = 1 term
-// (I @ a / 1 = a, exact) is taken directly.
-template <int N>
-__device__ __forceinline__ Mat<N> expm_minus_i_fast(const Mat<N>& hb) {
-  Mat<N> a;
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) a.v[r][c] = mkc(hb.v[r][c].im, -hb.v[r][c].re);
-  double norm = 0.0;
-#pragma unroll
-  for (int r = 0; r < N; ++r) {
-    double rs = 0.0;
-#pragma unroll
-    for (int c = 0; c < N; ++c) rs = QADD(rs, np_cabs(a.v[r][c]));
-    norm = fmax(norm, rs);
-  }
-  int s = 0;
-  if (norm > kScaleTarget) {
-    s = (int)ceil(log2(QDIV(norm, kScaleTarget)));
-    const double scl = ldexp(1.0, -s);
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-#pragma unroll
-      for (int c = 0; c < N; ++c) a.v[r][c] = mkc(a.v[r][c].re * scl, a.v[r][c].im * scl);
-  }
-  Mat<N> out, term = a;
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) out.v[r][c] = mkc((r == c ? 1.0 : 0.0) + a.v[r][c].re, a.v[r][c].im);
-#pragma unroll 1
-  for (int k = 2; k <= kTaylorOrder; ++k) {
-    term = mat_mul_fma<N>(term, a);
-    const double inv = 1.0 / (double)k;
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        term.v[r][c] = mkc(term.v[r][c].re * inv, term.v[r][c].im * inv);
-        out.v[r][c] = mkc(out.v[r][c].re + term.v[r][c].re, out.v[r][c].im + term.v[r][c].im);
-      }
-  }
-#pragma unroll 1
-  for (int q = 0; q < s; ++q) out = mat_mul_fma<N>(out, out);
-  return out;
 }
 
 constexpr int kScanThreads = 128;
@@ -389,60 +70,10 @@ __device__ Mat<N> block_scan(Mat<N> p, double2* sm) {
 template <int N>
 __global__ void __launch_bounds__(128) magnus_prop_kernel(SmallArgs g) {
   extern __shared__ __align__(16) double2 ssm[];
-  const int K = g.ca.K;
-  const int ncomm = K + K * (K - 1) / 2;
-  double2* s_ops = ssm;  // H0, Hk..., comm...
-  for (int q = threadIdx.x; q < N * N; q += blockDim.x) s_ops[q] = g.h0[q];
-  for (int q = threadIdx.x; q < K * N * N; q += blockDim.x) s_ops[N * N + q] = g.hk[q];
-  if (g.order >= 2)
-    for (int q = threadIdx.x; q < ncomm * N * N; q += blockDim.x) s_ops[(1 + K) * N * N + q] = g.comm[q];
-  __syncthreads();
+  load_ops<N>(g, ssm);
   const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (n >= g.ca.M) return;
-  Mat<N> hb;
-  // h = dt*drift; h = h + w*ctrl  (magnus.py:186-188)
-#pragma unroll
-  for (int r = 0; r < N; ++r)
-#pragma unroll
-    for (int c = 0; c < N; ++c) hb.v[r][c] = np_rmul(g.dt_int, d2c(s_ops[r * N + c]));
-  for (int k = 0; k < K; ++k) {
-    const double w = coef1(g.ca, n, k);
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-#pragma unroll
-      for (int c = 0; c < N; ++c) hb.v[r][c] = cadd(hb.v[r][c], np_rmul(w, d2c(s_ops[(1 + k) * N * N + r * N + c])));
-  }
-  if (g.order >= 2) {
-    Mat<N> x;
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-#pragma unroll
-      for (int c = 0; c < N; ++c) x.v[r][c] = mkc(0, 0);
-    int q = 0;
-    for (int k = 0; k < K; ++k, ++q) {
-      const double w = coef_alpha(g.ca, n, k);
-#pragma unroll
-      for (int r = 0; r < N; ++r)
-#pragma unroll
-        for (int c = 0; c < N; ++c)
-          x.v[r][c] = cadd(x.v[r][c], np_rmul(w, d2c(s_ops[(1 + K + q) * N * N + r * N + c])));
-    }
-    for (int k = 0; k < K; ++k)
-      for (int l = k + 1; l < K; ++l, ++q) {
-        const double w = coef_beta(g.ca, n, k, l);
-#pragma unroll
-        for (int r = 0; r < N; ++r)
-#pragma unroll
-          for (int c = 0; c < N; ++c)
-            x.v[r][c] = cadd(x.v[r][c], np_rmul(w, d2c(s_ops[(1 + K + q) * N * N + r * N + c])));
-      }
-    // hbar = hbar1 + (-0.5j) * X
-#pragma unroll
-    for (int r = 0; r < N; ++r)
-#pragma unroll
-      for (int c = 0; c < N; ++c) hb.v[r][c] = cadd(hb.v[r][c], np_cmul(mkc(0.0, -0.5), x.v[r][c]));
-  }
-  const Mat<N> u = expm_minus_i_fast<N>(hb);
+  const Mat<N> u = expm_minus_i_fast<N>(interval_hbar<N>(g, ssm, n));
   if (g.check && !validate_reg<N>(u)) atomicMin(g.bad, (unsigned long long)n);
   st_mat<N>(g.ubuf + n * N * N, u);
 }
@@ -1132,6 +763,18 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
   const double dt = (t_end - t_start) / (double)(S - 1);  // ControlGrid.dt, magnus.py:87-88
   const double dt_int = (t_end - t_start) / (double)M;     // magnus.py:199
   CoefArgs ca{d_sig, (int)K, S, M, (int)((S - 1) / M), dt};
+  if (N <= 4) {
+    SmallArgs g;
+    g.ca = ca;
+    g.h0 = (const double2*)d_h0;
+    g.hk = (const double2*)d_hk;
+    g.comm = (const double2*)d_comm_in;  // null: formed in the kernel preamble
+    g.order = order;
+    g.dt_int = dt_int;
+    g.check = check;
+    g.ubuf = (double2*)d_props;
+    return fused_evolve_device(g, N, M, (const double2*)d_psi0, (double2*)d_traj, bad_index, d_flags_out, st);
+  }
 
   DevBuf flags(st);
   QCH_CUDA(flags.alloc(sizeof(unsigned long long) * 2));
@@ -1140,40 +783,13 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
   QCH_CUDA(cudaMemsetAsync(bad_u, 0xff, sizeof(unsigned long long) * 2, st));
   DevBuf comm(st);
   const void* d_comm = d_comm_in;
-  if (order >= 2 && ncomm > 0 && d_comm == nullptr) {
+  if (order >= 2 && ncomm > 0 && d_comm == nullptr && N > 4) {
     QCH_CUDA(comm.alloc(sizeof(double2) * nn * ncomm));
     if (int rc = qch_magnus_commutators_c128(d_h0, d_hk, K, N, comm.p, stream)) return rc;
     d_comm = comm.p;
   }
 
-  if (N <= 4) {
-    DevBuf ws(st);
-    QCH_CUDA(ws.alloc(small_ws_bytes(N, M, d_props != nullptr)));
-    SmallArgs g = small_carve(ws.p, N, M, (double2*)d_props);
-    g.ca = ca;
-    g.h0 = (const double2*)d_h0;
-    g.hk = (const double2*)d_hk;
-    g.comm = (const double2*)d_comm;
-    g.order = order;
-    g.dt_int = dt_int;
-    g.check = check;
-    QCH_CUDA(cudaMemsetAsync(g.bad, 0xff, 2 * sizeof(unsigned long long), st));
-    const double2* psi0 = (const double2*)d_psi0;
-    double2* traj = (double2*)d_traj;
-    int rc = QCH_OK;
-    switch (N) {
-      case 1: rc = small_prepare<1>(g, M, nullptr, st); if (!rc) rc = small_finish<1>(g, M, psi0, traj, st); break;
-      case 2: rc = small_prepare<2>(g, M, nullptr, st); if (!rc) rc = small_finish<2>(g, M, psi0, traj, st); break;
-      case 3: rc = small_prepare<3>(g, M, nullptr, st); if (!rc) rc = small_finish<3>(g, M, psi0, traj, st); break;
-      default: rc = small_prepare<4>(g, M, nullptr, st); if (!rc) rc = small_finish<4>(g, M, psi0, traj, st); break;
-    }
-    if (rc) return rc;
-    if (d_flags_out) {
-      QCH_CUDA(cudaMemcpyAsync(d_flags_out, g.bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
-      return QCH_OK;
-    }
-    return small_report(g.bad, check, bad_index, st, 0);
-  } else {
+  {
     DevBuf coef(st);
     QCH_CUDA(coef.alloc(sizeof(double) * M * (K + ncomm + 1)));
     double* c1 = coef.as<double>();

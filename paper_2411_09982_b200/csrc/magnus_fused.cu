@@ -1,0 +1,655 @@
+// magnus_fused.cu — single-pass Magnus evolve for small N (N <= 4): the
+// dim-3 driven transmon of BASELINE config 2.
+//
+// Reference: evolve() (magnus.py:214-267) = coefficients (:151-169) ->
+// effective Hamiltonians (:172-190) -> propagators exp(-i Hbar_n)
+// (expm.py:56-71) -> ordered product psi_{n+1} = U_n psi_n (:249-252) with the
+// NormDrift check (:270-273).
+//
+// ONE kernel does all of it in a single pass over the intervals:
+//  * a block owns a tile of 128 threads x kR consecutive intervals; each
+//    thread forms Hbar_n and U_n in registers (magnus_small.cuh) and the
+//    product of its kR propagators;
+//  * warp-shuffle inclusive scan of the thread products (3x3 complex, later
+//    intervals multiplied on the left), then the 4 warp aggregates;
+//  * decoupled look-back across tiles (tile order = dynamic grab order, so
+//    every predecessor tile is owned by a running block): a tile publishes
+//    its aggregate, inspects 128 predecessors at once, takes the nearest one
+//    that has published its inclusive prefix, multiplies the aggregates in
+//    between with shuffle trees, and publishes its own inclusive prefix
+//    (block-wide windows keep the walk short when a whole wave of tiles
+//    finishes together);
+//  * psi at each thread's start = (thread prefix)(warp prefix) E psi0; each
+//    thread then applies its kR propagators sequentially (the reference's
+//    psi <- U psi), writing the trajectory rows and checking the norm.
+// The ordered product is re-associated (scan), which moves results by
+// O(M eps) ~ 1e-12 relative at M = 1e5: inside the 1e-10 parity bar.
+//
+// A block grabs its next tile before computing the current one (to prefetch
+// its signals).  Still deadlock-free: the smallest unfinished tile belongs to
+// a block that is computing it, and its look-back only waits on smaller tiles.
+//
+// The signals and the trajectory may live in mapped page-locked host memory:
+// each tile stages its signal window with one coalesced pass and writes its
+// trajectory rows directly, so a host-buffer call streams its I/O over the
+// host link while it computes (qch_magnus_evolve_host_c128).
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <vector>
+
+#include "magnus_small.cuh"
+#include "qch_internal.h"
+#include "qch_math.cuh"
+
+namespace qch {
+
+constexpr int kFusedWarps = 4;
+constexpr int kFusedThreads = 32 * kFusedWarps;
+constexpr int kR = 2;  // consecutive intervals per thread
+constexpr int kTile = kFusedThreads * kR;  // intervals per tile (one block)
+
+constexpr int kOpsInline = (1 + kMaxK) * 16;
+
+struct FusedArgs {
+  SmallArgs s;          // coefficients, operators, order, check, props (s.ubuf, nullable), flags (s.bad)
+  const double2* psi0;  // (N,); null: psi0v
+  double2 opsv[kOpsInline];  // H0 | H_k by value when s.h0 is null (no upload for the host-buffer call)
+  double2 psi0v[4];
+  int64_t win;          // > 0: stage each tile's signal window (win samples per control) in shared memory
+  int stream_blocks_per_sm;  // > 0: persistent grid of this many blocks per SM streaming the tiles (host I/O)
+  double2* traj;        // rows (M+1, N), indexed by GLOBAL interval
+  int64_t M;            // intervals of the whole evolve
+  int64_t tile_begin, tile_end;  // tiles of this launch
+  int* tile_ctr;        // this launch's grab counter (zeroed)
+  int* flag;            // per tile: 0 none, 1 aggregate, 2 inclusive prefix
+  double2* agg;         // per tile N*N
+  double2* inc;         // per tile N*N
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int W>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(W) : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ Mat<N> shfl_mat(const Mat<N>& m, int src) {
+  Mat<N> o;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+      o.v[r][c] = mkc(__shfl_sync(0xffffffffu, m.v[r][c].re, src), __shfl_sync(0xffffffffu, m.v[r][c].im, src));
+  return o;
+}
+template <int N>
+__device__ __forceinline__ Mat<N> shfl_up_mat(const Mat<N>& m, int d) {
+  Mat<N> o;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+      o.v[r][c] = mkc(__shfl_up_sync(0xffffffffu, m.v[r][c].re, d), __shfl_up_sync(0xffffffffu, m.v[r][c].im, d));
+  return o;
+}
+template <int N>
+__device__ __forceinline__ Mat<N> shfl_down_mat(const Mat<N>& m, int d) {
+  Mat<N> o;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+      o.v[r][c] =
+          mkc(__shfl_down_sync(0xffffffffu, m.v[r][c].re, d), __shfl_down_sync(0xffffffffu, m.v[r][c].im, d));
+  return o;
+}
+template <int N>
+__device__ __forceinline__ void ldcg_mat(Mat<N>& m, const double2* p) {
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) m.v[r][c] = d2c(__ldcg(p + r * N + c));
+}
+template <int N>
+__device__ __forceinline__ void stcg_mat(double2* p, const Mat<N>& m) {
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) __stcg(p + r * N + c, c2d(m.v[r][c]));
+}
+
+// y = A x
+template <int N>
+__device__ __forceinline__ void mat_vec(const Mat<N>& a, const cplx* x, cplx* y) {
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    double re = 0.0, im = 0.0;
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      re = fma(a.v[r][c].re, x[c].re, re);
+      re = fma(-a.v[r][c].im, x[c].im, re);
+      im = fma(a.v[r][c].re, x[c].im, im);
+      im = fma(a.v[r][c].im, x[c].re, im);
+    }
+    y[r] = mkc(re, im);
+  }
+}
+
+// ordered product over the lanes of a warp, lane 0 leftmost, of the first
+// `span` lanes; the result is broadcast to every lane
+template <int N>
+__device__ __forceinline__ Mat<N> warp_ordered_product(Mat<N> m, int span, int lane) {
+  for (int d = 1; d < span; d <<= 1) {
+    const Mat<N> o = shfl_down_mat<N>(m, d);
+    if ((lane & (2 * d - 1)) == 0 && lane + d < span) m = mat_mul_fma<N>(m, o);
+  }
+  return shfl_mat<N>(m, 0);
+}
+
+// Exclusive prefix of tile t, E = A_{t-1} ... A_0, by block-wide decoupled
+// look-back: the 128 threads inspect 128 predecessors at once, take the
+// nearest one that has published its inclusive prefix, and multiply the
+// aggregates in between (warp shuffle trees, then the 4 warp results).
+template <int N>
+__device__ Mat<N> block_lookback(const FusedArgs& g, int64_t t, Mat<N>* s_red, int* s_j) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  Mat<N> e = mat_eye<N>();
+  int64_t base = t - 1;
+  while (true) {
+    const int64_t p = base - tid;
+    int f = 3;  // before tile 0: identity prefix
+    if (p >= 0) {
+      do {
+        f = ld_acquire(g.flag + p);
+      } while (f == 0);
+    }
+    if (tid == 0) *s_j = kFusedThreads;
+    __syncthreads();
+    if (f >= 2) atomicMin(s_j, tid);
+    __syncthreads();
+    const int j = *s_j;
+    Mat<N> m = mat_eye<N>();
+    if (tid < j) {
+      ldcg_mat<N>(m, g.agg + p * N * N);
+    } else if (tid == j && f == 2) {
+      ldcg_mat<N>(m, g.inc + p * N * N);
+    }
+    const int last = j < kFusedThreads ? j : kFusedThreads - 1;  // threads 0..last matter
+    if (warp * 32 <= last) {
+      const int span = std::min(32, last - warp * 32 + 1);
+      m = warp_ordered_product<N>(m, span, lane);
+      if (lane == 0) s_red[warp] = m;
+    }
+    __syncthreads();
+    const int nw = last / 32 + 1;
+    Mat<N> r = s_red[0];
+    for (int w = 1; w < nw; ++w) r = mat_mul_fma<N>(r, s_red[w]);
+    e = mat_mul_fma<N>(e, r);
+    __syncthreads();  // s_red / s_j reuse
+    if (j < kFusedThreads) break;
+    base -= kFusedThreads;
+  }
+  return e;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
+    magnus_fused_kernel(const __grid_constant__ FusedArgs g) {
+  extern __shared__ __align__(16) double2 fsm[];
+  const int K = g.s.ca.K;
+  double2* s_ops = fsm;
+  const bool inl = g.s.h0 == nullptr;
+  load_ops<N>(g.s, s_ops, inl ? g.opsv : nullptr, inl ? g.opsv + N * N : nullptr);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double2* s_u = fsm + ops_smem_bytes<N>(K, 2) / sizeof(double2) + (size_t)tid * kR * N * N;
+  const size_t wstride = (((size_t)K * g.win + 1) & ~(size_t)1);  // doubles per window buffer (16 B multiple)
+  double* s_sig0 = (double*)(fsm + ops_smem_bytes<N>(K, 2) / sizeof(double2) + (size_t)kFusedThreads * kR * N * N);
+  double2* s_traj = (double2*)(s_sig0 + (g.win > 0 ? 2 * wstride : 0));
+  const double2* psi0p = g.psi0 ? g.psi0 : g.psi0v;
+  __shared__ Mat<N> s_w[kFusedWarps];    // warp aggregates -> in-block exclusive warp prefixes
+  __shared__ Mat<N> s_red[kFusedWarps];  // look-back partials
+  __shared__ Mat<N> s_e;                 // exclusive prefix of the tile
+  __shared__ int s_tile, s_j;
+
+  // the control samples of a tile: one coalesced pass into shared memory,
+  // issued asynchronously (cp.async) one tile ahead, so that the fetch of the
+  // next window — possibly from mapped host memory over the host link —
+  // overlaps this tile's arithmetic
+  auto prefetch = [&](int64_t tt, double* buf) {
+    const int64_t s0 = tt * kTile * (int64_t)g.s.ca.sub;
+    const int64_t cnt = std::min<int64_t>(g.win, g.s.ca.S - s0);
+    for (int k = 0; k < K; ++k)
+      for (int64_t q = tid; q < cnt; q += kFusedThreads) cp_async8(buf + k * g.win + q, g.s.ca.sig + k * g.s.ca.S + s0 + q);
+    cp_commit();
+  };
+
+  if (tid == 0) s_tile = atomicAdd(g.tile_ctr, 1);
+  __syncthreads();
+  int64_t t = g.tile_begin + s_tile;
+  if (g.win > 0 && t < g.tile_end) prefetch(t, s_sig0);
+  for (int it = 0;; ++it) {
+    if (t >= g.tile_end) break;
+    __syncthreads();  // everyone has read s_tile
+    if (tid == 0) s_tile = atomicAdd(g.tile_ctr, 1);  // grab the next tile now (order-safe, see header)
+    __syncthreads();
+    const int64_t tn = g.tile_begin + s_tile;
+    double* s_sig = s_sig0 + (it & 1) * wstride;
+    if (g.win > 0) {
+      if (tn < g.tile_end) {
+        prefetch(tn, s_sig0 + ((it + 1) & 1) * wstride);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+    }
+    __syncthreads();
+    const int64_t n0 = t * kTile + (int64_t)tid * kR;
+    SmallArgs gl = g.s;
+    int64_t nbase = 0;
+    if (g.win > 0) {
+      gl.ca.sig = s_sig;
+      gl.ca.S = g.win;
+      nbase = t * kTile;
+    }
+
+    // ---- propagators of this thread's kR intervals (to shared memory),
+    // then their product (registers stay free for the exponential)
+#pragma unroll 1
+    for (int r = 0; r < kR; ++r) {
+      const int64_t n = n0 + r;
+      Mat<N> u = mat_eye<N>();
+      if (n < g.M) {
+        u = expm_minus_i_fast<N>(interval_hbar<N>(gl, s_ops, n - nbase));
+        if (g.s.check && !validate_reg<N>(u)) atomicMin(g.s.bad, (unsigned long long)n);
+        if (g.s.ubuf != nullptr) st_mat<N>(g.s.ubuf + n * N * N, u);
+      }
+      st_mat<N>(s_u + r * N * N, u);
+    }
+    Mat<N> p;
+    ld_mat<N>(p, s_u);
+#pragma unroll 1
+    for (int r = 1; r < kR; ++r) {
+      Mat<N> u;
+      ld_mat<N>(u, s_u + r * N * N);
+      p = mat_mul_fma<N>(u, p);
+    }
+    // ---- warp inclusive scan: P_l = A_l ... A_0
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const Mat<N> q = shfl_up_mat<N>(p, d);
+      if (lane >= d) p = mat_mul_fma<N>(p, q);
+    }
+    if (lane == 31) s_w[warp] = p;
+    __syncthreads();
+    // ---- tile aggregate, in-block warp prefixes; publish; look-back
+    if (tid == 0) {
+      Mat<N> x = mat_eye<N>();
+      for (int w = 0; w < kFusedWarps; ++w) {
+        const Mat<N> a = s_w[w];
+        s_w[w] = x;  // exclusive prefix of warp w within the tile
+        x = (w == 0) ? a : mat_mul_fma<N>(a, x);
+      }
+      if (t == 0) {
+        stcg_mat<N>(g.inc, x);
+        __threadfence();
+        st_release(g.flag, 2);
+      } else {
+        stcg_mat<N>(g.agg + t * N * N, x);
+        __threadfence();
+        st_release(g.flag + t, 1);
+      }
+      s_red[0] = x;  // the tile aggregate, for the inclusive prefix below
+    }
+    __syncthreads();
+    Mat<N> agg = s_red[0];
+    __syncthreads();
+    if (t > 0) {
+      const Mat<N> e = block_lookback<N>(g, t, s_red, &s_j);
+      if (tid == 0) {
+        stcg_mat<N>(g.inc + t * N * N, mat_mul_fma<N>(agg, e));
+        __threadfence();
+        st_release(g.flag + t, 2);
+        s_e = e;
+      }
+    } else if (tid == 0) {
+      s_e = mat_eye<N>();
+    }
+    __syncthreads();
+    // ---- trajectory: psi at this thread's start = P_{lane-1} X_warp E psi0
+    cplx psi0[N], v[N], w[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) psi0[q] = d2c(psi0p[q]);
+    mat_vec<N>(s_e, psi0, v);
+    mat_vec<N>(s_w[warp], v, w);
+    Mat<N> pex = shfl_up_mat<N>(p, 1);
+    if (lane == 0) pex = mat_eye<N>();
+    mat_vec<N>(pex, w, v);
+#pragma unroll
+    for (int q = 0; q < N; ++q) w[q] = v[q];
+    if (t == 0 && tid == 0) {
+#pragma unroll
+      for (int q = 0; q < N; ++q) g.traj[q] = c2d(psi0[q]);
+    }
+#pragma unroll 1
+    for (int r = 0; r < kR; ++r) {
+      const int64_t n = n0 + r;
+      if (n >= g.M) break;
+      Mat<N> u;
+      ld_mat<N>(u, s_u + r * N * N);
+      mat_vec<N>(u, w, v);
+      double nrm2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        w[q] = v[q];
+        nrm2 = fma(v[q].re, v[q].re, fma(v[q].im, v[q].im, nrm2));
+        s_traj[(tid * kR + r) * N + q] = c2d(v[q]);
+      }
+      if (!(fabs(sqrt(nrm2) - 1.0) <= 1e-6)) atomicMin(g.s.bad + 1, (unsigned long long)n);  // magnus.py:28
+    }
+    __syncthreads();
+    // ---- the tile's trajectory rows leave in one coalesced, contiguous pass
+    // (rows t*kTile+1 .. ; the destination may be mapped host memory)
+    {
+      const int64_t row0 = t * kTile + 1;
+      const int64_t rows = std::min<int64_t>(kTile, g.M - t * kTile);
+      double2* dst = g.traj + row0 * N;
+      for (int64_t q = tid; q < rows * N; q += kFusedThreads) dst[q] = s_traj[q];
+    }
+    __syncthreads();  // s_w / s_e / s_traj reuse
+    t = tn;
+  }
+}
+
+constexpr size_t kStageMax = 24 * 1024;  // signal window staged in shared memory up to this size (x2 buffers)
+
+template <int N>
+static size_t fused_smem(int K) {
+  return ops_smem_bytes<N>(K, 2) + sizeof(double2) * (size_t)kFusedThreads * kR * N * N +
+         sizeof(double2) * (size_t)kTile * N;
+}
+// samples per control of one tile's window, or 0 when it does not fit
+static int64_t fused_window(int K, int sub) {
+  const int64_t w = (int64_t)kTile * sub + 1;
+  return (K > 0 && (size_t)K * w * sizeof(double) <= kStageMax) ? w : 0;
+}
+
+template <int N>
+static int fused_launch(FusedArgs& g, cudaStream_t st) {
+  g.win = fused_window(g.s.ca.K, g.s.ca.sub);
+  const size_t smem = fused_smem<N>(g.s.ca.K) + 2 * (((size_t)g.s.ca.K * g.win + 1) & ~(size_t)1) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    QCH_CUDA(cudaFuncSetAttribute(magnus_fused_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(fused_smem<N>(8) + 2 * kStageMax + 32)));
+    attr = true;
+  }
+  int blocks_per_sm = 0;
+  QCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, magnus_fused_kernel<N>, kFusedThreads, smem));
+  if (blocks_per_sm < 1) blocks_per_sm = 1;
+  const int64_t tiles = g.tile_end - g.tile_begin;
+  if (tiles <= 0) return QCH_OK;
+  int64_t slots = (int64_t)blocks_per_sm * sm_count();
+  if (g.stream_blocks_per_sm > 0) slots = std::min<int64_t>(slots, (int64_t)g.stream_blocks_per_sm * sm_count());
+  const int grid = (int)std::min<int64_t>(tiles, slots);
+  void* pr = prof_begin("magnus_fused_kernel", st);
+  magnus_fused_kernel<N><<<grid, kFusedThreads, smem, st>>>(g);
+  prof_end(pr, st);
+  QCH_LAUNCH_CHECK("magnus_fused_kernel");
+  note_launch(1);
+  return QCH_OK;
+}
+
+int fused_launch_any(int n, FusedArgs& g, cudaStream_t st) {
+  switch (n) {
+    case 1: return fused_launch<1>(g, st);
+    case 2: return fused_launch<2>(g, st);
+    case 3: return fused_launch<3>(g, st);
+    default: return fused_launch<4>(g, st);
+  }
+}
+
+int64_t fused_tiles(int64_t M) { return (M + kTile - 1) / kTile; }
+int64_t fused_tile_intervals() { return kTile; }
+
+// workspace: flags (ntiles int) | counters (nlaunch int) | bad (2 ull) | agg | inc
+size_t fused_ws_bytes(int64_t N, int64_t M, int nlaunch) {
+  const int64_t nt = fused_tiles(M);
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  return al(sizeof(int) * (nt + nlaunch)) + al(16) + 2 * al(sizeof(double2) * N * N * nt);
+}
+size_t fused_ws_zero_bytes(int64_t M, int nlaunch) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  return al(sizeof(int) * (fused_tiles(M) + nlaunch)) + al(16);
+}
+void fused_carve(void* ws, int64_t N, int64_t M, int nlaunch, FusedArgs* g, int** ctr) {
+  const int64_t nt = fused_tiles(M);
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  unsigned char* p = (unsigned char*)ws;
+  g->flag = (int*)p;
+  *ctr = g->flag + nt;
+  p += al(sizeof(int) * (nt + nlaunch));
+  g->s.bad = (unsigned long long*)p;
+  p += al(16);
+  g->agg = (double2*)p;
+  p += al(sizeof(double2) * N * N * nt);
+  g->inc = (double2*)p;
+}
+
+
+namespace {
+struct Trace {
+  bool on = getenv("QCH_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[qch trace] %-28s %8.1f us\n", what, std::chrono::duration<double, std::micro>(t - t0).count());
+  }
+};
+struct FBuf {
+  cudaStream_t st;
+  void* p = nullptr;
+  explicit FBuf(cudaStream_t s) : st(s) {}
+  cudaError_t alloc(size_t b) {
+    ensure_pool();
+    return cudaMallocAsync(&p, std::max<size_t>(b, 16), st);
+  }
+  ~FBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+// page-locked status words of the host-buffer call (one pair per device)
+struct Pipe {
+  unsigned long long* h_flags = nullptr;
+};
+Pipe& pipe_for_device() {
+  static Pipe pipes[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Pipe& p = pipes[dev & 63];
+  if (p.h_flags == nullptr) cudaMallocHost(&p.h_flags, 2 * sizeof(unsigned long long));
+  return p;
+}
+
+// device address of a page-locked, mapped host buffer (UVA), or null for
+// pageable memory
+void* mapped_ptr(const void* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return (a.type == cudaMemoryTypeHost) ? a.devicePointer : nullptr;
+}
+}  // namespace
+
+// Device-buffer fused evolve (N <= 4).  d_flags_out non-null: copy the two
+// status words there and return without synchronising (async evolve).
+int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const double2* d_psi0, double2* d_traj,
+                        int64_t* bad_index, unsigned long long* d_flags_out, cudaStream_t st) {
+  FBuf ws(st);
+  QCH_CUDA(ws.alloc(fused_ws_bytes(N, M, 1)));
+  FusedArgs g;
+  g.s = base;
+  g.stream_blocks_per_sm = 0;
+  int* ctr = nullptr;
+  fused_carve(ws.p, N, M, 1, &g, &ctr);
+  QCH_CUDA(cudaMemsetAsync(ws.p, 0, fused_ws_zero_bytes(M, 1), st));
+  QCH_CUDA(cudaMemsetAsync(g.s.bad, 0xff, 2 * sizeof(unsigned long long), st));
+  g.psi0 = d_psi0;
+  g.traj = d_traj;
+  g.M = M;
+  g.tile_begin = 0;
+  g.tile_end = fused_tiles(M);
+  g.tile_ctr = ctr;
+  if (int rc = fused_launch_any((int)N, g, st)) return rc;
+  if (d_flags_out) {
+    QCH_CUDA(cudaMemcpyAsync(d_flags_out, g.s.bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+    return QCH_OK;
+  }
+  unsigned long long b[2];
+  QCH_CUDA(cudaMemcpyAsync(b, g.s.bad, sizeof b, cudaMemcpyDeviceToHost, st));
+  QCH_CUDA(cudaStreamSynchronize(st));
+  if (base.check && b[0] != ~0ull) {
+    if (bad_index) *bad_index = (int64_t)b[0];
+    return fail(QCH_ERR_NONFINITE, "propagator not unitary (interval " + std::to_string(b[0]) + ")");
+  }
+  if (b[1] != ~0ull) {
+    if (bad_index) *bad_index = (int64_t)b[1];
+    return fail(QCH_ERR_NORM_DRIFT, "state norm drifted after interval " + std::to_string(b[1]));
+  }
+  return QCH_OK;
+}
+
+}  // namespace qch
+
+using namespace qch;
+
+extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                                      const double* d_sig, int64_t S, double t_start, double t_end, int64_t M,
+                                      int order, const void* d_psi0, void* d_traj, void* d_props, int check,
+                                      int64_t* bad_index, void* stream);
+
+// evolve() with HOST buffers (magnus.py:214-267): inputs are read from and the
+// trajectory written to host memory.  For N <= 4 one fused launch streams the
+// page-locked buffers over the host link itself (zero-copy), so transfers and
+// compute overlap; pageable buffers are staged through device memory.
+extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, int64_t K, int64_t N,
+                                           const double* h_sig, int64_t S, double t_start, double t_end, int64_t M,
+                                           int order, const void* h_psi0, void* h_traj, int check,
+                                           int64_t* bad_index, void* stream) {
+  if (M < 1) return fail(QCH_ERR_GRID, "need at least one interval");
+  if ((S - 1) % M)
+    return fail(QCH_ERR_GRID, std::to_string(M) + " intervals do not divide " + std::to_string(S - 1) + " sample steps");
+  if (K > 8) return fail(QCH_ERR_UNSUPPORTED, "at most 8 control channels");
+  if (order != 1 && order != 2) return fail(QCH_ERR_VALUE, "order must be 1 or 2");
+  if (N < 1) return fail(QCH_ERR_VALUE, "dimension must be at least 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  Trace tr;
+  const int64_t nn = N * N;
+  const int64_t Kd = std::max<int64_t>(K, 1);
+  FBuf dev(st);
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t b_ops = al(sizeof(double2) * nn * (1 + Kd)), b_psi = al(sizeof(double2) * N),
+               b_sig = al(sizeof(double) * Kd * S), b_traj = al(sizeof(double2) * N * (M + 1));
+  QCH_CUDA(dev.alloc(b_ops + b_psi + b_sig + b_traj));
+  unsigned char* base = (unsigned char*)dev.p;
+  double2* d_h0 = (double2*)base;
+  double2* d_hk = d_h0 + nn;
+  double2* d_psi0 = (double2*)(base + b_ops);
+  double* d_sig = (double*)(base + b_ops + b_psi);
+  double2* d_traj = (double2*)(base + b_ops + b_psi + b_sig);
+  QCH_CUDA(cudaMemcpyAsync(d_h0, h_h0, sizeof(double2) * nn, cudaMemcpyHostToDevice, st));
+  if (K > 0) QCH_CUDA(cudaMemcpyAsync(d_hk, h_hk, sizeof(double2) * nn * K, cudaMemcpyHostToDevice, st));
+  QCH_CUDA(cudaMemcpyAsync(d_psi0, h_psi0, sizeof(double2) * N, cudaMemcpyHostToDevice, st));
+  tr.mark("alloc + operand upload");
+
+  if (N > 4) {  // generic path: upload, device evolve, download
+    if (K > 0) QCH_CUDA(cudaMemcpyAsync(d_sig, h_sig, sizeof(double) * K * S, cudaMemcpyHostToDevice, st));
+    else QCH_CUDA(cudaMemsetAsync(d_sig, 0, sizeof(double) * S, st));
+    if (int rc = qch_magnus_evolve_c128(d_h0, d_hk, nullptr, K, N, d_sig, S, t_start, t_end, M, order, d_psi0,
+                                        d_traj, nullptr, check, bad_index, stream))
+      return rc;
+    QCH_CUDA(cudaMemcpyAsync(h_traj, d_traj, sizeof(double2) * N * (M + 1), cudaMemcpyDeviceToHost, st));
+    QCH_CUDA(cudaStreamSynchronize(st));
+    return QCH_OK;
+  }
+
+  // N <= 4: ONE launch.  Operators and psi0 travel inside the kernel
+  // arguments; page-locked (mapped) signal / trajectory buffers are read and
+  // written by the kernel directly over the host link, so the H2D of the
+  // signals, the compute and the D2H of the trajectory all overlap.
+  const int64_t sub = (S - 1) / M;
+  FusedArgs g;
+  memcpy(g.opsv, h_h0, sizeof(double2) * nn);
+  if (K > 0) memcpy(g.opsv + nn, h_hk, sizeof(double2) * nn * K);
+  memcpy(g.psi0v, h_psi0, sizeof(double2) * N);
+  const double* sig = getenv("QCH_NOMAP_SIG") ? nullptr : (const double*)mapped_ptr(h_sig);
+  double2* traj = getenv("QCH_NOMAP_TRAJ") ? nullptr : (double2*)mapped_ptr(h_traj);
+  if (K > 0 && sig == nullptr) {
+    QCH_CUDA(cudaMemcpyAsync(d_sig, h_sig, sizeof(double) * K * S, cudaMemcpyHostToDevice, st));
+    sig = d_sig;
+  } else if (K == 0) {
+    sig = d_sig;
+  }
+  tr.mark(traj ? "signals ready (mapped out)" : "signals ready (device out)");
+  if (traj == nullptr) traj = d_traj;
+  // host-link I/O: a persistent grid streams the tiles so fetches, arithmetic
+  // and write-backs of different tiles overlap
+  g.stream_blocks_per_sm = (sig != d_sig || traj != d_traj) ? 1 : 0;
+  if (const char* e = getenv("QCH_STREAM_BPS")) g.stream_blocks_per_sm = atoi(e);
+
+  FBuf ws(st);
+  QCH_CUDA(ws.alloc(fused_ws_bytes(N, M, 1)));
+  int* ctr = nullptr;
+  fused_carve(ws.p, N, M, 1, &g, &ctr);
+  QCH_CUDA(cudaMemsetAsync(ws.p, 0, fused_ws_zero_bytes(M, 1), st));
+  QCH_CUDA(cudaMemsetAsync(g.s.bad, 0xff, 2 * sizeof(unsigned long long), st));
+  g.s.ca = CoefArgs{sig, (int)K, S, M, (int)sub, (t_end - t_start) / (double)(S - 1)};
+  g.s.h0 = nullptr;  // operators inline (g.opsv)
+  g.s.hk = nullptr;
+  g.s.comm = nullptr;  // formed in the kernel preamble
+  g.s.order = order;
+  g.s.dt_int = (t_end - t_start) / (double)M;
+  g.s.check = check;
+  g.s.ubuf = nullptr;
+  g.psi0 = nullptr;
+  g.traj = traj;
+  g.M = M;
+  g.tile_begin = 0;
+  g.tile_end = fused_tiles(M);
+  g.tile_ctr = ctr;
+  if (int rc = fused_launch_any((int)N, g, st)) return rc;
+  Pipe& pp = pipe_for_device();
+  QCH_CUDA(cudaMemcpyAsync(pp.h_flags, g.s.bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  if (traj == d_traj)
+    QCH_CUDA(cudaMemcpyAsync(h_traj, d_traj, sizeof(double2) * N * (M + 1), cudaMemcpyDeviceToHost, st));
+  tr.mark("enqueued");
+  QCH_CUDA(cudaStreamSynchronize(st));
+  tr.mark("synchronized");
+  const unsigned long long b0 = pp.h_flags[0], b1 = pp.h_flags[1];
+  if (check && b0 != ~0ull) {
+    if (bad_index) *bad_index = (int64_t)b0;
+    return fail(QCH_ERR_NONFINITE, "propagator not unitary (interval " + std::to_string(b0) + ")");
+  }
+  if (b1 != ~0ull) {
+    if (bad_index) *bad_index = (int64_t)b1;
+    return fail(QCH_ERR_NORM_DRIFT, "state norm drifted after interval " + std::to_string(b1));
+  }
+  return QCH_OK;
+}

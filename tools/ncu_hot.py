@@ -1,5 +1,5 @@
 """Summarise an ncu report's source page: top CUDA lines by warp-stall
-samples (with the dominant stall reasons).  python tools/ncu_hot.py rep [n]"""
+samples (with the dominant stall reasons).  python tools/ncu_hot.py rep [n] [inst]"""
 import csv
 import io
 import subprocess
@@ -28,17 +28,21 @@ def main():
         except ValueError:
             return 0.0
 
+    key = si
+    if len(sys.argv) > 3 and sys.argv[3] == "inst" and ii is not None:
+        key = ii
+        print(f"total warp instructions {sum(f(r[ii]) for r in data):.0f}")
     total = sum(f(r[si]) for r in data)
-    data.sort(key=lambda r: -f(r[si]))
+    data.sort(key=lambda r: -f(r[key]))
     print(f"total samples {total:.0f}")
     for r in data[:top]:
         s = f(r[si])
-        if s == 0:
+        if s == 0 and key == si:
             break
         reasons = sorted(((f(r[k]), hdr[k][6:]) for k in stall_cols), reverse=True)[:3]
         rs = ", ".join(f"{n}:{v / s:.0%}" for v, n in reasons if v > 0)
         ins = f(r[ii]) if ii is not None else 0
-        print(f"{s / total:6.1%} L{r[0]:>5} inst={ins:>10.0f} [{rs}] {r[1].strip()[:90]}")
+        print(f"{s / max(total, 1):6.1%} L{r[0]:>5} inst={ins:>10.0f} [{rs}] {r[1].strip()[:90]}")
 
 
 if __name__ == "__main__":
