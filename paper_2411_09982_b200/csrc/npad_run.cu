@@ -24,6 +24,8 @@
 // reference's _conjugate_dense.  Bitwise-Hermitian matrices (checked by
 // qch_hermitian_exact_c128) are updated by reading rows only and writing the
 // columns as conjugates: 96*N bytes per rotation.
+#include <cstdlib>
+
 #include "npad_run.h"
 #include "npad_select.cuh"
 #include "qch_internal.h"
@@ -771,6 +773,10 @@ int npad_launch2(NpadJob2* jobs, int njobs, const NpadCommon2& cm, bool herm, bo
                  bool allow_smem_h, cudaStream_t st) {
   int cpt, threads;
   shape_for(cm.n, pref_threads, &cpt, &threads);
+  // many independent chains (the sweep): one warp per chain
+  const char* wenv = getenv("QCH_NPAD_WARP");
+  const bool warp_mode = wenv ? atoi(wenv) != 0 : njobs > 1;
+  if (trows && warp_mode) return npad_launch_trows_warp(jobs, njobs, cm, st);
   if (trows) {
     switch (cpt) {
       case 1: return launch_trows_t<1>(jobs, njobs, cm, threads, st);

@@ -41,7 +41,7 @@ __device__ __forceinline__ Cand cand_none() {
 
 // out-of-line exact magnitude: the rare path must not bloat the hot loops
 // (the instruction cache is the first limiter of these kernels)
-__device__ __noinline__ double np_cabs_ool(double re, double im) { return np_cabs(re, im); }
+static __device__ __noinline__ double np_cabs_ool(double re, double im) { return np_cabs(re, im); }
 
 __device__ __forceinline__ double key_of(double2 v, bool ek) {
   return ek ? np_cabs_ool(v.x, v.y) : fma(v.x, v.x, v.y * v.y);
@@ -62,7 +62,7 @@ __device__ __forceinline__ double cand_m(Cand& a) {
 }
 
 // near-tie resolution with exact numpy magnitudes (out of line)
-__device__ __noinline__ bool cand_better_exact(Cand& a, Cand& b) {
+static __device__ __noinline__ bool cand_better_exact(Cand& a, Cand& b) {
   double ma = cand_m(a), mb = cand_m(b);
   if (ma != mb) return ma > mb;
   return a.cr < b.cr;
@@ -81,7 +81,7 @@ __device__ __forceinline__ void cand_take(Cand& best, Cand c) {
   if (cand_better(c, best)) best = c;
 }
 
-__device__ __noinline__ int warp_argmax_exact(Cand& c, bool nearf) {
+static __device__ __noinline__ int warp_argmax_exact(Cand& c, bool nearf) {
   double m = -1.0;
   unsigned cr = 0xffffffffu;
   if (nearf) {

@@ -1,0 +1,116 @@
+"""The warp-per-chain subspace driver (npad_warp.cu: lazy columns, cp.async
+ring) — the BASELINE config-4 sweep path — against the oracle and against the
+eager block driver, bit for bit."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel_fro
+from oracle import npad_oracle
+
+pytestmark = pytest.mark.gpu
+TOL_F = 1e-10
+
+
+@pytest.fixture(scope="module")
+def E():
+    import paper_2411_09982_b200 as eff
+
+    return eff
+
+
+@pytest.fixture
+def warp_mode():
+    old = os.environ.get("QCH_NPAD_WARP")
+    os.environ["QCH_NPAD_WARP"] = "1"
+    yield
+    if old is None:
+        del os.environ["QCH_NPAD_WARP"]
+    else:
+        os.environ["QCH_NPAD_WARP"] = old
+
+
+def _herm(n, seed, scale=1.0):
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = (a + a.conj().T) * (0.5 * scale)
+    h = np.triu(h) + np.triu(h, 1).conj().T  # bitwise Hermitian
+    return h + np.diag(np.arange(n, dtype=float))
+
+
+def test_warp_driver_golden_subspace(E, golden, warp_mode):
+    g = golden("npad_tr4x30_sub")
+    st, piv = E.npad_run_logged(E.HermitianOperator(g["h"]), g["target"].tolist(), tol=float(g["tol"]))
+    np.testing.assert_array_equal(piv, g["pivots"])
+    assert st.applied == int(g["applied"]) and st.converged == bool(g["converged"])
+    assert rel_fro(st.current.data, g["final"]) <= TOL_F
+
+
+@pytest.mark.parametrize("n,nt,seed", [(40, 3, 1), (150, 10, 2), (257, 32, 3)])
+def test_warp_driver_random_vs_oracle(E, warp_mode, n, nt, seed):
+    h = _herm(n, seed)
+    tgt = sorted(np.random.default_rng(seed + 100).choice(n, nt, replace=False).tolist())
+    ref = npad_oracle.run_incremental(h, tgt, tol=1e-12)
+    st, piv = E.npad_run_logged(E.HermitianOperator(h), tgt, tol=1e-12)
+    np.testing.assert_array_equal(piv, ref["pivots"])
+    assert st.applied == ref["applied"] and st.converged == ref["converged"]
+    assert rel_fro(st.current.data, ref["h"]) <= TOL_F
+
+
+def test_warp_driver_touched_overflow_flush(E, warp_mode):
+    # a dense chain that touches far more than 128 distinct rows: exercises the
+    # mid-chain column flush of the lazy scheme
+    n = 420
+    h = _herm(n, 7, scale=0.3)
+    tgt = list(range(0, n, 35))  # 12 target levels spread over the spectrum
+    ref = npad_oracle.run_incremental(h, tgt, tol=1e-12, max_iter=2500)
+    assert len(set(ref["pivots"].ravel().tolist())) > 140
+    st, piv = E.npad_run_logged(E.HermitianOperator(h), tgt, tol=1e-12, max_iter=2500)
+    np.testing.assert_array_equal(piv, ref["pivots"])
+    assert rel_fro(st.current.data, ref["h"]) <= TOL_F
+
+
+def test_lazy_columns_bit_identical_to_eager(E):
+    # batch (warp driver, lazy columns) vs single runs (block driver, eager
+    # mirrored columns): the same matrices, bit for bit
+    pts = E.sweep_points(4, 4)[[0, 5, 10, 15]]
+    nq, nr = 4, 64
+    tgt = E.sweep_target(nr)
+    res = E.npad_sweep_transmon(pts, nq, nr, tgt, tol=1e-12)
+    old = os.environ.pop("QCH_NPAD_WARP", None)
+    try:
+        for b, row in enumerate(pts):
+            h = E.transmon_resonator_hamiltonian(nq, nr, omega_q=row[0], alpha=row[1], omega_r=row[2], g=row[3]).data
+            st = E.npad_run(E.HermitianOperator(h), tgt, tol=1e-12)
+            assert st.applied == res.applied[b]
+            np.testing.assert_array_equal(res.operator(b).data, st.current.data)
+    finally:
+        if old is not None:
+            os.environ["QCH_NPAD_WARP"] = old
+
+
+def test_config4_sweep_full_size(E):
+    # BASELINE config 4: 1024 (g, Delta) points of a dim-1024 transmon x
+    # resonator, subspace target of 10 levels; sampled points vs the oracle,
+    # size-independent properties on all of them
+    import torch
+
+    nq, nr = 4, 256
+    pts = E.sweep_points(32, 32)
+    tgt = E.sweep_target(nr)
+    res = E.npad_sweep_transmon(pts, nq, nr, tgt, tol=1e-12)
+    assert bool(np.all(res.converged))
+    assert 300_000 < int(np.sum(res.applied)) < 600_000
+    for b in (0, 31, 512, 700, 1023):
+        row = pts[b]
+        h = E.transmon_resonator_hamiltonian(nq, nr, omega_q=row[0], alpha=row[1], omega_r=row[2], g=row[3]).data
+        ref = npad_oracle.run_incremental(h, tgt, tol=1e-12)
+        assert res.applied[b] == ref["applied"]
+        assert rel_fro(res.operator(b).data, ref["h"]) <= TOL_F
+    # every output is bitwise Hermitian and keeps its trace
+    mats = res.matrices if hasattr(res, "matrices") else None
+    if mats is not None:
+        for b in range(0, 1024, 97):
+            m = mats[b]
+            assert bool(torch.equal(m, m.conj().T))
