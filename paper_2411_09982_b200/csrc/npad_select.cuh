@@ -61,32 +61,37 @@ __device__ __forceinline__ double cand_m(Cand& a) {
   return a.m;
 }
 
-// near-tie resolution with exact numpy magnitudes (out of line)
-static __device__ __noinline__ bool cand_better_exact(Cand& a, Cand& b) {
-  double ma = cand_m(a), mb = cand_m(b);
-  if (ma != mb) return ma > mb;
-  return a.cr < b.cr;
+// near-tie resolution with exact numpy magnitudes (out of line; operands by
+// value so the callers' candidates stay in registers)
+static __device__ __noinline__ bool cand_better_exact_v(double2 av, double am, unsigned acr, double2 bv, double bm,
+                                                        unsigned bcr) {
+  if (am < 0.0) am = np_cabs(av.x, av.y);
+  if (bm < 0.0) bm = np_cabs(bv.x, bv.y);
+  if (am != bm) return am > bm;
+  return acr < bcr;
 }
 
 // a strictly before b in the reference order (mag desc, c asc, r asc)
-__device__ __forceinline__ bool cand_better(Cand& a, Cand& b) {
+__device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
   if (!(a.q > 0.0)) return false;
   if (!(b.q > 0.0)) return true;
   if (a.q > b.q * (1.0 + kRel)) return true;
   if (b.q > a.q * (1.0 + kRel)) return false;
-  return cand_better_exact(a, b);
+  return cand_better_exact_v(a.v, a.m, a.cr, b.v, b.m, b.cr);
 }
 
-__device__ __forceinline__ void cand_take(Cand& best, Cand c) {
+__device__ __forceinline__ void cand_take(Cand& best, const Cand& c) {
   if (cand_better(c, best)) best = c;
 }
 
-static __device__ __noinline__ int warp_argmax_exact(Cand& c, bool nearf) {
+static __device__ __noinline__ int warp_argmax_exact(double2 v, double m0, unsigned cr0, bool nearf) {
   double m = -1.0;
   unsigned cr = 0xffffffffu;
+  double mine = -1.0;
   if (nearf) {
-    m = cand_m(c);
-    cr = c.cr;
+    mine = (m0 < 0.0) ? np_cabs(v.x, v.y) : m0;
+    m = mine;
+    cr = cr0;
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -97,12 +102,11 @@ static __device__ __noinline__ int warp_argmax_exact(Cand& c, bool nearf) {
       cr = ocr;
     }
   }
-  const unsigned w = __ballot_sync(kFull, nearf && c.m == m && c.cr == cr);
+  const unsigned w = __ballot_sync(kFull, nearf && mine == m && cr0 == cr);
   return __ffs(w) - 1;
 }
 
 // winner lane of the warp (all lanes agree), -1 if no lane has a candidate.
-// May fill c.m for near-tie lanes.
 __device__ __forceinline__ int warp_argmax(Cand& c) {
   const unsigned long long b = (c.q > 0.0) ? (unsigned long long)__double_as_longlong(c.q) : 0ull;
   const unsigned hi = (unsigned)(b >> 32);
@@ -114,7 +118,7 @@ __device__ __forceinline__ int warp_argmax(Cand& c) {
   const bool nearf = (c.q > 0.0) && (c.q >= qs * (1.0 - kRel));
   const unsigned near = __ballot_sync(kFull, nearf);
   if (__popc(near) == 1) return __ffs(near) - 1;
-  return warp_argmax_exact(c, nearf);
+  return warp_argmax_exact(c.v, c.m, c.cr, nearf);
 }
 
 // Rotation scalars for the device loop: same mathematics as

@@ -78,10 +78,57 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
   return o;
 }
 
+// Per-lane running best of a row's candidates H[t, x] over the lane's
+// columns, visited in increasing x.  For a fixed row t the reference's
+// tie-break (magnitude desc, then lower-triangle (c, r) asc) is simply x asc,
+// so a strictly larger key replaces the best; keys within the certification
+// band (npad_select.cuh) are resolved with exact numpy magnitudes, equal ones
+// keep the earlier (smaller) x.
+struct LaneBest {
+  double hi, lo;  // certified band of the current best key
+  int x;
+  double2 v;      // H[t, x]
+};
+__device__ __forceinline__ void lb_init(LaneBest& b) {
+  b.hi = 0.0;
+  b.lo = 1.0e308;
+  b.x = -1;
+  b.v = make_double2(0.0, 0.0);
+}
+static __device__ __noinline__ bool mag_greater(double2 a, double2 b) {
+  return np_cabs(a.x, a.y) > np_cabs(b.x, b.y);
+}
+__device__ __forceinline__ void lb_take(LaneBest& b, double2 v, int x) {
+  const double q = fma(v.x, v.x, v.y * v.y);
+  if (q > b.hi) {
+    b.hi = q * (1.0 + kRel);
+    b.lo = q * (1.0 - kRel);
+    b.x = x;
+    b.v = v;
+  } else if (q >= b.lo && mag_greater(v, b.v)) {
+    b.hi = q * (1.0 + kRel);
+    b.lo = q * (1.0 - kRel);
+    b.x = x;
+    b.v = v;
+  }
+}
+
+// rotate_rows (qch_math.cuh, npad.py:136-137) with the real-by-complex
+// products as two rounded multiplies: numpy's (c + 0j) * z gives the same
+// values for finite z (up to the sign of an exact zero), in 16 instead of 24
+// FP64 instructions
+__device__ __forceinline__ void rotate_rows_fast(double c, cplx s, cplx ri, cplx rj, cplx* ni, cplx* nj) {
+  const cplx b = np_cmul(cconj(s), rj);
+  *ni = mkc(QSUB(QMUL(c, ri.re), b.re), QSUB(QMUL(c, ri.im), b.im));
+  const cplx d = np_cmul(s, ri);
+  *nj = mkc(QADD(d.re, QMUL(c, rj.re)), QADD(d.im, QMUL(c, rj.im)));
+}
+
 __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ double2 conj2(double2 v) { return make_double2(v.x, -v.y); }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int W>
 __device__ __forceinline__ void cpa_wait() {
@@ -91,6 +138,7 @@ __device__ __forceinline__ void cpa_wait() {
 // per-warp shared-memory layout
 struct WarpSm {
   double2 ring[kStages][2][kStageCols];  // 16 KB
+  double2 diag[2];
   double2 fold[32];
   double2 stale_v[2][kStaleCap];
   int stale_c[2][kStaleCap];
@@ -135,26 +183,32 @@ __device__ __forceinline__ int gather_stale(const Touch& tc, const double2* __re
   }
   return cnt;
 }
-__device__ __forceinline__ double2 conj2(double2 v) { return make_double2(v.x, -v.y); }
-
 // write the columns of every touched row where that row is the newer one:
 // afterwards the matrix in memory is exactly the eagerly updated one
 __device__ void flush_columns(Touch& tc, double2* __restrict__ h, int n, int lane) {
+  double2* flat = &tc.sm->ring[0][0][0];
+  constexpr int kFlat = kStages * 2 * kStageCols;
   for (int k = 0; k < tc.count; ++k) {
     const int y = tc.sm->touch_row[k];
     const int wy = tc.sm->touch_w[k];
     const double2* __restrict__ row = h + (size_t)y * n;
-    for (int x = lane; x < n; x += 32) {
-      if (x == y) continue;
-      int wx = 0;
-      if ((tc.bits[x >> 5] >> (x & 31)) & 1u) {
-        for (int q = 0; q < tc.count; ++q)
-          if (tc.sm->touch_row[q] == x) wx = tc.sm->touch_w[q];
+    for (int base = 0; base < n; base += kFlat) {
+      const int cnt = min(kFlat, n - base);
+      for (int q = lane; q < cnt; q += 32) cpa16(flat + q, row + base + q);
+      cpa_commit();
+      cpa_wait<0>();
+      __syncwarp();
+      for (int q = lane; q < cnt; q += 32) {
+        const int x = base + q;
+        if (x == y) continue;
+        int wx = 0;
+        if ((tc.bits[x >> 5] >> (x & 31)) & 1u) {
+          for (int p = 0; p < tc.count; ++p)
+            if (tc.sm->touch_row[p] == x) wx = tc.sm->touch_w[p];
+        }
+        if (wx < wy) h[(size_t)x * n + y] = conj2(flat[q]);
       }
-      if (wx < wy) {
-        const double2 v = row[x];
-        h[(size_t)x * n + y] = make_double2(v.x, -v.y);
-      }
+      __syncwarp();
     }
   }
   __syncwarp();
@@ -183,15 +237,18 @@ __device__ __forceinline__ void touch(Touch& tc, int r, int w, int lane) {
   __syncwarp();
 }
 
+// EK: exact keys (q := numpy |z|) for matrices whose entries could leave the
+// normal range of |z|^2 (npad.cu:exact_keys) — the generic candidate path.
+template <bool EK>
 __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restrict__ jobs, int njobs,
                                                               NpadCommon2 cm) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   const int n = cm.n, nT = cm.n_target;
-  const bool ek = cm.ek != 0;
+  constexpr bool ek = EK;
   const int nwords = (n + 31) / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   WarpSm* wsm = (WarpSm*)smem + wib;
-  int* s_kof = (int*)(smem + sizeof(WarpSm) * wpb);           // x -> index in T, -1 outside (block-shared)
+  int* s_kof = (int*)(smem + sizeof(WarpSm) * wpb);  // x -> index in T, -1 outside (block-shared)
   unsigned* s_bits = (unsigned*)(s_kof + n) + (size_t)wib * nwords;
 
   for (int x = threadIdx.x; x < n; x += blockDim.x) s_kof[x] = -1;
@@ -204,6 +261,12 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
   NpadJob2* job = jobs + jb;
   double2* __restrict__ h = job->h;
   for (int k = lane; k < nwords; k += 32) s_bits[k] = 0u;
+  // T membership of this lane's columns x = 32 k + lane (n <= 1024: a register)
+  const bool small_n = n <= 1024;
+  unsigned tmask = 0u;
+  if (small_n)
+    for (int k = 0; k * 32 + lane < n; ++k)
+      if (s_kof[k * 32 + lane] >= 0) tmask |= 1u << k;
   Touch tc{wsm, s_bits, 0};
   Cand mine = cand_none();  // lane l: T-row l
   int my_t = -1;
@@ -215,9 +278,12 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
     mine.v = job->st_v[lane];
   }
   __syncwarp();
+  auto in_T = [&](int x) -> bool { return small_n ? ((tmask >> (x >> 5)) & 1u) != 0u : s_kof[x] >= 0; };
 
   long long applied = job->applied;
   const double thr = job->threshold;
+  int* const pivots = job->pivots;
+  const long long pivot_cap = job->pivot_cap;
   int status = 0;
   long long rescans = 0;
   int clock = 0;
@@ -254,11 +320,14 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
     // matrix is then fully consistent and nothing is stale)
     if (tc.count + 2 > kTouchCap) flush_columns(tc, h, n, lane);
 
-    // ---- stale lists + their async gathers, then the ring (rows i, j); the
-    // gathers ride in the first commit group
+    // ---- stale lists + their async gathers and the two diagonal entries
+    // (rows own their diagonal: never stale) ride in the first commit group
+    // with ring stage 0; the ring streams rows i, j
     const int wi = row_clock(tc, i, lane), wj = row_clock(tc, j, lane);
     const int ns_i = gather_stale(tc, h, n, i, wi, 0, lane);
     const int ns_j = gather_stale(tc, h, n, j, wj, 1, lane);
+    if (lane == 0) cpa16(&wsm->diag[0], ri_p + i);
+    if (lane == 1) cpa16(&wsm->diag[1], rj_p + j);
     auto issue = [&](int stg) {
       if (stg < nstage) {
         const int slot = stg % kStages;
@@ -275,25 +344,29 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
     };
 #pragma unroll
     for (int stg = 0; stg < kStages - 1; ++stg) issue(stg);
-    // the diagonal lives in its own row (never stale)
-    const double hii = h[(size_t)i * n + i].x, hjj = h[(size_t)j * n + j].x;
-    // rotation scalars (every lane, same values): givens_rotation_matrix +
-    // _block_params (npad.py:101-128)
-    const cplx v = d2c(piv.v);
-    double c;
-    cplx s;
-    givens_fast(v, hii, hjj, &c, &s);
-    if (lane == 0 && job->pivots != nullptr && applied < job->pivot_cap) {
-      job->pivots[2 * applied] = i;
-      job->pivots[2 * applied + 1] = j;
+    if (lane == 0 && pivots != nullptr && applied < pivot_cap) {
+      pivots[2 * applied] = i;
+      pivots[2 * applied + 1] = j;
     }
+    const cplx v = d2c(piv.v);
+    double c = 0.0, hii = 0.0, hjj = 0.0;
+    cplx s = mkc(0.0, 0.0);
 
-    Cand pt = cand_none();
+    LaneBest lbt;  // new row t (fast keys)
+    lb_init(lbt);
+    Cand pt = cand_none();  // new row t (exact keys)
 #pragma unroll 1
     for (int stg = 0; stg < nstage; ++stg) {
       issue(stg + kStages - 1);
       cpa_wait<kStages - 1>();
       __syncwarp();
+      if (stg == 0) {
+        // rotation scalars (every lane, same values): givens_rotation_matrix
+        // + _block_params (npad.py:101-128)
+        hii = wsm->diag[0].x;
+        hjj = wsm->diag[1].x;
+        givens_fast(v, hii, hjj, &c, &s);
+      }
       const int slot = stg % kStages;
       const int base = stg * kStageCols;
       // patch stale columns of this stage
@@ -306,25 +379,41 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
         if (y >= base && y < base + kStageCols) wsm->ring[slot][1][y - base] = conj2(wsm->stale_v[1][q]);
       }
       __syncwarp();
+      // rotate this stage.  Columns i, j get provisional values here; the 2x2
+      // block below overwrites them (same warp, after a __syncwarp).
+      const double2* __restrict__ ra = &wsm->ring[slot][0][lane];
+      const double2* __restrict__ rb = &wsm->ring[slot][1][lane];
+      double2* __restrict__ oi = h + (size_t)i * n + base + lane;
+      double2* __restrict__ oj = h + (size_t)j * n + base + lane;
+      const bool full = base + kStageCols <= n;
+      const unsigned tbits = small_n ? (tmask >> (base >> 5)) : 0u;
 #pragma unroll
       for (int k = 0; k < kStageCols / 32; ++k) {
         const int x = base + k * 32 + lane;
-        if (x >= n || x == i || x == j) continue;
+        if (!full && x >= n) break;
         cplx ni, nj;
-        rotate_rows(c, s, d2c(wsm->ring[slot][0][k * 32 + lane]), d2c(wsm->ring[slot][1][k * 32 + lane]), &ni, &nj);
-        h[(size_t)i * n + x] = c2d(ni);
-        h[(size_t)j * n + x] = c2d(nj);
-        const int kx = s_kof[x];
-        if (kx < 0) {
-          cand_take(pt, tcand(c2d(t_is_i ? ni : nj), t, x, ek));
-        } else {
+        rotate_rows_fast(c, s, d2c(ra[k * 32]), d2c(rb[k * 32]), &ni, &nj);
+        oi[k * 32] = c2d(ni);
+        oj[k * 32] = c2d(nj);
+        const bool inTx = small_n ? ((tbits >> k) & 1u) != 0u : s_kof[x] >= 0;
+        if (!inTx) {
+          if (x != u) {
+            if (EK) {
+              cand_take(pt, tcand(c2d(t_is_i ? ni : nj), t, x, ek));
+            } else {
+              lb_take(lbt, c2d(t_is_i ? ni : nj), x);
+            }
+          }
+        } else if (x != t) {
           // x = t' in T: new H[t', u] = conj(new H[u, t'])
-          wsm->fold[kx] = c2d(cconj(t_is_i ? nj : ni));
+          wsm->fold[s_kof[x]] = c2d(cconj(t_is_i ? nj : ni));
         }
       }
       __syncwarp();  // ring slot reuse
     }
     cpa_wait<0>();
+    __syncwarp();  // provisional writes of columns i, j before the 2x2 block
+    if (!EK && lbt.x >= 0) pt = tcand(lbt.v, t, lbt.x, ek);
     // the 2x2 block (npad.py:136-144 incl. the Hermitian pin) and its
     // coupling H[j, i] as a candidate of T-row t
     if (lane == 0) {
@@ -363,8 +452,8 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
       }
       rm = __ballot_sync(kFull, need);
     }
-    // rescans: the whole row in one shot through the ring (8 stages of 128
-    // columns = 1024 columns per pass), stale columns patched from gathers
+    // rescans: the whole row in one shot through the ring (1024 columns per
+    // pass), stale columns patched from gathers
     while (rm) {
       const int kr = __ffs(rm) - 1;
       rm &= rm - 1;
@@ -376,6 +465,8 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
       double2* flat = &wsm->ring[0][0][0];
       constexpr int kFlat = kStages * 2 * kStageCols;
       Cand pr = cand_none();
+      LaneBest lbr;
+      lb_init(lbr);
       for (int base = 0; base < n; base += kFlat) {
         const int cnt = min(kFlat, n - base);
         for (int q = lane; q < cnt; q += 32) cpa16(flat + q, row + base + q);
@@ -389,10 +480,16 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
         __syncwarp();
         for (int q = lane; q < cnt; q += 32) {
           const int x = base + q;
-          if (s_kof[x] < 0) cand_take(pr, tcand(flat[q], tr, x, ek));
+          if (in_T(x)) continue;
+          if (EK) {
+            cand_take(pr, tcand(flat[q], tr, x, ek));
+          } else {
+            lb_take(lbr, flat[q], x);
+          }
         }
         __syncwarp();
       }
+      if (!EK && lbr.x >= 0) pr = tcand(lbr.v, tr, lbr.x, ek);
       const int wl = warp_argmax(pr);
       const Cand best = (wl >= 0) ? shfl_cand(pr, wl) : cand_none();
       if (lane == kr) mine = best;
@@ -425,10 +522,11 @@ int npad_launch_trows_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cud
   while (wpb > 1 && trows_warp_smem(cm.n, wpb) > (size_t)max_smem_optin()) wpb >>= 1;
   const size_t smem = trows_warp_smem(cm.n, wpb);
   if (smem > (size_t)max_smem_optin()) return fail(QCH_ERR_UNSUPPORTED, "npad: warp T-rows driver shared memory");
-  QCH_CUDA(cudaFuncSetAttribute(npad_trows_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = cm.ek ? npad_trows_warp_kernel<true> : npad_trows_warp_kernel<false>;
+  QCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (njobs + wpb - 1) / wpb;
   void* pr = prof_begin("npad_run_kernel", st);
-  npad_trows_warp_kernel<<<grid, 32 * wpb, smem, st>>>(jobs, njobs, cm);
+  kern<<<grid, 32 * wpb, smem, st>>>(jobs, njobs, cm);
   prof_end(pr, st);
   QCH_LAUNCH_CHECK("npad_trows_warp_kernel");
   note_launch(1);
