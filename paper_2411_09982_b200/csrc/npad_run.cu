@@ -25,6 +25,7 @@
 // qch_hermitian_exact_c128) are updated by reading rows only and writing the
 // columns as conjugates: 96*N bytes per rotation.
 #include <cstdlib>
+#include <cstring>
 
 #include "npad_run.h"
 #include "npad_select.cuh"
@@ -773,10 +774,17 @@ int npad_launch2(NpadJob2* jobs, int njobs, const NpadCommon2& cm, bool herm, bo
                  bool allow_smem_h, cudaStream_t st) {
   int cpt, threads;
   shape_for(cm.n, pref_threads, &cpt, &threads);
-  // many independent chains (the sweep): one warp per chain
-  const char* wenv = getenv("QCH_NPAD_WARP");
-  const bool warp_mode = wenv ? atoi(wenv) != 0 : njobs > 1;
-  if (trows && warp_mode) return npad_launch_trows_warp(jobs, njobs, cm, st);
+  // many independent chains (the sweep): one warp per chain with lazy
+  // columns (npad_warp.cu); QCH_NPAD_DRIVER=warp|cta|block overrides (cta:
+  // npad_cta.cu, lower per-rotation latency when few chains run)
+  if (trows) {
+    const char* d = getenv("QCH_NPAD_DRIVER");
+    const char* wenv = getenv("QCH_NPAD_WARP");  // legacy switch: 1 = many-chain driver for any batch
+    const bool many = wenv ? atoi(wenv) != 0 : njobs > 1;
+    if (d != nullptr && strcmp(d, "warp") == 0) return npad_launch_trows_warp(jobs, njobs, cm, st);
+    if (d != nullptr && strcmp(d, "cta") == 0) return npad_launch_trows_cta(jobs, njobs, cm, st);
+    if ((d == nullptr || strcmp(d, "block") != 0) && many) return npad_launch_trows_warp(jobs, njobs, cm, st);
+  }
   if (trows) {
     switch (cpt) {
       case 1: return launch_trows_t<1>(jobs, njobs, cm, threads, st);

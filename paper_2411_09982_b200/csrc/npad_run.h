@@ -35,6 +35,7 @@ bool npad_use_trows(const NpadCommon2& cm, bool herm);
 int npad_state_init(const double2* h, int64_t batch, const NpadCommon2& cm, bool trows, double* q, int* c,
                     double2* v, cudaStream_t st);
 int npad_launch_trows_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st);
+int npad_launch_trows_cta(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st);
 int npad_launch2(NpadJob2* jobs, int njobs, const NpadCommon2& cm, bool herm, bool trows, int pref_threads,
                  bool allow_smem_h, cudaStream_t st);
 

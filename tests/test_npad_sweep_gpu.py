@@ -1,4 +1,4 @@
-"""The warp-per-chain subspace driver (npad_warp.cu: lazy columns, cp.async
+"""The many-chain subspace drivers (npad_warp.cu, npad_cta.cu: lazy columns)
 ring) — the BASELINE config-4 sweep path — against the oracle and against the
 eager block driver, bit for bit."""
 import os
@@ -20,15 +20,16 @@ def E():
     return eff
 
 
-@pytest.fixture
-def warp_mode():
-    old = os.environ.get("QCH_NPAD_WARP")
-    os.environ["QCH_NPAD_WARP"] = "1"
-    yield
+@pytest.fixture(params=["cta", "warp"])
+def warp_mode(request):
+    """Force a many-chain driver (npad_cta.cu / npad_warp.cu) even for one chain."""
+    old = os.environ.get("QCH_NPAD_DRIVER")
+    os.environ["QCH_NPAD_DRIVER"] = request.param
+    yield request.param
     if old is None:
-        del os.environ["QCH_NPAD_WARP"]
+        del os.environ["QCH_NPAD_DRIVER"]
     else:
-        os.environ["QCH_NPAD_WARP"] = old
+        os.environ["QCH_NPAD_DRIVER"] = old
 
 
 def _herm(n, seed, scale=1.0):
@@ -58,7 +59,7 @@ def test_warp_driver_random_vs_oracle(E, warp_mode, n, nt, seed):
     assert rel_fro(st.current.data, ref["h"]) <= TOL_F
 
 
-def test_warp_driver_touched_overflow_flush(E, warp_mode):
+def test_driver_many_touched_rows(E, warp_mode):
     # a dense chain that touches far more than 128 distinct rows: exercises the
     # mid-chain column flush of the lazy scheme
     n = 420
@@ -78,7 +79,8 @@ def test_lazy_columns_bit_identical_to_eager(E):
     nq, nr = 4, 64
     tgt = E.sweep_target(nr)
     res = E.npad_sweep_transmon(pts, nq, nr, tgt, tol=1e-12)
-    old = os.environ.pop("QCH_NPAD_WARP", None)
+    old = os.environ.get("QCH_NPAD_DRIVER")
+    os.environ["QCH_NPAD_DRIVER"] = "block"
     try:
         for b, row in enumerate(pts):
             h = E.transmon_resonator_hamiltonian(nq, nr, omega_q=row[0], alpha=row[1], omega_r=row[2], g=row[3]).data
@@ -86,8 +88,10 @@ def test_lazy_columns_bit_identical_to_eager(E):
             assert st.applied == res.applied[b]
             np.testing.assert_array_equal(res.operator(b).data, st.current.data)
     finally:
-        if old is not None:
-            os.environ["QCH_NPAD_WARP"] = old
+        if old is None:
+            del os.environ["QCH_NPAD_DRIVER"]
+        else:
+            os.environ["QCH_NPAD_DRIVER"] = old
 
 
 def test_config4_sweep_full_size(E):
