@@ -1,6 +1,6 @@
-"""The many-chain subspace drivers (npad_warp.cu, npad_cta.cu: lazy columns)
-ring) — the BASELINE config-4 sweep path — against the oracle and against the
-eager block driver, bit for bit."""
+"""The many-chain subspace drivers (npad_warp.cu, npad_cta.cu: lazy
+columns) — the BASELINE config-4 sweep path — against the oracle and against
+the eager block driver, bit for bit."""
 import os
 
 import numpy as np
