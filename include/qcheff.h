@@ -126,7 +126,7 @@ int qch_magnus_assemble_c128(const void* d_h0, const void* d_hk, const void* d_c
                              int order, void* d_hbar, void* stream);
 
 /* _expm_minus_i (expm.py:56-71) for a batch: U_b = exp(-i H_b), scaling and
- * squaring Taylor order 18.  d_work: scratch of 3*batch*n*n complex128.
+ * squaring Taylor (degree <= 18, Paterson-Stockmeyer).  d_work: scratch of 4*batch*n*n complex128.
  * Checks finiteness (expm.py:81-82, 97-99): QCH_ERR_NONFINITE, first bad
  * item index in *bad_index (host, nullable). */
 int qch_expm_minus_i_batch_c128(const void* d_h, int64_t batch, int64_t n, void* d_u, void* d_work,

@@ -17,6 +17,7 @@
 //    complex GEMM with the fused "term = term@a/k; out += term" epilogue
 //    (zgemm.cu), squaring, then the sequential ordered product.
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "qch_internal.h"
@@ -30,6 +31,7 @@ int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, i
 int zgemm_taylor(const double2* a, const double2* b, double2* t, double2* o, int n, int64_t batch, double inv_k,
                  cudaStream_t st);
 int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st);
+int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st);
 int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const double2* d_psi0, double2* d_traj,
                         int64_t* bad_index, unsigned long long* d_flags_out, cudaStream_t st);
 
@@ -306,6 +308,38 @@ __global__ void taylor_init_kernel(const double2* __restrict__ h, int n, int64_t
 }
 
 // out = (s_b > step) ? sq : out
+// Q = c0 I + c1 a + c2 a^2 (elementwise, batched)
+__global__ void ps_q_kernel(const double2* __restrict__ p1, const double2* __restrict__ p2, int64_t nn, int n,
+                            int64_t batch, double2* __restrict__ q, double c0, double c1, double c2) {
+  const int64_t total = nn * batch;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = k % nn;
+    const double2 a = p1[k], b = p2[k];
+    const double d = (e / n == e % n) ? c0 : 0.0;
+    q[k] = make_double2(fma(c2, b.x, fma(c1, a.x, d)), fma(c2, b.y, c1 * a.y));
+  }
+}
+
+// host copies of the degree table / Taylor coefficients (magnus_small.cuh)
+static const double kThetaH[19] = {
+    6.9388939039072284e-18, 3.7252902984619141e-09, 3.4658824783938236e-06, 0.00011359922596461176,
+    0.00096403832316153276, 0.0041346344980966003,  0.011958436387519561,   0.026968161873314821,
+    0.051431375833317965,   0.087117484748903212,   0.13524818677402944,    0.19654813817446753,
+    0.27133475643086408,    0.3596131914026986,     0.46116109021995333,    0.57559811770713287,
+    0.70244016939905507,    0.84114022780138098,    0.99111835560814376};
+static int taylor_degree(double nu) {
+  if (!(nu == nu)) return kTaylorOrder;
+  int m = kTaylorOrder;
+  while (m > 1 && nu <= kThetaH[m - 1]) --m;
+  return m;
+}
+static double coef_of(int k, int m) {
+  if (k > m) return 0.0;
+  double f = 1.0;
+  for (int q = 2; q <= k; ++q) f *= q;
+  return 1.0 / f;
+}
+
 __global__ void select_square_kernel(double2* __restrict__ out, const double2* __restrict__ sq, int64_t nn,
                                      int64_t batch, const int* __restrict__ sarr, int step) {
   int64_t total = nn * batch;
@@ -484,32 +518,69 @@ struct DevBuf {
 
 // exp(-i H) for a batch of n x n (n > 4) with the DMMA GEMM; d_u receives U.
 // work: 3*batch*n*n complex.  sarr: int[batch] (device).
+// exp(-i H) for a batch of n x n (n > 4) on the DMMA GEMM.  Same scaling as
+// the reference (expm.py:56-71: numpy max row sum of |a|, target 0.5, then s
+// squarings); the Taylor polynomial is cut at the degree m whose remainder is
+// < 2^-56 (kTheta; m = 12 for the config-5 intervals) and evaluated by
+// Paterson-Stockmeyer with a^3 blocks:
+//     p(a) = sum_j (a^3)^j Q_j,   Q_j = c_3j I + c_3j+1 a + c_3j+2 a^2,
+//     X <- Q_j + a^3 X  (one GEMM with an accumulate epilogue per step)
+// i.e. 2 + m/3 GEMMs (6 at m = 12) instead of the reference's 17.
+// work: 4 * batch * n * n complex.  sarr: int[batch] (device).
 static int expm_generic(const double2* h, int64_t batch, int n, double2* u, double2* work, int* sarr,
                         unsigned long long* norm, cudaStream_t st) {
   const int64_t nn = (int64_t)n * n;
-  double2* a = work;
-  double2* t0 = work + batch * nn;
-  double2* t1 = work + 2 * batch * nn;
+  double2* p1 = work;
+  double2* p2 = work + batch * nn;
+  double2* p3 = work + 2 * batch * nn;
+  double2* xb = work + 3 * batch * nn;
   QCH_CUDA(cudaMemsetAsync(norm, 0, sizeof(unsigned long long) * batch, st));
   rownorm_kernel<<<(int)((n * batch + 127) / 128), 128, 0, st>>>(h, n, batch, norm);
-  taylor_init_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, n, batch, norm, a, t0, u, sarr);
+  taylor_init_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, n, batch, norm, p1, p2, u, sarr);
   QCH_LAUNCH_CHECK("taylor_init_kernel");
   note_launch(2);
-  for (int k = 2; k <= kTaylorOrder; ++k) {
-    int rc = zgemm_taylor(t0, a, t1, u, n, batch, QDIV(1.0, (double)k), st);
-    if (rc) return rc;
-    std::swap(t0, t1);
-  }
-  // squaring: s_b times for matrix b
+  // degree from the scaled norms (one small D2H)
+  std::vector<unsigned long long> hn(batch);
   std::vector<int> hs(batch);
+  QCH_CUDA(cudaMemcpyAsync(hn.data(), norm, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost, st));
   QCH_CUDA(cudaMemcpyAsync(hs.data(), sarr, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
   QCH_CUDA(cudaStreamSynchronize(st));
-  int smax = 0;
-  for (int v : hs) smax = std::max(smax, v);
+  int m = 1, smax = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    double nu;
+    memcpy(&nu, &hn[b], sizeof nu);
+    nu = ldexp(nu, -hs[b]);
+    m = std::max(m, taylor_degree(nu));
+    smax = std::max(smax, hs[b]);
+  }
+  // powers a, a^2, a^3 (p1 holds a; taylor_init also left a in p2)
+  if (m >= 2) {
+    if (int rc = zgemm(p1, p1, p2, n, n, n, batch, nn, nn, nn, st)) return rc;
+  }
+  const int r = m / 3;
+  if (r >= 1) {
+    if (int rc = zgemm(p2, p1, p3, n, n, n, batch, nn, nn, nn, st)) return rc;
+  }
+  // X = Q_r, then X <- Q_j + a^3 X for j = r-1 .. 0; the last step lands in u
+  double2* bufs[2] = {((r & 1) ? xb : u), ((r & 1) ? u : xb)};
+  double2* x = bufs[0];
+  ps_q_kernel<<<grid_for(nn * batch), 256, 0, st>>>(p1, p2, nn, n, batch, x, coef_of(3 * r, m), coef_of(3 * r + 1, m),
+                                                    coef_of(3 * r + 2, m));
+  note_launch(1);
+  for (int j = r - 1, q = 1; j >= 0; --j, q ^= 1) {
+    double2* y = bufs[q];
+    ps_q_kernel<<<grid_for(nn * batch), 256, 0, st>>>(p1, p2, nn, n, batch, y, coef_of(3 * j, m),
+                                                      coef_of(3 * j + 1, m), coef_of(3 * j + 2, m));
+    note_launch(1);
+    if (int rc = zgemm_accum(p3, x, y, n, batch, st)) return rc;
+    x = y;
+  }
+  QCH_LAUNCH_CHECK("ps_q_kernel");
+  // squaring: s_b times for matrix b
   for (int step = 0; step < smax; ++step) {
-    int rc = zgemm(u, u, t0, n, n, n, batch, nn, nn, nn, st);
+    int rc = zgemm(u, u, p1, n, n, n, batch, nn, nn, nn, st);
     if (rc) return rc;
-    select_square_kernel<<<grid_for(nn * batch), 256, 0, st>>>(u, t0, nn, batch, sarr, step);
+    select_square_kernel<<<grid_for(nn * batch), 256, 0, st>>>(u, p1, nn, batch, sarr, step);
     QCH_LAUNCH_CHECK("select_square_kernel");
     note_launch(1);
   }
@@ -797,17 +868,17 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
     if (K > 0) {
       if (int rc = qch_magnus_coefficients(d_sig, K, S, M, dt, order, c1, c2, stream)) return rc;
     }
-    // chunk so that 5 matrices per interval stay within ~12 GiB
+    // chunk so that 6 matrices per interval (Hbar, U, 4 of expm work) stay within ~12 GiB
     const size_t per = sizeof(double2) * (size_t)nn;
-    int64_t mb = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)((12ull << 30) / (5 * per))));
+    int64_t mb = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)((12ull << 30) / (6 * per))));
     mb = std::min<int64_t>(mb, 4096);
     DevBuf buf(st);
-    QCH_CUDA(buf.alloc(per * mb * 5 + sizeof(double2) * N + sizeof(int) * mb + sizeof(unsigned long long) * mb +
+    QCH_CUDA(buf.alloc(per * mb * 6 + sizeof(double2) * N + sizeof(int) * mb + sizeof(unsigned long long) * mb +
                        sizeof(double) * 2 * mb + 64));
     double2* hbar = buf.as<double2>();
     double2* ubuf = hbar + nn * mb;
-    double2* work = ubuf + nn * mb;  // 3 * mb
-    double2* psi = work + 3 * nn * mb;
+    double2* work = ubuf + nn * mb;  // 4 * mb
+    double2* psi = work + 4 * nn * mb;
     int* sarr = (int*)(psi + N);
     unsigned long long* norms = (unsigned long long*)(sarr + mb + (mb & 1));
     double* vbuf = (double*)(norms + mb);

@@ -17,12 +17,13 @@
 //                                             complex by k as x*(1/k))
 //   DEFECT  sum |(A B^H) - I|^2 into a per-batch accumulator (unitarity audit,
 //           npad.py:257, expm.py:35-38)
+//   ACCUM   C += A B   (Paterson-Stockmeyer Horner steps of exp(-iH))
 #include "qch_internal.h"
 #include "qch_math.cuh"
 
 namespace qch {
 
-enum { ZG_STORE = 0, ZG_TAYLOR = 1, ZG_DEFECT = 2 };
+enum { ZG_STORE = 0, ZG_TAYLOR = 1, ZG_DEFECT = 2, ZG_ACCUM = 3 };
 
 struct ZgemmArgs {
   const double2* a;
@@ -185,6 +186,9 @@ __global__ void __launch_bounds__(128) zgemm_kernel(ZgemmArgs g) {
         const int64_t off = bz * g.sc + (int64_t)r * g.ldc + cidx;
         if (MODE == ZG_STORE) {
           g.c[off] = make_double2(re, im);
+        } else if (MODE == ZG_ACCUM) {
+          const double2 o = g.c[off];
+          g.c[off] = make_double2(o.x + re, o.y + im);
         } else if (MODE == ZG_TAYLOR) {
           double tr = QMUL(re, g.inv_k), ti = QMUL(im, g.inv_k);
           g.c[off] = make_double2(tr, ti);
@@ -228,7 +232,11 @@ static int zgemm_launch(const ZgemmArgs& g, int64_t batch, cudaStream_t st) {
     if (h.o) h.o += done * g.sc;
     if (h.acc) h.acc += done;
     dim3 grid((g.n + BN - 1) / BN, (g.m + BM - 1) / BM, (unsigned)nb);
-    void* pr = prof_begin(MODE == ZG_TAYLOR ? "zgemm_taylor" : (MODE == ZG_STORE ? "zgemm" : "zgemm_defect"), st);
+    void* pr = prof_begin(MODE == ZG_TAYLOR   ? "zgemm_taylor"
+                          : MODE == ZG_STORE  ? "zgemm"
+                          : MODE == ZG_ACCUM  ? "zgemm_accum"
+                                              : "zgemm_defect",
+                          st);
     zgemm_kernel<MODE, BH><<<grid, 128, smem, st>>>(h);
     prof_end(pr, st);
     QCH_LAUNCH_CHECK("zgemm_kernel");
@@ -255,6 +263,18 @@ int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, i
   g.ldb = n;
   g.ldc = n;
   return zgemm_launch<ZG_STORE, false>(g, batch, st);
+}
+
+// C += A @ B   (square n x n, batched contiguous; C must not alias A or B)
+int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st) {
+  ZgemmArgs g{};
+  g.a = a;
+  g.b = b;
+  g.c = c;
+  g.m = g.n = g.k = n;
+  g.sa = g.sb = g.sc = (int64_t)n * n;
+  g.lda = g.ldb = g.ldc = n;
+  return zgemm_launch<ZG_ACCUM, false>(g, batch, st);
 }
 
 // T = (A @ B) * inv_k ; O += T   (square n x n, batched contiguous)
