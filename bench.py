@@ -391,7 +391,10 @@ def sec_npad4096(torch, eff, lib, args, peaks, rotations=None):
             "us_per_rotation_kernel": kms * 1e3 / st.applied,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks[0], "unit": "GB/s", "frac": ach / peaks[0],
                          "bytes_per_rotation": 96 * n, "note": "single greedy chain: latency-bound (see DESIGN.md)",
-                         "traffic": traffic_from_profiles("npad_rows_kernel@npad4096")},
+                         "traffic": (traffic_from_profiles("npad_rows_kernel@npad4096") or 0) / 2000 * st.applied
+                         or None,
+                         "traffic_note": "ncu DRAM bytes of a 2000-rotation launch (tools/prof_round.sh), scaled per "
+                                         "rotation to this launch"},
             "cpu_baseline": {"value": cpu, "unit": "rotations/s", "cores": 1, "kind": "port",
                              "sample": "3 rotations of the same operator, oracle run_full_scan"}}
 
@@ -446,7 +449,7 @@ def sec_sweep(torch, eff, lib, args, peaks, n_points=1024):
             "metric": "NPAD rotations/s", "unit": "rotations/s", "value": rot / (per * 1e-3), "rotations": rot,
             "all_converged": bool(conv.all()), "ms_per_sweep": per,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks[0], "unit": "GB/s", "frac": ach / peaks[0],
-                         "bytes_per_rotation": 96 * n, "traffic": traffic_from_profiles("npad_trows_kernel@sweep")},
+                         "bytes_per_rotation": 96 * n, "traffic": traffic_from_profiles("npad_trows_warp_kernel@sweep")},
             "cpu_baseline": {"value": cpu, "unit": "rotations/s", "cores": 1, "kind": "port",
                              "sample": "first 60 rotations of 2 sweep points, oracle run_full_scan"}}
 
