@@ -426,6 +426,24 @@ extern "C" int qch_npad_run_dense_c128(void* d_h, int64_t n, const int32_t* d_ta
   }
   if (int rc = npad_state_init((const double2*)d_h, 1, cm, trows, rb.q, rb.c, rb.v, st)) return rc;
 
+  // one large full-diagonal chain: the whole GPU (cooperative, npad_coop.cu)
+  {
+    const char* e = getenv("QCH_NPAD_COOP");
+    const bool coop = e ? atoi(e) != 0 : n >= 1024;
+    if (coop && !trows && herm && d_u == nullptr && d_target == nullptr) {
+      long long ap = 0;
+      int stt = 0;
+      const int rc = npad_run_coop((double2*)d_h, ni, threshold, max_iter, cm.ek, rb.q, rb.c, rb.v, d_pivots,
+                                   d_pivots ? pivot_cap : 0, &ap, &stt, st);
+      if (rc == QCH_OK) {
+        *applied = ap;
+        *converged = stt == 0 ? 1 : 0;
+        return QCH_OK;
+      }
+      if (rc != QCH_ERR_UNSUPPORTED) return rc;
+    }
+  }
+
   NpadJob2 job;
   job.h = (double2*)d_h;
   job.u = (double2*)d_u;

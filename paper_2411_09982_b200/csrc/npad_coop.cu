@@ -1,0 +1,404 @@
+// npad_coop.cu — ONE greedy NPAD chain (npad_run, npad.py:320-354) spread
+// over the whole GPU: the full-diagonal driver for large dense operators
+// (BASELINE config 3: dim 4096, 292,068 rotations).
+//
+// A single chain is serial (each pick needs the previous rotation), and one
+// SM cannot move the ~400 KB a dim-4096 rotation touches in less than tens
+// of microseconds.  Here G CTAs (one per SM, cooperative launch) share the
+// chain.  CTA g owns a contiguous block of ROWS R_g (their incremental
+// best-candidate state, in shared memory) and the same block of COLUMNS
+// C_g = R_g.  Per rotation (i, j):
+//
+//   phase A (every CTA, no communication)
+//     * rotate rows i, j on the columns x in C_g (npad.py:136-137), write
+//       them and the mirrored columns H[x, i], H[x, j] (the matrix stays
+//       bitwise Hermitian, npad.py:139-144) — those are rows x in R_g;
+//     * fold the two new entries of each own row x into its best candidate;
+//       rows whose best sat in column i or j are rescanned by the CTA;
+//     * partial bests of the NEW rows i and j over C_g (the 2x2 block's
+//       H[j, i] included by the owner of column i), and the best over the own
+//       rows other than i, j; published to a double-buffered record array;
+//   publish (release), then wait for every CTA's record (acquire);
+//   phase B (every CTA redundantly, identical results)
+//     * combine the G partials into the new row-i / row-j candidates (their
+//       owners store them) and pick the global pivot with the reference
+//       order (npad_select.cuh: certified |z|^2 keys, numpy |z| near ties,
+//       (mag desc, i asc, j asc));
+//     * every CTA keeps a full copy of the diagonal and updates it from the
+//       2x2 block it computes itself, so the rotation scalars need no load.
+//
+// The records carry the rotation count as an epoch (release store after the
+// CTA's matrix writes); waiting for all G records of an epoch (acquire) IS the
+// grid barrier — one per rotation, no atomics.  Bit-identical to the
+// single-CTA driver (same arithmetic, same candidate order).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "npad_run.h"
+#include "npad_select.cuh"
+#include "qch_internal.h"
+
+namespace qch {
+namespace {
+
+constexpr int kCoopThreads = 256;
+constexpr int kCoopWarps = kCoopThreads / 32;
+constexpr int kRescanBatch = 8;  // loads in flight per thread in a row rescan
+
+struct CoopRec {
+  Cand own;   // best over the CTA's rows other than i, j
+  Cand pi;    // new row i over the CTA's columns
+  Cand pj;    // new row j over the CTA's columns
+  int epoch;  // = rotations applied when published (release store; readers acquire)
+};
+
+struct CoopArgs {
+  double2* h;
+  int n;
+  int rows_per;        // rows (and columns) per CTA
+  int ek;
+  double threshold;
+  long long max_iter;
+  const double* st_q;  // initial row state (rows_init_kernel)
+  const int* st_c;
+  const double2* st_v;
+  CoopRec* rec;        // [2][G]; epochs initialised to -1
+  int* pivots;
+  long long pivot_cap;
+  long long* out_applied;
+  int* out_status;
+};
+
+__device__ __forceinline__ int ld_acq(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_rel(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ Cand shfl_cand_p(const Cand& c, int src) {
+  Cand o;
+  o.q = __shfl_sync(kFull, c.q, src);
+  o.m = __shfl_sync(kFull, c.m, src);
+  o.cr = __shfl_sync(kFull, c.cr, src);
+  o.v.x = __shfl_sync(kFull, c.v.x, src);
+  o.v.y = __shfl_sync(kFull, c.v.y, src);
+  return o;
+}
+__device__ __forceinline__ Cand warp_best(Cand c) {
+  const int wl = warp_argmax(c);
+  return (wl >= 0) ? shfl_cand_p(c, wl) : cand_none();
+}
+// three block-wide bests at once (every thread gets them; one barrier pair);
+// s_part: 3 * kCoopWarps entries
+__device__ __forceinline__ void block_best3(Cand& a, Cand& b, Cand& c, Cand* s_part) {
+  const Cand wa = warp_best(a), wb = warp_best(b), wc = warp_best(c);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_part[w] = wa;
+    s_part[kCoopWarps + w] = wb;
+    s_part[2 * kCoopWarps + w] = wc;
+  }
+  __syncthreads();
+  a = s_part[0];
+  b = s_part[kCoopWarps];
+  c = s_part[2 * kCoopWarps];
+#pragma unroll
+  for (int k = 1; k < kCoopWarps; ++k) {
+    cand_take(a, s_part[k]);
+    cand_take(b, s_part[kCoopWarps + k]);
+    cand_take(c, s_part[2 * kCoopWarps + k]);
+  }
+  __syncthreads();
+}
+// block-wide best (every thread gets it); s_part: kCoopWarps entries
+__device__ __forceinline__ Cand block_best_p(const Cand& c, Cand* s_part) {
+  const Cand w = warp_best(c);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = w;
+  __syncthreads();
+  Cand b = s_part[0];
+#pragma unroll
+  for (int k = 1; k < kCoopWarps; ++k) cand_take(b, s_part[k]);
+  __syncthreads();
+  return b;
+}
+
+template <bool EK>
+__global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid_constant__ CoopArgs a) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int G = gridDim.x, g = blockIdx.x;
+  const int n = a.n;
+  constexpr bool ek = EK;
+  const int r0 = g * a.rows_per, r1 = min(n, r0 + a.rows_per);
+  const int nr = max(0, r1 - r0);
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* s_dg = (double*)smem;                  // full diagonal copy
+  Cand* s_row = (Cand*)(smem + (((size_t)8 * n + 15) & ~(size_t)15));  // best candidate of each own row
+  Cand* s_part = s_row + a.rows_per;             // [kCoopWarps] reduction scratch
+  int* s_resc = (int*)(s_part + 3 * kCoopWarps);  // own rows to rescan
+  __shared__ int s_nresc;
+  double2* __restrict__ h = a.h;
+
+  for (int x = tid; x < n; x += kCoopThreads) s_dg[x] = h[(size_t)x * n + x].x;
+  for (int k = tid; k < nr; k += kCoopThreads) {
+    const int x = r0 + k;
+    Cand c = cand_none();
+    if (a.st_q[x] > 0.0) {
+      c.q = a.st_q[x];
+      c.cr = ((unsigned)a.st_c[x] << 16) | (unsigned)x;
+      c.v = a.st_v[x];
+    }
+    s_row[k] = c;
+  }
+  __syncthreads();
+
+  long long applied = 0;
+  int status = 0;
+  int pi_row = -1, pj_row = -1;  // rows whose state comes from the partials of the last rotation
+  // first publication: own bests only
+  {
+    Cand own = cand_none();
+    for (int k = tid; k < nr; k += kCoopThreads) cand_take(own, s_row[k]);
+    own = block_best_p(own, s_part);
+    if (tid == 0) {
+      a.rec[g].own = own;
+      a.rec[g].pi = cand_none();
+      a.rec[g].pj = cand_none();
+      __threadfence();
+      st_rel(&a.rec[g].epoch, 0);
+    }
+  }
+
+  while (true) {
+    // ---- phase B: combine the records, pick the pivot (every CTA)
+    // (waiting for every CTA's record of this epoch is the grid barrier: the
+    // acquire makes each publisher's matrix writes visible)
+    CoopRec* rec = a.rec + (size_t)(applied & 1) * G;
+    if (tid < 32) {
+      for (int k = tid; k < G; k += 32)
+        while (ld_acq(&rec[k].epoch) != (int)applied) {
+        }
+    }
+    __syncthreads();
+    Cand cown = cand_none(), cpi = cand_none(), cpj = cand_none();
+    for (int k = tid; k < G; k += kCoopThreads) {
+      cown = rec[k].own;
+      cpi = rec[k].pi;
+      cpj = rec[k].pj;
+    }
+    block_best3(cown, cpi, cpj, s_part);
+    // the new candidates of the last rotation's rows i, j (their owners keep them)
+    if (pi_row >= r0 && pi_row < r1 && tid == 0) s_row[pi_row - r0] = cpi;
+    if (pj_row >= r0 && pj_row < r1 && tid == 0) s_row[pj_row - r0] = cpj;
+    Cand piv = cown;
+    cand_take(piv, cpi);
+    cand_take(piv, cpj);
+    if (!(piv.q > 0.0) || [&] {
+          if (ek) return piv.q < a.threshold;
+          const double t2 = a.threshold * a.threshold;
+          if (piv.q > t2 * (1.0 + kRel)) return false;
+          if (piv.q < t2 * (1.0 - kRel)) return true;
+          return np_cabs(piv.v.x, piv.v.y) < a.threshold;
+        }()) {
+      status = 0;
+      break;
+    }
+    if (applied >= a.max_iter) {
+      status = 1;
+      break;
+    }
+    const int i = (int)(piv.cr >> 16), j = (int)(piv.cr & 0xffffu);
+    if (g == 0 && tid == 0 && a.pivots != nullptr && applied < a.pivot_cap) {
+      a.pivots[2 * applied] = i;
+      a.pivots[2 * applied + 1] = j;
+    }
+    // rotation scalars and the 2x2 block: every thread, same values
+    const cplx v = d2c(piv.v);
+    const double hii = s_dg[i], hjj = s_dg[j];
+    double c;
+    cplx s;
+    givens_fast(v, hii, hjj, &c, &s);
+    const Block2 blk = rotate_block(c, s, mkc(hii, 0.0), cconj(v), v, mkc(hjj, 0.0));
+
+    // ---- phase A: own columns of rows i, j; mirrored columns = own rows
+    if (tid == 0) s_nresc = 0;
+    __syncthreads();
+    Cand ppi = cand_none(), ppj = cand_none();
+    for (int k = tid; k < nr; k += kCoopThreads) {
+      const int x = r0 + k;
+      if (x == i || x == j) continue;
+      const cplx ri = d2c(h[(size_t)i * n + x]), rj = d2c(h[(size_t)j * n + x]);
+      cplx ni, nj;
+      rotate_rows(c, s, ri, rj, &ni, &nj);
+      h[(size_t)i * n + x] = c2d(ni);
+      h[(size_t)j * n + x] = c2d(nj);
+      h[(size_t)x * n + i] = c2d(cconj(ni));
+      h[(size_t)x * n + j] = c2d(cconj(nj));
+      // new rows i, j: lower-triangle entries (i, x) for x < i, (j, x) for x < j
+      if (x < i) cand_take(ppi, make_cand(c2d(ni), ((unsigned)x << 16) | (unsigned)i, ek));
+      if (x < j) cand_take(ppj, make_cand(c2d(nj), ((unsigned)x << 16) | (unsigned)j, ek));
+      // own row x: its entries (x, i) if i < x and (x, j) if j < x changed
+      Cand st = s_row[k];
+      const int bc = (st.q > 0.0) ? (int)(st.cr >> 16) : -1;
+      if (bc == i || bc == j) {
+        s_resc[atomicAdd(&s_nresc, 1)] = x;
+      } else {
+        if (i < x) cand_take(st, make_cand(c2d(cconj(ni)), ((unsigned)i << 16) | (unsigned)x, ek));
+        if (j < x) cand_take(st, make_cand(c2d(cconj(nj)), ((unsigned)j << 16) | (unsigned)x, ek));
+        s_row[k] = st;
+      }
+    }
+    // the 2x2 block entries, by the owners of columns i and j
+    if (tid == 0) {
+      if (i >= r0 && i < r1) {
+        h[(size_t)i * n + i] = c2d(blk.ii);
+        h[(size_t)j * n + i] = c2d(blk.ji);
+        cand_take(ppj, make_cand(c2d(blk.ji), ((unsigned)i << 16) | (unsigned)j, ek));
+      }
+      if (j >= r0 && j < r1) {
+        h[(size_t)i * n + j] = c2d(blk.ij);
+        h[(size_t)j * n + j] = c2d(blk.jj);
+      }
+    }
+    s_dg[i] = blk.ii.re;  // every thread writes the same value
+    s_dg[j] = blk.jj.re;
+    __syncthreads();  // own rows' new entries written and visible to the CTA
+    // rescans of own rows whose best sat in column i or j (whole CTA per row)
+    const int nresc = s_nresc;
+    for (int q = 0; q < nresc; ++q) {
+      const int x = s_resc[q];
+      const double2* __restrict__ row = h + (size_t)x * n;
+      Cand b = cand_none();
+      int bx = -1;
+      double bhi = 0.0, blo = 1.0e308;
+      double2 bv = make_double2(0.0, 0.0);
+      for (int base = 0; base < x; base += kCoopThreads * kRescanBatch) {
+        double2 vals[kRescanBatch];
+#pragma unroll
+        for (int k = 0; k < kRescanBatch; ++k) {
+          const int cc = base + k * kCoopThreads + tid;
+          vals[k] = cc < x ? row[cc] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < kRescanBatch; ++k) {
+          const int cc = base + k * kCoopThreads + tid;
+          if (cc >= x) break;
+          if (EK) {
+            cand_take(b, make_cand(vals[k], ((unsigned)cc << 16) | (unsigned)x, ek));
+          } else {
+            // running best in increasing column order (ties keep the smaller column)
+            const double qv = fma(vals[k].x, vals[k].x, vals[k].y * vals[k].y);
+            if (qv > bhi || (qv >= blo && np_cabs_ool(vals[k].x, vals[k].y) > np_cabs_ool(bv.x, bv.y))) {
+              bhi = qv * (1.0 + kRel);
+              blo = qv * (1.0 - kRel);
+              bx = cc;
+              bv = vals[k];
+            }
+          }
+        }
+      }
+      if (!EK && bx >= 0) b = make_cand(bv, ((unsigned)bx << 16) | (unsigned)x, ek);
+      b = block_best_p(b, s_part);
+      if (tid == 0) s_row[x - r0] = b;
+    }
+    // best over own rows other than i, j (their state arrives with the next phase B)
+    Cand own = cand_none();
+    for (int k = tid; k < nr; k += kCoopThreads) {
+      const int x = r0 + k;
+      if (x != i && x != j) cand_take(own, s_row[k]);
+    }
+    block_best3(own, ppi, ppj, s_part);
+    ++applied;
+    if (tid == 0) {
+      CoopRec* w = a.rec + (size_t)(applied & 1) * G + g;
+      w->own = own;
+      w->pi = ppi;
+      w->pj = ppj;
+      __threadfence();
+      st_rel(&w->epoch, (int)applied);
+    }
+    pi_row = i;
+    pj_row = j;
+  }
+  if (g == 0 && tid == 0) {
+    *a.out_applied = applied;
+    *a.out_status = status;
+  }
+}
+
+}  // namespace
+
+size_t npad_coop_smem(int n, int rows_per) {
+  return (((size_t)8 * n + 15) & ~(size_t)15) + sizeof(Cand) * (rows_per + 3 * kCoopWarps) + (size_t)4 * rows_per + 64;
+}
+
+// Run the greedy full-diagonal chain of ONE bitwise-Hermitian matrix on the
+// whole GPU.  State arrays from rows_init_kernel.  Returns QCH_ERR_UNSUPPORTED
+// (caller falls back to the single-CTA driver) when a cooperative launch of
+// one CTA per SM is not possible.
+int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int ek, const double* q, const int* c,
+                  const double2* v, int* pivots, long long pivot_cap, long long* applied, int* status,
+                  cudaStream_t st) {
+  int dev = 0, coop = 0;
+  QCH_CUDA(cudaGetDevice(&dev));
+  QCH_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) return QCH_ERR_UNSUPPORTED;
+  int G = sm_count();
+  if (const char* e = getenv("QCH_NPAD_COOP_CTAS")) G = std::max(1, std::min(G, atoi(e)));
+  const int rows_per = (n + G - 1) / G;
+  G = (n + rows_per - 1) / rows_per;
+  const size_t smem = npad_coop_smem(n, rows_per);
+  if (smem > (size_t)max_smem_optin()) return QCH_ERR_UNSUPPORTED;
+  auto kern = ek ? npad_coop_kernel<true> : npad_coop_kernel<false>;
+  QCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  QCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCoopThreads, smem));
+  if (per_sm < 1) return QCH_ERR_UNSUPPORTED;
+
+  void* ws = nullptr;
+  ensure_pool();
+  const size_t bytes = sizeof(CoopRec) * 2 * G + 256;
+  QCH_CUDA(cudaMallocAsync(&ws, bytes, st));
+  CoopArgs a;
+  a.h = h;
+  a.n = n;
+  a.rows_per = rows_per;
+  a.ek = ek;
+  a.threshold = threshold;
+  a.max_iter = max_iter;
+  a.st_q = q;
+  a.st_c = c;
+  a.st_v = v;
+  a.rec = (CoopRec*)ws;
+  a.out_applied = (long long*)((char*)ws + sizeof(CoopRec) * 2 * G);
+  a.out_status = (int*)(a.out_applied + 1);
+  a.pivots = pivots;
+  a.pivot_cap = pivot_cap;
+  QCH_CUDA(cudaMemsetAsync(ws, 0xff, sizeof(CoopRec) * 2 * G, st));  // epochs = -1
+  void* args[] = {&a};
+  void* pr = prof_begin("npad_run_kernel", st);
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kCoopThreads), args, smem, st);
+  prof_end(pr, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaFreeAsync(ws, st);
+    return QCH_ERR_UNSUPPORTED;
+  }
+  note_launch(1);
+  long long ap = 0;
+  int stt = 0;
+  QCH_CUDA(cudaMemcpyAsync(&ap, a.out_applied, sizeof ap, cudaMemcpyDeviceToHost, st));
+  QCH_CUDA(cudaMemcpyAsync(&stt, a.out_status, sizeof stt, cudaMemcpyDeviceToHost, st));
+  QCH_CUDA(cudaFreeAsync(ws, st));
+  QCH_CUDA(cudaStreamSynchronize(st));
+  *applied = ap;
+  *status = stt;
+  return QCH_OK;
+}
+
+}  // namespace qch

@@ -36,6 +36,9 @@ int npad_state_init(const double2* h, int64_t batch, const NpadCommon2& cm, bool
                     double2* v, cudaStream_t st);
 int npad_launch_trows_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st);
 int npad_launch_trows_cta(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st);
+int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int ek, const double* q, const int* c,
+                  const double2* v, int* pivots, long long pivot_cap, long long* applied, int* status,
+                  cudaStream_t st);
 int npad_launch2(NpadJob2* jobs, int njobs, const NpadCommon2& cm, bool herm, bool trows, int pref_threads,
                  bool allow_smem_h, cudaStream_t st);
 

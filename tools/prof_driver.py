@@ -26,9 +26,14 @@ def main():
         print("applied", st.applied)
     elif case == "npad4096":
         op = eff.HermitianOperator(eff.transmon_resonator_hamiltonian(4, 1024).data, validate=False)
+        import time as _t
         for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = _t.perf_counter()
             st = eff.npad_run(op, tol=1e-12, max_iter=arg or 2000)
-        print("applied", st.applied)
+            torch.cuda.synchronize()
+            dt = _t.perf_counter() - t0
+        print("applied", st.applied, f"us/rot {dt / max(st.applied, 1) * 1e6:.2f}")
     elif case == "sweep":
         pts = eff.sweep_points(32, 32)[: (arg or 64)]
         for _ in range(2):
