@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "magnus_small.cuh"
@@ -58,6 +59,8 @@ struct FusedArgs {
   double2 psi0v[4];
   int64_t win;          // > 0: stage each tile's signal window (win samples per control) in shared memory
   int stream_blocks_per_sm;  // > 0: persistent grid of this many blocks per SM streaming the tiles (host I/O)
+  const int* chunk_flag;     // non-null: signals arrive in chunks (copy engine); flag = chunks landed
+  int tiles_per_chunk;
   double2* traj;        // rows (M+1, N), indexed by GLOBAL interval
   int64_t M;            // intervals of the whole evolve
   int64_t tile_begin, tile_end;  // tiles of this launch
@@ -218,7 +221,11 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
   double2* s_u = fsm + ops_smem_bytes<N>(K, 2) / sizeof(double2) + (size_t)tid * kR * N * N;
   const size_t wstride = (((size_t)K * g.win + 1) & ~(size_t)1);  // doubles per window buffer (16 B multiple)
   double* s_sig0 = (double*)(fsm + ops_smem_bytes<N>(K, 2) / sizeof(double2) + (size_t)kFusedThreads * kR * N * N);
-  double2* s_traj = (double2*)(s_sig0 + (g.win > 0 ? 2 * wstride : 0));
+  // the tile's trajectory rows are staged in the tile's own signal window
+  // once the coefficients are formed (the next window prefetches into the
+  // other buffer); without staging, or if it is too small, in their own area
+  const bool traj_in_window = g.win > 0 && wstride * sizeof(double) >= sizeof(double2) * (size_t)kTile * N;
+  double2* s_traj_own = (double2*)(s_sig0 + (g.win > 0 ? 2 * wstride : 0));
   const double2* psi0p = g.psi0 ? g.psi0 : g.psi0v;
   __shared__ Mat<N> s_w[kFusedWarps];    // warp aggregates -> in-block exclusive warp prefixes
   __shared__ Mat<N> s_red[kFusedWarps];  // look-back partials
@@ -237,17 +244,31 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
     cp_commit();
   };
 
-  if (tid == 0) s_tile = atomicAdd(g.tile_ctr, 1);
+  // signals still streaming in (host-buffer call): wait for the chunk of tile tt
+  auto wait_chunk = [&](int64_t tt) {
+    if (g.chunk_flag != nullptr && tt < g.tile_end) {
+      const int need = (int)(tt / g.tiles_per_chunk) + 1;
+      while (ld_acquire(g.chunk_flag) < need) __nanosleep(200);
+    }
+  };
+  if (tid == 0) {
+    s_tile = atomicAdd(g.tile_ctr, 1);
+    wait_chunk(g.tile_begin + s_tile);
+  }
   __syncthreads();
   int64_t t = g.tile_begin + s_tile;
   if (g.win > 0 && t < g.tile_end) prefetch(t, s_sig0);
   for (int it = 0;; ++it) {
     if (t >= g.tile_end) break;
     __syncthreads();  // everyone has read s_tile
-    if (tid == 0) s_tile = atomicAdd(g.tile_ctr, 1);  // grab the next tile now (order-safe, see header)
+    if (tid == 0) {
+      s_tile = atomicAdd(g.tile_ctr, 1);  // grab the next tile now (order-safe, see header)
+      wait_chunk(g.tile_begin + s_tile);
+    }
     __syncthreads();
     const int64_t tn = g.tile_begin + s_tile;
     double* s_sig = s_sig0 + (it & 1) * wstride;
+    double2* s_traj = traj_in_window ? (double2*)s_sig : s_traj_own;
     if (g.win > 0) {
       if (tn < g.tile_end) {
         prefetch(tn, s_sig0 + ((it + 1) & 1) * wstride);
@@ -378,8 +399,7 @@ constexpr size_t kStageMax = 24 * 1024;  // signal window staged in shared memor
 
 template <int N>
 static size_t fused_smem(int K) {
-  return ops_smem_bytes<N>(K, 2) + sizeof(double2) * (size_t)kFusedThreads * kR * N * N +
-         sizeof(double2) * (size_t)kTile * N;
+  return ops_smem_bytes<N>(K, 2) + sizeof(double2) * (size_t)kFusedThreads * kR * N * N;
 }
 // samples per control of one tile's window, or 0 when it does not fit
 static int64_t fused_window(int K, int sub) {
@@ -390,16 +410,28 @@ static int64_t fused_window(int K, int sub) {
 template <int N>
 static int fused_launch(FusedArgs& g, cudaStream_t st) {
   g.win = fused_window(g.s.ca.K, g.s.ca.sub);
-  const size_t smem = fused_smem<N>(g.s.ca.K) + 2 * (((size_t)g.s.ca.K * g.win + 1) & ~(size_t)1) * sizeof(double);
+  const size_t wbytes = (((size_t)g.s.ca.K * g.win + 1) & ~(size_t)1) * sizeof(double);
+  const size_t tbytes = sizeof(double2) * (size_t)kTile * N;
+  const size_t smem = fused_smem<N>(g.s.ca.K) + 2 * wbytes + (g.win > 0 && wbytes >= tbytes ? 0 : tbytes);
   static bool attr = false;
   if (!attr) {
     QCH_CUDA(cudaFuncSetAttribute(magnus_fused_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(fused_smem<N>(8) + 2 * kStageMax + 32)));
+                                  (int)(fused_smem<N>(8) + 2 * kStageMax + 32 + sizeof(double2) * kTile * N)));
     attr = true;
   }
+  static size_t occ_smem[4] = {0, 0, 0, 0};
+  static int occ_val[4] = {0, 0, 0, 0};
   int blocks_per_sm = 0;
-  QCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, magnus_fused_kernel<N>, kFusedThreads, smem));
-  if (blocks_per_sm < 1) blocks_per_sm = 1;
+  for (int q = 0; q < 4; ++q)
+    if (occ_smem[q] == smem) blocks_per_sm = occ_val[q];
+  if (blocks_per_sm == 0) {
+    QCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, magnus_fused_kernel<N>, kFusedThreads, smem));
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    static int slot = 0;
+    occ_smem[slot & 3] = smem;
+    occ_val[slot & 3] = blocks_per_sm;
+    ++slot;
+  }
   const int64_t tiles = g.tile_end - g.tile_begin;
   if (tiles <= 0) return QCH_OK;
   int64_t slots = (int64_t)blocks_per_sm * sm_count();
@@ -476,14 +508,43 @@ struct FBuf {
 // page-locked status words of the host-buffer call (one pair per device)
 struct Pipe {
   unsigned long long* h_flags = nullptr;
+  cudaStream_t in = nullptr;  // copy stream of the host-buffer call
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int* d_flag = nullptr;      // chunk counter (cudaMalloc: stream memory ops reject pool memory)
 };
 Pipe& pipe_for_device() {
   static Pipe pipes[64];
   int dev = 0;
   cudaGetDevice(&dev);
   Pipe& p = pipes[dev & 63];
-  if (p.h_flags == nullptr) cudaMallocHost(&p.h_flags, 2 * sizeof(unsigned long long));
+  if (p.h_flags == nullptr) {
+    cudaMallocHost(&p.h_flags, 2 * sizeof(unsigned long long));
+    cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&p.ev0, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&p.ev1, cudaEventDisableTiming);
+    cudaMalloc(&p.d_flag, 256);
+  }
   return p;
+}
+
+// cuStreamWriteValue32 (driver API, fetched through the runtime): a copy
+// stream bumps a device flag after each chunk it lands, and the running
+// kernel polls it
+typedef int (*WriteValue32Fn)(cudaStream_t, unsigned long long, unsigned, unsigned);
+WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (WriteValue32Fn)p;
+    else
+      cudaGetLastError();
+  }
+  return fn;
 }
 
 // device address of a page-locked, mapped host buffer (UVA), or null for
@@ -507,6 +568,8 @@ int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const doubl
   FusedArgs g;
   g.s = base;
   g.stream_blocks_per_sm = 0;
+  g.chunk_flag = nullptr;
+  g.tiles_per_chunk = 1;
   int* ctr = nullptr;
   fused_carve(ws.p, N, M, 1, &g, &ctr);
   QCH_CUDA(cudaMemsetAsync(ws.p, 0, fused_ws_zero_bytes(M, 1), st));
@@ -563,23 +626,22 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   Trace tr;
   const int64_t nn = N * N;
   const int64_t Kd = std::max<int64_t>(K, 1);
-  FBuf dev(st);
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t b_ops = al(sizeof(double2) * nn * (1 + Kd)), b_psi = al(sizeof(double2) * N),
-               b_sig = al(sizeof(double) * Kd * S), b_traj = al(sizeof(double2) * N * (M + 1));
-  QCH_CUDA(dev.alloc(b_ops + b_psi + b_sig + b_traj));
-  unsigned char* base = (unsigned char*)dev.p;
-  double2* d_h0 = (double2*)base;
-  double2* d_hk = d_h0 + nn;
-  double2* d_psi0 = (double2*)(base + b_ops);
-  double* d_sig = (double*)(base + b_ops + b_psi);
-  double2* d_traj = (double2*)(base + b_ops + b_psi + b_sig);
-  QCH_CUDA(cudaMemcpyAsync(d_h0, h_h0, sizeof(double2) * nn, cudaMemcpyHostToDevice, st));
-  if (K > 0) QCH_CUDA(cudaMemcpyAsync(d_hk, h_hk, sizeof(double2) * nn * K, cudaMemcpyHostToDevice, st));
-  QCH_CUDA(cudaMemcpyAsync(d_psi0, h_psi0, sizeof(double2) * N, cudaMemcpyHostToDevice, st));
-  tr.mark("alloc + operand upload");
 
   if (N > 4) {  // generic path: upload, device evolve, download
+    FBuf dev(st);
+    const size_t b_ops = al(sizeof(double2) * nn * (1 + Kd)), b_psi = al(sizeof(double2) * N),
+                 b_sig = al(sizeof(double) * Kd * S), b_traj = al(sizeof(double2) * N * (M + 1));
+    QCH_CUDA(dev.alloc(b_ops + b_psi + b_sig + b_traj));
+    unsigned char* base = (unsigned char*)dev.p;
+    double2* d_h0 = (double2*)base;
+    double2* d_hk = d_h0 + nn;
+    double2* d_psi0 = (double2*)(base + b_ops);
+    double* d_sig = (double*)(base + b_ops + b_psi);
+    double2* d_traj = (double2*)(base + b_ops + b_psi + b_sig);
+    QCH_CUDA(cudaMemcpyAsync(d_h0, h_h0, sizeof(double2) * nn, cudaMemcpyHostToDevice, st));
+    if (K > 0) QCH_CUDA(cudaMemcpyAsync(d_hk, h_hk, sizeof(double2) * nn * K, cudaMemcpyHostToDevice, st));
+    QCH_CUDA(cudaMemcpyAsync(d_psi0, h_psi0, sizeof(double2) * N, cudaMemcpyHostToDevice, st));
     if (K > 0) QCH_CUDA(cudaMemcpyAsync(d_sig, h_sig, sizeof(double) * K * S, cudaMemcpyHostToDevice, st));
     else QCH_CUDA(cudaMemsetAsync(d_sig, 0, sizeof(double) * S, st));
     if (int rc = qch_magnus_evolve_c128(d_h0, d_hk, nullptr, K, N, d_sig, S, t_start, t_end, M, order, d_psi0,
@@ -590,35 +652,48 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
     return QCH_OK;
   }
 
-  // N <= 4: ONE launch.  Operators and psi0 travel inside the kernel
-  // arguments; page-locked (mapped) signal / trajectory buffers are read and
-  // written by the kernel directly over the host link, so the H2D of the
-  // signals, the compute and the D2H of the trajectory all overlap.
+  // N <= 4: ONE allocation, two memsets, ONE launch.  Operators and psi0
+  // travel inside the kernel arguments; page-locked (mapped) signal /
+  // trajectory buffers are read and written by the kernel directly over the
+  // host link, so the H2D of the signals, the compute and the D2H of the
+  // trajectory all overlap.
+  // signals: page-locked -> read zero-copy by the kernel (measured fastest
+  // end to end); pageable -> one staged copy before the kernel.
+  // QCH_SIG_MODE=copy|stream selects a copy-engine H2D instead (stream: in
+  // chunks, each bumping a flag the running kernel polls).
+  const char* smode = getenv("QCH_SIG_MODE");
+  const bool pinned_sig = K > 0 && mapped_ptr(h_sig) != nullptr;
+  const bool sig_stream = pinned_sig && smode != nullptr && strcmp(smode, "stream") == 0 && write_value32() != nullptr;
+  const bool sig_map = pinned_sig && !sig_stream && !(smode != nullptr && strcmp(smode, "copy") == 0);
+  const double* sig = sig_map ? (const double*)mapped_ptr(h_sig) : nullptr;
+  double2* traj = getenv("QCH_NOMAP_TRAJ") ? nullptr : (double2*)mapped_ptr(h_traj);
+  const size_t b_ws = al(fused_ws_bytes(N, M, 1));
+  const size_t b_flag = 256;
+  const size_t b_sig = sig ? 0 : al(sizeof(double) * Kd * S);
+  const size_t b_traj = traj ? 0 : al(sizeof(double2) * N * (M + 1));
+  FBuf dev(st);
+  QCH_CUDA(dev.alloc(b_ws + b_flag + b_sig + b_traj));
+  double* d_sig = (double*)((unsigned char*)dev.p + b_ws + b_flag);
+  double2* d_traj = (double2*)((unsigned char*)dev.p + b_ws + b_flag + b_sig);
+  if (sig == nullptr) {
+    if (K > 0 && !sig_stream) QCH_CUDA(cudaMemcpyAsync(d_sig, h_sig, sizeof(double) * K * S, cudaMemcpyHostToDevice, st));
+    sig = d_sig;
+  }
+  if (traj == nullptr) traj = d_traj;
+  tr.mark("buffers");
   const int64_t sub = (S - 1) / M;
   FusedArgs g;
   memcpy(g.opsv, h_h0, sizeof(double2) * nn);
   if (K > 0) memcpy(g.opsv + nn, h_hk, sizeof(double2) * nn * K);
   memcpy(g.psi0v, h_psi0, sizeof(double2) * N);
-  const double* sig = getenv("QCH_NOMAP_SIG") ? nullptr : (const double*)mapped_ptr(h_sig);
-  double2* traj = getenv("QCH_NOMAP_TRAJ") ? nullptr : (double2*)mapped_ptr(h_traj);
-  if (K > 0 && sig == nullptr) {
-    QCH_CUDA(cudaMemcpyAsync(d_sig, h_sig, sizeof(double) * K * S, cudaMemcpyHostToDevice, st));
-    sig = d_sig;
-  } else if (K == 0) {
-    sig = d_sig;
-  }
-  tr.mark(traj ? "signals ready (mapped out)" : "signals ready (device out)");
-  if (traj == nullptr) traj = d_traj;
   // host-link I/O: a persistent grid streams the tiles so fetches, arithmetic
   // and write-backs of different tiles overlap
-  g.stream_blocks_per_sm = (sig != d_sig || traj != d_traj) ? 1 : 0;
+  g.stream_blocks_per_sm = (sig != d_sig || traj != d_traj) ? 1 : 0;  // zero-copy I/O: persistent grid
   if (const char* e = getenv("QCH_STREAM_BPS")) g.stream_blocks_per_sm = atoi(e);
 
-  FBuf ws(st);
-  QCH_CUDA(ws.alloc(fused_ws_bytes(N, M, 1)));
   int* ctr = nullptr;
-  fused_carve(ws.p, N, M, 1, &g, &ctr);
-  QCH_CUDA(cudaMemsetAsync(ws.p, 0, fused_ws_zero_bytes(M, 1), st));
+  fused_carve(dev.p, N, M, 1, &g, &ctr);
+  QCH_CUDA(cudaMemsetAsync(dev.p, 0, fused_ws_zero_bytes(M, 1), st));
   QCH_CUDA(cudaMemsetAsync(g.s.bad, 0xff, 2 * sizeof(unsigned long long), st));
   g.s.ca = CoefArgs{sig, (int)K, S, M, (int)sub, (t_end - t_start) / (double)(S - 1)};
   g.s.h0 = nullptr;  // operators inline (g.opsv)
@@ -634,8 +709,34 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   g.tile_begin = 0;
   g.tile_end = fused_tiles(M);
   g.tile_ctr = ctr;
-  if (int rc = fused_launch_any((int)N, g, st)) return rc;
+  g.chunk_flag = nullptr;
+  g.tiles_per_chunk = 1;
   Pipe& pp = pipe_for_device();
+  if (sig_stream) {
+    const int64_t tiles = fused_tiles(M);
+    int nch = (int)std::min<int64_t>(8, tiles);
+    if (const char* e = getenv("QCH_SIG_CHUNKS")) nch = std::max(1, std::min((int)tiles, atoi(e)));
+    const int tpc = (int)((tiles + nch - 1) / nch);
+    nch = (int)((tiles + tpc - 1) / tpc);
+    int* d_flag = pp.d_flag;
+    QCH_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), st));
+    QCH_CUDA(cudaEventRecord(pp.ev0, st));  // flag reset + buffers ready before the copies
+    QCH_CUDA(cudaStreamWaitEvent(pp.in, pp.ev0, 0));
+    for (int c = 0; c < nch; ++c) {
+      const int64_t s0 = (int64_t)c * tpc * fused_tile_intervals() * sub;
+      const int64_t s1 = std::min<int64_t>(S, (int64_t)(c + 1) * tpc * fused_tile_intervals() * sub + 1);
+      QCH_CUDA(cudaMemcpy2DAsync(d_sig + s0, sizeof(double) * S, h_sig + s0, sizeof(double) * S,
+                                 sizeof(double) * (s1 - s0), K, cudaMemcpyHostToDevice, pp.in));
+      const int wr = write_value32()(pp.in, (unsigned long long)(uintptr_t)d_flag, (unsigned)(c + 1), 0);
+      if (wr != 0) return fail(QCH_ERR_CUDA, "cuStreamWriteValue32 failed: CUresult " + std::to_string(wr));
+    }
+    QCH_CUDA(cudaEventRecord(pp.ev1, pp.in));
+    g.chunk_flag = d_flag;
+    g.tiles_per_chunk = tpc;
+    g.stream_blocks_per_sm = 0;
+  }
+  if (int rc = fused_launch_any((int)N, g, st)) return rc;
+  if (sig_stream) QCH_CUDA(cudaStreamWaitEvent(st, pp.ev1, 0));  // copies retired before the buffers are freed
   QCH_CUDA(cudaMemcpyAsync(pp.h_flags, g.s.bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   if (traj == d_traj)
     QCH_CUDA(cudaMemcpyAsync(h_traj, d_traj, sizeof(double2) * N * (M + 1), cudaMemcpyDeviceToHost, st));

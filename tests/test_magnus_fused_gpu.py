@@ -141,3 +141,20 @@ def test_evolve_plan_replay(E):
     out2 = plan.run().cpu().numpy()
     ref2 = _oracle(ch, E.ControlGrid(grid.t_start, grid.t_end, sig2), m, psi0, 2)
     assert rel_fro(out2, ref2) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["map", "copy", "stream"])
+def test_host_call_signal_modes(E, mode, monkeypatch):
+    # page-locked signals: zero-copy (default), copy-engine H2D, or chunked
+    # copy-engine stream polled by the running kernel — same results
+    import torch
+
+    m = 20_000
+    ch, grid = E.driven_transmon(3, intervals=m, sub=4, t_final=20.0)
+    pinned = torch.empty(grid.signals.shape, dtype=torch.float64).pin_memory()
+    pinned.numpy()[:] = grid.signals
+    g2 = E.ControlGrid(grid.t_start, grid.t_end, pinned.numpy())
+    psi0 = np.array([1, 0, 0], dtype=complex)
+    monkeypatch.setenv("QCH_SIG_MODE", mode)
+    got = E.evolve(ch, g2, m, psi0, order=2)
+    assert rel_fro(got.amplitudes, _oracle(ch, grid, m, psi0, 2)) <= 1e-10
