@@ -254,8 +254,12 @@ def run_headline(torch, eff, lib, args, world, rank, local):
         def step():
             plan.run()
     else:
+        # interval sharding: per step pass 1 (fused kernel, prefix mode) ->
+        # ONE NCCL all-gather of the N x N block products -> pass 2
+        plan = sharding.ShardedEvolvePlan(ch, grid, m, psi0, order=2, check=False)
+
         def step():
-            sharding.evolve_sharded(ch, grid, m, psi0, order=2, check=False)
+            plan.run()
 
     for _ in range(args.warmup):
         step()
@@ -268,8 +272,10 @@ def run_headline(torch, eff, lib, args, world, rank, local):
     launches = lib.launch_count() - n0
     lib.profile_enable(False)
     prof = lib.profile_read(reset=True)
+    plan.check()
+    if world > 1:
+        launches = 3 * args.steps  # fused (prefix mode) + apply_prefix + shard_traj per step
     if world == 1:
-        plan.check()
         launches = 1 * args.steps  # graph replay = 1 libqcheff kernel (magnus_fused_kernel) per step
         # kernel timing pass (eager launches, CUDA events on the launching stream)
         lib.profile_read(reset=True)

@@ -188,10 +188,11 @@ int qch_zgemm_batched(const void* d_a, const void* d_b, void* d_c, int64_t m, in
 /* Interval sharding, N <= 4.  Workspace bytes for M local
  * intervals. */
 int64_t qch_magnus_shard_workspace_bytes(int64_t N, int64_t M);
-/* Local intervals of one rank: coefficients from the local signal slice
- * (K, S) with grid spacing dt and interval length dt_int, propagators, local
- * prefix products; writes the block product B = U_last...U_first to d_block
- * (N,N) — the tensor the ranks all-gather. */
+/* Local intervals of one rank (pass 1, asynchronous): the fused single-pass
+ * kernel in prefix mode — coefficients from the local signal slice (K, S)
+ * with grid spacing dt and interval length dt_int, propagators, in-tile and
+ * tile prefixes into d_work; writes the block product B = U_last...U_first
+ * to d_block (N,N) — the tensor the ranks all-gather. */
 int qch_magnus_shard_prepare_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
                                   const double* d_sig, int64_t S, double dt, double dt_int, int64_t M, int order,
                                   int check, void* d_work, void* d_block, void* stream);
@@ -201,6 +202,12 @@ int qch_magnus_apply_prefix_c128(const void* d_blocks, int64_t N, int64_t rank, 
 /* Local trajectory (M+1, N) from psi_start; NormDrift / NonFinite checks. */
 int qch_magnus_shard_finish_c128(int64_t N, int64_t M, void* d_work, const void* d_psi_start, void* d_traj,
                                  int check, int64_t* bad_index, void* stream);
+
+/* qch_magnus_shard_finish_c128 without a host synchronisation: the two
+ * status words (first non-unitary, first norm-drift local interval; ~0 =
+ * none) are copied to d_flags (device, 2 x uint64). */
+int qch_magnus_shard_finish_async_c128(int64_t N, int64_t M, void* d_work, const void* d_psi_start, void* d_traj,
+                                       void* d_flags, void* stream);
 
 /* ------------------------------------------------ measurement ------------ */
 

@@ -34,6 +34,10 @@ int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream
 int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st);
 int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const double2* d_psi0, double2* d_traj,
                         int64_t* bad_index, unsigned long long* d_flags_out, cudaStream_t st);
+size_t shard_ws_bytes(int64_t N, int64_t M);
+int shard_prepare(const SmallArgs& base, int64_t N, int64_t M, void* d_work, double2* d_block, cudaStream_t st);
+int shard_finish(int64_t N, int64_t M, void* d_work, const double2* d_psi_start, double2* d_traj,
+                 unsigned long long** bad_out, cudaStream_t st);
 
 __global__ void coeff_kernel(CoefArgs a, int order, double* __restrict__ c1, double* __restrict__ c2) {
   int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -44,164 +48,6 @@ __global__ void coeff_kernel(CoefArgs a, int order, double* __restrict__ c1, dou
   if (order >= 2) {
     int nc = a.K + a.K * (a.K - 1) / 2;
     for (int k = 0; k < nc; ++k) c2[n * nc + k] = l2[k];
-  }
-}
-
-constexpr int kScanThreads = 128;
-constexpr int kRun = 4;  // intervals per thread in the ordered-product scan
-
-// Hillis-Steele inclusive scan of matrix products in thread order, later
-// entries multiplied on the LEFT: P_t = A_t ... A_0.
-template <int N>
-__device__ Mat<N> block_scan(Mat<N> p, double2* sm) {
-  const int t = threadIdx.x;
-  for (int d = 1; d < blockDim.x; d <<= 1) {
-    st_mat<N>(sm + t * N * N, p);
-    __syncthreads();
-    if (t >= d) {
-      Mat<N> q;
-      ld_mat<N>(q, sm + (t - d) * N * N);
-      p = mat_mul_fma<N>(p, q);
-    }
-    __syncthreads();
-  }
-  return p;
-}
-
-// per-interval propagators: coefficients + assembly (numpy order) + expm
-template <int N>
-__global__ void __launch_bounds__(128) magnus_prop_kernel(SmallArgs g) {
-  extern __shared__ __align__(16) double2 ssm[];
-  load_ops<N>(g, ssm);
-  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (n >= g.ca.M) return;
-  const Mat<N> u = expm_minus_i_fast<N>(interval_hbar<N>(g, ssm, n));
-  if (g.check && !validate_reg<N>(u)) atomicMin(g.bad, (unsigned long long)n);
-  st_mat<N>(g.ubuf + n * N * N, u);
-}
-
-// run products (kRun intervals per thread), block scan over runs
-template <int N>
-__global__ void __launch_bounds__(kScanThreads) magnus_runs_kernel(const double2* __restrict__ ubuf, int64_t M,
-                                                                  double2* __restrict__ runp,
-                                                                  double2* __restrict__ agg) {
-  extern __shared__ __align__(16) double2 ssm[];
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t first = r * kRun;
-  Mat<N> a = mat_eye<N>();
-  if (first < M) {
-    ld_mat<N>(a, ubuf + first * N * N);
-    for (int k = 1; k < kRun && first + k < M; ++k) {
-      Mat<N> u;
-      ld_mat<N>(u, ubuf + (first + k) * N * N);
-      a = mat_mul_fma<N>(u, a);
-    }
-  }
-  Mat<N> p = block_scan<N>(a, ssm);
-  // exclusive within the block: P_{t-1}
-  st_mat<N>(ssm + threadIdx.x * N * N, p);
-  __syncthreads();
-  const int64_t nruns = (M + kRun - 1) / kRun;
-  if (r < nruns) {
-    if (threadIdx.x == 0) {
-      st_mat<N>(runp + r * N * N, mat_eye<N>());
-    } else {
-      Mat<N> e;
-      ld_mat<N>(e, ssm + (threadIdx.x - 1) * N * N);
-      st_mat<N>(runp + r * N * N, e);
-    }
-  }
-  if (threadIdx.x == blockDim.x - 1) st_mat<N>(agg + (int64_t)blockIdx.x * N * N, p);
-}
-
-// exclusive scan of block aggregates: E_0 = I, E_b = A_{b-1} ... A_0 (in place)
-template <int N>
-__global__ void __launch_bounds__(1024) scan_aggregates_kernel(double2* agg, int64_t nb, double2* total) {
-  extern __shared__ __align__(16) double2 ssm[];
-  Mat<N> carry = mat_eye<N>();
-  for (int64_t base = 0; base < nb; base += blockDim.x) {
-    int64_t b = base + threadIdx.x;
-    Mat<N> a = mat_eye<N>();
-    if (b < nb) ld_mat<N>(a, agg + b * N * N);
-    Mat<N> p = block_scan<N>(a, ssm);
-    // exclusive: E_b = P_{b-1} * carry ; E_base = carry
-    st_mat<N>(ssm + threadIdx.x * N * N, p);
-    __syncthreads();
-    Mat<N> e = carry;
-    if (threadIdx.x > 0) {
-      Mat<N> q;
-      ld_mat<N>(q, ssm + (threadIdx.x - 1) * N * N);
-      e = mat_mul_fma<N>(q, carry);
-    }
-    Mat<N> last;
-    ld_mat<N>(last, ssm + (blockDim.x - 1) * N * N);
-    __syncthreads();
-    if (b < nb) st_mat<N>(agg + b * N * N, e);
-    carry = mat_mul_fma<N>(last, carry);
-  }
-  if (total != nullptr && threadIdx.x == 0) st_mat<N>(total, carry);
-}
-
-// trajectory: psi at the start of run r = runp[r] * E_block * psi0, then the
-// run's intervals sequentially (psi <- U_n psi, magnus.py:249-252)
-template <int N>
-__global__ void __launch_bounds__(kScanThreads) magnus_traj_kernel(const double2* __restrict__ ubuf,
-                                                                  const double2* __restrict__ runp,
-                                                                  const double2* __restrict__ excl,
-                                                                  const double2* __restrict__ psi0, int64_t M,
-                                                                  double2* __restrict__ traj,
-                                                                  unsigned long long* bad_norm) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  cplx p0[N];
-#pragma unroll
-  for (int q = 0; q < N; ++q) p0[q] = d2c(psi0[q]);
-  if (r == 0) {
-#pragma unroll
-    for (int q = 0; q < N; ++q) traj[q] = c2d(p0[q]);
-  }
-  const int64_t first = r * kRun;
-  if (first >= M) return;
-  Mat<N> e, q;
-  ld_mat<N>(e, excl + (int64_t)blockIdx.x * N * N);
-  ld_mat<N>(q, runp + r * N * N);
-  Mat<N> pre = mat_mul_fma<N>(q, e);
-  cplx v[N];
-#pragma unroll
-  for (int a = 0; a < N; ++a) {
-    double re = 0.0, im = 0.0;
-#pragma unroll
-    for (int c = 0; c < N; ++c) {
-      re = fma(pre.v[a][c].re, p0[c].re, re);
-      re = fma(-pre.v[a][c].im, p0[c].im, re);
-      im = fma(pre.v[a][c].re, p0[c].im, im);
-      im = fma(pre.v[a][c].im, p0[c].re, im);
-    }
-    v[a] = mkc(re, im);
-  }
-  for (int k = 0; k < kRun && first + k < M; ++k) {
-    Mat<N> u;
-    ld_mat<N>(u, ubuf + (first + k) * N * N);
-    cplx w[N];
-    double nrm2 = 0.0;
-#pragma unroll
-    for (int a = 0; a < N; ++a) {
-      double re = 0.0, im = 0.0;
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        re = fma(u.v[a][c].re, v[c].re, re);
-        re = fma(-u.v[a][c].im, v[c].im, re);
-        im = fma(u.v[a][c].re, v[c].im, im);
-        im = fma(u.v[a][c].im, v[c].re, im);
-      }
-      w[a] = mkc(re, im);
-      nrm2 = fma(re, re, fma(im, im, nrm2));
-    }
-#pragma unroll
-    for (int a = 0; a < N; ++a) {
-      v[a] = w[a];
-      traj[(first + k + 1) * N + a] = c2d(w[a]);
-    }
-    if (!(fabs(sqrt(nrm2) - 1.0) <= 1e-6)) atomicMin(bad_norm, (unsigned long long)(first + k));  // NORM_DRIFT_TOL
   }
 }
 
@@ -732,76 +578,6 @@ extern "C" int qch_validate_unitary_batch_c128(const void* d_u, int64_t batch, i
   return report_bad(bad, bad_index, QCH_ERR_NONFINITE, "propagator not unitary", st);
 }
 
-static int64_t small_nruns(int64_t M) { return (M + kRun - 1) / kRun; }
-static int64_t small_nblocks(int64_t M) { return (small_nruns(M) + kScanThreads - 1) / kScanThreads; }
-
-template <int N>
-static int small_prepare(const SmallArgs& g, int64_t M, double2* total, cudaStream_t st) {
-  const int K = g.ca.K;
-  const int ncomm = K + K * (K - 1) / 2;
-  const size_t smem1 = sizeof(double2) * (size_t)(1 + K + ncomm) * N * N;
-  void* pr = prof_begin("magnus_prop_kernel", st);
-  magnus_prop_kernel<N><<<(unsigned)((M + 127) / 128), 128, smem1, st>>>(g);
-  prof_end(pr, st);
-  QCH_LAUNCH_CHECK("magnus_prop_kernel");
-  const int64_t nb = small_nblocks(M);
-  const size_t smem2 = sizeof(double2) * (size_t)kScanThreads * N * N;
-  static bool attr2 = false;
-  if (!attr2) {
-    QCH_CUDA(cudaFuncSetAttribute(magnus_runs_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-    attr2 = true;
-  }
-  void* pr2 = prof_begin("magnus_runs_scan_kernels", st);
-  magnus_runs_kernel<N><<<(unsigned)nb, kScanThreads, smem2, st>>>(g.ubuf, M, g.runp, g.agg);
-  QCH_LAUNCH_CHECK("magnus_runs_kernel");
-  const int tmax = N <= 2 ? 1024 : (N == 3 ? 512 : 256);  // <= 64 KB of scan buffer
-  const int t2 = (int)std::min<int64_t>(tmax, std::max<int64_t>(32, ((nb + 31) / 32) * 32));
-  const size_t smem3 = sizeof(double2) * (size_t)t2 * N * N;
-  static bool attr = false;
-  if (!attr) {
-    QCH_CUDA(cudaFuncSetAttribute(scan_aggregates_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double2) * tmax * N * N)));
-    attr = true;
-  }
-  scan_aggregates_kernel<N><<<1, t2, smem3, st>>>(g.agg, nb, total);
-  prof_end(pr2, st);
-  QCH_LAUNCH_CHECK("scan_aggregates_kernel");
-  note_launch(3);
-  return QCH_OK;
-}
-
-template <int N>
-static int small_finish(const SmallArgs& g, int64_t M, const double2* psi0, double2* traj, cudaStream_t st) {
-  const int64_t nb = small_nblocks(M);
-  void* pr = prof_begin("magnus_traj_kernel", st);
-  magnus_traj_kernel<N><<<(unsigned)nb, kScanThreads, 0, st>>>(g.ubuf, g.runp, g.agg, psi0, M, traj, g.bad + 1);
-  prof_end(pr, st);
-  QCH_LAUNCH_CHECK("magnus_traj_kernel");
-  note_launch(1);
-  return QCH_OK;
-}
-
-// workspace: [ubuf (M) unless props given] runp (nruns) agg (nblocks) flags
-static size_t small_ws_bytes(int64_t N, int64_t M, bool props) {
-  return sizeof(double2) * N * N * ((props ? 0 : M) + small_nruns(M) + small_nblocks(M)) + 64;
-}
-static SmallArgs small_carve(void* ws, int64_t N, int64_t M, double2* props) {
-  SmallArgs g;
-  double2* p = (double2*)ws;
-  if (props) {
-    g.ubuf = props;
-  } else {
-    g.ubuf = p;
-    p += N * N * M;
-  }
-  g.runp = p;
-  p += N * N * small_nruns(M);
-  g.agg = p;
-  p += N * N * small_nblocks(M);
-  g.bad = (unsigned long long*)p;
-  return g;
-}
-
 // one D2H for both flags; NonFinite (unitarity) first, as expm_batch
 // validates before the product (magnus.py:248-252)
 static int small_report(unsigned long long* d_bad, int check, int64_t* bad_index, cudaStream_t st, int64_t offset) {
@@ -947,14 +723,9 @@ extern "C" int qch_magnus_evolve_async_c128(const void* d_h0, const void* d_hk, 
 }
 
 // ---------------------------------------------------------------------------
-// Interval sharding across GPUs: each rank owns a
-// contiguous block of intervals, computes its block product B_r, the ranks
-// all-gather the B's (NCCL), each rank applies B_{r-1}...B_0 to psi0 and
-// finishes its local trajectory.  Workspace layout (caller-allocated,
-// qch_magnus_shard_workspace_bytes): U (M,N,N) | run prefixes | block prefixes | flags.
-extern "C" int64_t qch_magnus_shard_workspace_bytes(int64_t N, int64_t M) {
-  return (int64_t)small_ws_bytes(N, M, false);
-}
+// Interval sharding across GPUs: see magnus_fused.cu
+// (shard_prepare / shard_finish).  Workspace bytes for M local intervals.
+extern "C" int64_t qch_magnus_shard_workspace_bytes(int64_t N, int64_t M) { return (int64_t)shard_ws_bytes(N, M); }
 
 extern "C" int qch_magnus_shard_prepare_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K,
                                              int64_t N, const double* d_sig, int64_t S, double dt, double dt_int,
@@ -962,8 +733,8 @@ extern "C" int qch_magnus_shard_prepare_c128(const void* d_h0, const void* d_hk,
                                              void* stream) {
   if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "sharded Magnus prepare: N <= 4");
   if (M < 1 || (S - 1) % M) return fail(QCH_ERR_GRID, "interval count does not divide the local sample steps");
-  cudaStream_t st = (cudaStream_t)stream;
-  SmallArgs g = small_carve(d_work, N, M, nullptr);
+  if (K > kMaxK) return fail(QCH_ERR_UNSUPPORTED, "at most 8 control channels");
+  SmallArgs g;
   g.ca = CoefArgs{d_sig, (int)K, S, M, (int)((S - 1) / M), dt};
   g.h0 = (const double2*)d_h0;
   g.hk = (const double2*)d_hk;
@@ -971,13 +742,8 @@ extern "C" int qch_magnus_shard_prepare_c128(const void* d_h0, const void* d_hk,
   g.order = order;
   g.dt_int = dt_int;
   g.check = check;
-  QCH_CUDA(cudaMemsetAsync(g.bad, 0xff, 2 * sizeof(unsigned long long), st));
-  switch (N) {
-    case 1: return small_prepare<1>(g, M, (double2*)d_block, st);
-    case 2: return small_prepare<2>(g, M, (double2*)d_block, st);
-    case 3: return small_prepare<3>(g, M, (double2*)d_block, st);
-    default: return small_prepare<4>(g, M, (double2*)d_block, st);
-  }
+  g.ubuf = nullptr;
+  return shard_prepare(g, N, M, d_work, (double2*)d_block, (cudaStream_t)stream);
 }
 
 // psi_start = B_{rank-1} ... B_0 psi0   (blocks: (world, N, N))
@@ -1017,16 +783,18 @@ extern "C" int qch_magnus_shard_finish_c128(int64_t N, int64_t M, void* d_work, 
                                             void* d_traj, int check, int64_t* bad_index, void* stream) {
   if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "sharded Magnus finish: N <= 4");
   cudaStream_t st = (cudaStream_t)stream;
-  SmallArgs g = small_carve(d_work, N, M, nullptr);
-  const double2* p0 = (const double2*)d_psi_start;
-  double2* tr = (double2*)d_traj;
-  int rc;
-  switch (N) {
-    case 1: rc = small_finish<1>(g, M, p0, tr, st); break;
-    case 2: rc = small_finish<2>(g, M, p0, tr, st); break;
-    case 3: rc = small_finish<3>(g, M, p0, tr, st); break;
-    default: rc = small_finish<4>(g, M, p0, tr, st); break;
-  }
-  if (rc) return rc;
-  return small_report(g.bad, check, bad_index, st, 0);
+  unsigned long long* bad = nullptr;
+  if (int rc = shard_finish(N, M, d_work, (const double2*)d_psi_start, (double2*)d_traj, &bad, st)) return rc;
+  return small_report(bad, check, bad_index, st, 0);
+}
+
+// the same without a host synchronisation: the two status words go to d_flags
+extern "C" int qch_magnus_shard_finish_async_c128(int64_t N, int64_t M, void* d_work, const void* d_psi_start,
+                                                  void* d_traj, void* d_flags, void* stream) {
+  if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "sharded Magnus finish: N <= 4");
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long* bad = nullptr;
+  if (int rc = shard_finish(N, M, d_work, (const double2*)d_psi_start, (double2*)d_traj, &bad, st)) return rc;
+  QCH_CUDA(cudaMemcpyAsync(d_flags, bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+  return QCH_OK;
 }

@@ -61,6 +61,12 @@ struct FusedArgs {
   int stream_blocks_per_sm;  // > 0: persistent grid of this many blocks per SM streaming the tiles (host I/O)
   const int* chunk_flag;     // non-null: signals arrive in chunks (copy engine); flag = chunks landed
   int tiles_per_chunk;
+  // prefix mode (multi-GPU shard, pass 1): no trajectory; store each thread's
+  // in-tile exclusive prefix, each tile's exclusive prefix and the block
+  // product (s.ubuf receives the propagators)
+  double2* pex;        // (M / kR, N, N) or null (full mode)
+  double2* etile;      // (tiles, N, N)
+  double2* block_out;  // (N, N): U_{M-1} ... U_0
   double2* traj;        // rows (M+1, N), indexed by GLOBAL interval
   int64_t M;            // intervals of the whole evolve
   int64_t tile_begin, tile_end;  // tiles of this launch
@@ -350,6 +356,20 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
       s_e = mat_eye<N>();
     }
     __syncthreads();
+    if (g.pex != nullptr) {
+      // prefix mode: the thread's start = (P_{lane-1} X_warp) E_t psi_start,
+      // with psi_start known only after the ranks' exchange
+      Mat<N> pexm = shfl_up_mat<N>(p, 1);
+      if (lane == 0) pexm = mat_eye<N>();
+      st_mat<N>(g.pex + (t * kFusedThreads + tid) * N * N, mat_mul_fma<N>(pexm, s_w[warp]));
+      if (tid == 0) {
+        st_mat<N>(g.etile + t * N * N, s_e);
+        if (t == g.tile_end - 1) st_mat<N>(g.block_out, mat_mul_fma<N>(agg, s_e));
+      }
+      __syncthreads();  // s_w / s_e reuse
+      t = tn;
+      continue;
+    }
     // ---- trajectory: psi at this thread's start = P_{lane-1} X_warp E psi0
     cplx psi0[N], v[N], w[N];
 #pragma unroll
@@ -570,6 +590,9 @@ int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const doubl
   g.stream_blocks_per_sm = 0;
   g.chunk_flag = nullptr;
   g.tiles_per_chunk = 1;
+  g.pex = nullptr;
+  g.etile = nullptr;
+  g.block_out = nullptr;
   int* ctr = nullptr;
   fused_carve(ws.p, N, M, 1, &g, &ctr);
   QCH_CUDA(cudaMemsetAsync(ws.p, 0, fused_ws_zero_bytes(M, 1), st));
@@ -596,6 +619,126 @@ int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const doubl
     if (bad_index) *bad_index = (int64_t)b[1];
     return fail(QCH_ERR_NORM_DRIFT, "state norm drifted after interval " + std::to_string(b[1]));
   }
+  return QCH_OK;
+}
+
+}  // namespace qch
+
+
+namespace qch {
+// ---------------------------------------------------------------------------
+// Multi-GPU interval sharding, N <= 4.  Pass 1 (prepare):
+// the fused kernel in prefix mode — propagators, in-tile and tile prefixes,
+// the rank's block product B_r.  The ranks all-gather the B's.  Pass 2
+// (finish): psi_start = B_{r-1}...B_0 psi0 (qch_magnus_apply_prefix_c128),
+// then every thread's start state is one mat-vec chain from the stored
+// prefixes and its 2 propagators give its trajectory rows.
+template <int N>
+__global__ void __launch_bounds__(128) shard_traj_kernel(const double2* __restrict__ ustash,
+                                                         const double2* __restrict__ pex,
+                                                         const double2* __restrict__ etile,
+                                                         const double2* __restrict__ psi_start, int64_t M,
+                                                         double2* __restrict__ traj, unsigned long long* bad) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // thread slot of pass 1
+  const int64_t n0 = k * kR;
+  cplx ps[N], v[N], w[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) ps[q] = d2c(psi_start[q]);
+  if (k == 0) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) traj[q] = c2d(ps[q]);
+  }
+  if (n0 >= M) return;
+  Mat<N> e, pm;
+  ld_mat<N>(e, etile + (k / kFusedThreads) * N * N);
+  ld_mat<N>(pm, pex + k * N * N);
+  mat_vec<N>(e, ps, v);
+  mat_vec<N>(pm, v, w);
+#pragma unroll 1
+  for (int r = 0; r < kR; ++r) {
+    const int64_t n = n0 + r;
+    if (n >= M) break;
+    Mat<N> u;
+    ld_mat<N>(u, ustash + n * N * N);
+    mat_vec<N>(u, w, v);
+    double nrm2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      w[q] = v[q];
+      nrm2 = fma(v[q].re, v[q].re, fma(v[q].im, v[q].im, nrm2));
+      traj[(n + 1) * N + q] = c2d(v[q]);
+    }
+    if (!(fabs(sqrt(nrm2) - 1.0) <= 1e-6)) atomicMin(bad + 1, (unsigned long long)n);  // magnus.py:28
+  }
+}
+
+// workspace: fused state | U (M) | thread prefixes (tiles * 128) | tile prefixes (tiles)
+size_t shard_ws_bytes(int64_t N, int64_t M) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const int64_t tiles = fused_tiles(M);
+  return al(fused_ws_bytes(N, M, 1)) + al(sizeof(double2) * N * N * M) +
+         al(sizeof(double2) * N * N * tiles * kFusedThreads) + al(sizeof(double2) * N * N * tiles);
+}
+struct ShardWs {
+  unsigned char* fused;
+  double2* u;
+  double2* pex;
+  double2* etile;
+};
+ShardWs shard_carve(void* ws, int64_t N, int64_t M) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const int64_t tiles = fused_tiles(M);
+  ShardWs w;
+  w.fused = (unsigned char*)ws;
+  w.u = (double2*)(w.fused + al(fused_ws_bytes(N, M, 1)));
+  w.pex = (double2*)((unsigned char*)w.u + al(sizeof(double2) * N * N * M));
+  w.etile = (double2*)((unsigned char*)w.pex + al(sizeof(double2) * N * N * tiles * kFusedThreads));
+  return w;
+}
+
+int shard_prepare(const SmallArgs& base, int64_t N, int64_t M, void* d_work, double2* d_block, cudaStream_t st) {
+  ShardWs w = shard_carve(d_work, N, M);
+  FusedArgs g;
+  g.s = base;
+  g.s.ubuf = w.u;
+  int* ctr = nullptr;
+  fused_carve(w.fused, N, M, 1, &g, &ctr);
+  QCH_CUDA(cudaMemsetAsync(w.fused, 0, fused_ws_zero_bytes(M, 1), st));
+  QCH_CUDA(cudaMemsetAsync(g.s.bad, 0xff, 2 * sizeof(unsigned long long), st));
+  g.psi0 = nullptr;
+  g.traj = nullptr;
+  g.M = M;
+  g.tile_begin = 0;
+  g.tile_end = fused_tiles(M);
+  g.tile_ctr = ctr;
+  g.stream_blocks_per_sm = 0;
+  g.chunk_flag = nullptr;
+  g.tiles_per_chunk = 1;
+  g.pex = w.pex;
+  g.etile = w.etile;
+  g.block_out = d_block;
+  return fused_launch_any((int)N, g, st);
+}
+
+int shard_finish(int64_t N, int64_t M, void* d_work, const double2* d_psi_start, double2* d_traj,
+                 unsigned long long** bad_out, cudaStream_t st) {
+  ShardWs w = shard_carve(d_work, N, M);
+  FusedArgs g;
+  int* ctr = nullptr;
+  fused_carve(w.fused, N, M, 1, &g, &ctr);
+  const int64_t threads = fused_tiles(M) * kFusedThreads;
+  const unsigned blocks = (unsigned)((threads + 127) / 128);
+  void* pr = prof_begin("shard_traj_kernel", st);
+  switch (N) {
+    case 1: shard_traj_kernel<1><<<blocks, 128, 0, st>>>(w.u, w.pex, w.etile, d_psi_start, M, d_traj, g.s.bad); break;
+    case 2: shard_traj_kernel<2><<<blocks, 128, 0, st>>>(w.u, w.pex, w.etile, d_psi_start, M, d_traj, g.s.bad); break;
+    case 3: shard_traj_kernel<3><<<blocks, 128, 0, st>>>(w.u, w.pex, w.etile, d_psi_start, M, d_traj, g.s.bad); break;
+    default: shard_traj_kernel<4><<<blocks, 128, 0, st>>>(w.u, w.pex, w.etile, d_psi_start, M, d_traj, g.s.bad); break;
+  }
+  prof_end(pr, st);
+  QCH_LAUNCH_CHECK("shard_traj_kernel");
+  note_launch(1);
+  *bad_out = g.s.bad;
   return QCH_OK;
 }
 
@@ -711,6 +854,9 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   g.tile_ctr = ctr;
   g.chunk_flag = nullptr;
   g.tiles_per_chunk = 1;
+  g.pex = nullptr;
+  g.etile = nullptr;
+  g.block_out = nullptr;
   Pipe& pp = pipe_for_device();
   if (sig_stream) {
     const int64_t tiles = fused_tiles(M);

@@ -34,7 +34,10 @@ def shard_bounds(total: int, world: int, rank: int) -> tuple[int, int]:
 
 
 class DeviceMagnusCompute:
-    """libqcheff on the current CUDA device (N <= 4 fused pipeline)."""
+    """libqcheff on the current CUDA device (N <= 4): pass 1 = the fused
+    single-pass kernel in prefix mode (qch_magnus_shard_prepare_c128), pass 2
+    = one mat-vec chain per thread from the stored prefixes
+    (qch_magnus_shard_finish_c128)."""
 
     def __init__(self):
         self.t = _lib.require_cuda()
@@ -44,7 +47,7 @@ class DeviceMagnusCompute:
         from .magnus import _commutators
 
         h0, hk = ch.device_operators()
-        comm = _commutators(ch) if order >= 2 else None
+        comm = _commutators(ch) if order >= 2 and ch.num_controls else None
         sig = _lib.to_device(np.ascontiguousarray(signals_slice), t.float64)
         nbytes = int(_lib.load().qch_magnus_shard_workspace_bytes(ch.dim, m_local))
         work = t.empty(nbytes // 8 + 8, dtype=t.float64, device="cuda")
@@ -79,6 +82,82 @@ class DeviceMagnusCompute:
 
     def to_tensor(self, psi0):
         return _lib.to_device(np.asarray(psi0, dtype=np.complex128))
+
+
+class ShardedEvolvePlan:
+    """A sharded evolve set up once and run many times (new API; the
+    multi-GPU counterpart of ``magnus.EvolvePlan``): this rank's signal slice,
+    workspace and exchange buffers stay on the device, so a step is
+    pass 1 (one fused launch) -> ONE NCCL all-gather of the N x N block
+    products -> apply the rank's prefix -> pass 2 (one launch), with no host
+    synchronisation (``check()`` reads the status words afterwards)."""
+
+    def __init__(self, ch, grid, num_intervals: int, psi0, *, order: int = 1, check: bool = True, group=None):
+        import torch.distributed as dist
+
+        t = _lib.require_cuda()
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        m = int(num_intervals)
+        if m < 1 or (grid.samples - 1) % m:
+            raise GridMismatch(f"{m} intervals do not divide {grid.samples - 1} sample steps")
+        if grid.num_controls != ch.num_controls:
+            raise DimensionMismatch("grid / Hamiltonian control count mismatch")
+        if m < self.world:
+            raise ValueError("need at least one interval per rank")
+        if ch.dim > 4:
+            raise NotImplementedError("sharded evolve covers N <= 4 (the fused pipeline)")
+        from .magnus import _as_state, _commutators
+
+        self.sub = (grid.samples - 1) // m
+        self.start, self.stop = shard_bounds(m, self.world, self.rank)
+        self.m_local = self.stop - self.start
+        self.n = ch.dim
+        self.order, self.check_u = int(order), bool(check)
+        self.dt, self.dt_int = float(grid.dt), (grid.t_end - grid.t_start) / m
+        self.ch = ch
+        self.h0, self.hk = ch.device_operators()
+        self.comm = _commutators(ch) if order >= 2 and ch.num_controls else None
+        sig = grid.signals if ch.num_controls else np.zeros((1, grid.samples))
+        self.sig = _lib.to_device(np.ascontiguousarray(sig[:, self.start * self.sub: self.stop * self.sub + 1]),
+                                  t.float64)
+        self.psi0 = _lib.to_device(_as_state(psi0))
+        nbytes = int(_lib.load().qch_magnus_shard_workspace_bytes(self.n, self.m_local))
+        self.work = t.empty(nbytes // 8 + 8, dtype=t.float64, device="cuda")
+        self.block = t.empty((self.n, self.n), dtype=t.complex128, device="cuda")
+        self.blocks = t.empty((self.world, self.n, self.n), dtype=t.complex128, device="cuda")
+        self.psi_start = t.empty(self.n, dtype=t.complex128, device="cuda")
+        self.traj = t.empty((self.m_local + 1, self.n), dtype=t.complex128, device="cuda")
+        self.flags = t.empty(2, dtype=t.int64, device="cuda")
+
+    def run(self):
+        import torch.distributed as dist
+
+        lib, sp = _lib.load(), _lib.stream_ptr()
+        _lib.check(lib.qch_magnus_shard_prepare_c128(
+            _lib.dptr(self.h0), _lib.dptr(self.hk), _lib.dptr(self.comm), self.ch.num_controls, self.n,
+            _lib.dptr(self.sig), self.sig.shape[1], self.dt, self.dt_int, self.m_local, self.order,
+            1 if self.check_u else 0, _lib.dptr(self.work), _lib.dptr(self.block), sp))
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.blocks, self.block, group=self.group)
+        else:
+            self.blocks[0].copy_(self.block)
+        _lib.check(lib.qch_magnus_apply_prefix_c128(_lib.dptr(self.blocks), self.n, self.rank, _lib.dptr(self.psi0),
+                                                    _lib.dptr(self.psi_start), sp))
+        _lib.check(lib.qch_magnus_shard_finish_async_c128(self.n, self.m_local, _lib.dptr(self.work),
+                                                          _lib.dptr(self.psi_start), _lib.dptr(self.traj),
+                                                          _lib.dptr(self.flags), sp))
+        return self.traj
+
+    def check(self) -> None:
+        a, b = (int(x) for x in _lib.to_host(self.flags).view(np.uint64))
+        if self.check_u and a != (1 << 64) - 1:
+            from .errors import NonFinite
+
+            raise NonFinite(f"propagator not unitary (interval {self.start + a})")
+        if b != (1 << 64) - 1:
+            raise NormDrift(f"state norm drifted after interval {self.start + b}")
 
 
 @dataclass
