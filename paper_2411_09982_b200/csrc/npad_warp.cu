@@ -239,8 +239,8 @@ __device__ __forceinline__ void touch(Touch& tc, int r, int w, int lane) {
 
 // EK: exact keys (q := numpy |z|) for matrices whose entries could leave the
 // normal range of |z|^2 (npad.cu:exact_keys) — the generic candidate path.
-template <bool EK>
-__global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restrict__ jobs, int njobs,
+template <bool EK, bool FULL>
+__global__ void __launch_bounds__(256, 1) npad_trows_warp_kernel(NpadJob2* __restrict__ jobs, int njobs,
                                                               NpadCommon2 cm) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   const int n = cm.n, nT = cm.n_target;
@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
   double2* __restrict__ h = job->h;
   for (int k = lane; k < nwords; k += 32) s_bits[k] = 0u;
   // T membership of this lane's columns x = 32 k + lane (n <= 1024: a register)
-  const bool small_n = n <= 1024;
+  // FULL: n is a multiple of the stage width and <= 1024, so each lane's
+  // columns are x = 32 k + lane, k < 32: T membership fits a register
+  const bool small_n = FULL;
   unsigned tmask = 0u;
   if (small_n)
     for (int k = 0; k * 32 + lane < n; ++k)
@@ -289,7 +291,9 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
   int clock = 0;
   const int nstage = (n + kStageCols - 1) / kStageCols;
 
+  long long cyc_sel = 0, cyc_stage = 0, cyc_post = 0;
   while (true) {
+    const long long c0 = cm.stats ? clock64() : 0;
     // ---- selection over the |T| T-row candidates
     Cand sel = mine;
     const int pl = warp_argmax(sel);
@@ -320,6 +324,7 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
     // matrix is then fully consistent and nothing is stale)
     if (tc.count + 2 > kTouchCap) flush_columns(tc, h, n, lane);
 
+    const long long c1 = cm.stats ? clock64() : 0;
     // ---- stale lists + their async gathers and the two diagonal entries
     // (rows own their diagonal: never stale) ride in the first commit group
     // with ring stage 0; the ring streams rows i, j
@@ -328,15 +333,22 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
     const int ns_j = gather_stale(tc, h, n, j, wj, 1, lane);
     if (lane == 0) cpa16(&wsm->diag[0], ri_p + i);
     if (lane == 1) cpa16(&wsm->diag[1], rj_p + j);
+    // per-lane addresses of the ring (shared) and of rows i, j (global)
+    const unsigned ring_sa = (unsigned)__cvta_generic_to_shared(&wsm->ring[0][0][lane]);
+    const double2* __restrict__ ri_l = ri_p + lane;
+    const double2* __restrict__ rj_l = rj_p + lane;
     auto issue = [&](int stg) {
       if (stg < nstage) {
-        const int slot = stg % kStages;
+        const unsigned sa = ring_sa + (unsigned)((stg & (kStages - 1)) * 2 * kStageCols * 16);
+        const int base = stg * kStageCols;
 #pragma unroll
         for (int k = 0; k < kStageCols / 32; ++k) {
-          const int x = stg * kStageCols + k * 32 + lane;
-          if (x < n) {
-            cpa16(&wsm->ring[slot][0][k * 32 + lane], ri_p + x);
-            cpa16(&wsm->ring[slot][1][k * 32 + lane], rj_p + x);
+          if (FULL || base + k * 32 + lane < n) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + k * 32 * 16), "l"(ri_l + base + k * 32)
+                         : "memory");
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + (kStageCols + k * 32) * 16),
+                         "l"(rj_l + base + k * 32)
+                         : "memory");
           }
         }
       }
@@ -367,26 +379,28 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
         hjj = wsm->diag[1].x;
         givens_fast(v, hii, hjj, &c, &s);
       }
-      const int slot = stg % kStages;
+      const int slot = stg & (kStages - 1);
       const int base = stg * kStageCols;
       // patch stale columns of this stage
-      for (int q = lane; q < ns_i; q += 32) {
-        const int y = wsm->stale_c[0][q];
-        if (y >= base && y < base + kStageCols) wsm->ring[slot][0][y - base] = conj2(wsm->stale_v[0][q]);
+      if (ns_i + ns_j > 0) {
+        for (int q = lane; q < ns_i; q += 32) {
+          const int y = wsm->stale_c[0][q];
+          if (y >= base && y < base + kStageCols) wsm->ring[slot][0][y - base] = conj2(wsm->stale_v[0][q]);
+        }
+        for (int q = lane; q < ns_j; q += 32) {
+          const int y = wsm->stale_c[1][q];
+          if (y >= base && y < base + kStageCols) wsm->ring[slot][1][y - base] = conj2(wsm->stale_v[1][q]);
+        }
+        __syncwarp();
       }
-      for (int q = lane; q < ns_j; q += 32) {
-        const int y = wsm->stale_c[1][q];
-        if (y >= base && y < base + kStageCols) wsm->ring[slot][1][y - base] = conj2(wsm->stale_v[1][q]);
-      }
-      __syncwarp();
       // rotate this stage.  Columns i, j get provisional values here; the 2x2
       // block below overwrites them (same warp, after a __syncwarp).
       const double2* __restrict__ ra = &wsm->ring[slot][0][lane];
       const double2* __restrict__ rb = &wsm->ring[slot][1][lane];
       double2* __restrict__ oi = h + (size_t)i * n + base + lane;
       double2* __restrict__ oj = h + (size_t)j * n + base + lane;
-      const bool full = base + kStageCols <= n;
-      const unsigned tbits = small_n ? (tmask >> (base >> 5)) : 0u;
+      const bool full = FULL || base + kStageCols <= n;
+      const unsigned tbits = FULL ? (tmask >> (base >> 5)) : 0u;
 #pragma unroll
       for (int k = 0; k < kStageCols / 32; ++k) {
         const int x = base + k * 32 + lane;
@@ -395,7 +409,7 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
         rotate_rows_fast(c, s, d2c(ra[k * 32]), d2c(rb[k * 32]), &ni, &nj);
         oi[k * 32] = c2d(ni);
         oj[k * 32] = c2d(nj);
-        const bool inTx = small_n ? ((tbits >> k) & 1u) != 0u : s_kof[x] >= 0;
+        const bool inTx = FULL ? ((tbits >> k) & 1u) != 0u : s_kof[x] >= 0;
         if (!inTx) {
           if (x != u) {
             if (EK) {
@@ -412,6 +426,7 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
       __syncwarp();  // ring slot reuse
     }
     cpa_wait<0>();
+    const long long c2 = cm.stats ? clock64() : 0;
     __syncwarp();  // provisional writes of columns i, j before the 2x2 block
     if (!EK && lbt.x >= 0) pt = tcand(lbt.v, t, lbt.x, ek);
     // the 2x2 block (npad.py:136-144 incl. the Hermitian pin) and its
@@ -494,6 +509,12 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
       const Cand best = (wl >= 0) ? shfl_cand(pr, wl) : cand_none();
       if (lane == kr) mine = best;
     }
+    if (cm.stats) {
+      const long long c3 = clock64();
+      cyc_sel += c1 - c0;
+      cyc_stage += c2 - c1;
+      cyc_post += c3 - c2;
+    }
     ++applied;
   }
 
@@ -506,7 +527,17 @@ __global__ void __launch_bounds__(256) npad_trows_warp_kernel(NpadJob2* __restri
   if (lane == 0) {
     job->applied = applied;
     job->status = status;
-    if (cm.stats) job->stats[0] += rescans;
+    if (cm.stats) {
+      job->stats[0] += rescans;
+      job->stats[1] += cyc_sel;
+      job->stats[2] += cyc_stage;
+      job->stats[3] += cyc_post;
+      if (blockIdx.x == 0 && wib == 0)
+        printf("npad warp driver: chain 0: %lld rotations, %.2f rescans/rot, cycles/rot: select %.0f, rows %.0f, "
+               "fold+rescan %.0f\n", applied, (double)rescans / (applied ? applied : 1),
+               (double)cyc_sel / (applied ? applied : 1), (double)cyc_stage / (applied ? applied : 1),
+               (double)cyc_post / (applied ? applied : 1));
+    }
   }
 }
 
@@ -522,7 +553,9 @@ int npad_launch_trows_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cud
   while (wpb > 1 && trows_warp_smem(cm.n, wpb) > (size_t)max_smem_optin()) wpb >>= 1;
   const size_t smem = trows_warp_smem(cm.n, wpb);
   if (smem > (size_t)max_smem_optin()) return fail(QCH_ERR_UNSUPPORTED, "npad: warp T-rows driver shared memory");
-  auto kern = cm.ek ? npad_trows_warp_kernel<true> : npad_trows_warp_kernel<false>;
+  const bool full = cm.n % kStageCols == 0 && cm.n <= 1024;
+  auto kern = cm.ek ? (full ? npad_trows_warp_kernel<true, true> : npad_trows_warp_kernel<true, false>)
+                    : (full ? npad_trows_warp_kernel<false, true> : npad_trows_warp_kernel<false, false>);
   QCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (njobs + wpb - 1) / wpb;
   void* pr = prof_begin("npad_run_kernel", st);
