@@ -510,6 +510,61 @@ def sec_magnus4096(torch, eff, lib, args, fp64, n_int=2):
                                        "OpenBLAS); not re-timed here (42 h full run)"}}
 
 
+def sec_givens(torch, eff, lib, args, peaks, sizes=(10**5, 10**6, 10**7, 10**8)):
+    """SURVEY 8(f) rank 1 / the paper's Fig. 4 protocol (bench_givens,
+    experiments.py:420-453): ONE Givens rotation eliminating the smallest
+    coupling (0, 1) of the sparse ladder a^dag a + (a + a^dag) (CSR, built on
+    the device), through the public eliminate_coupling."""
+    from oracle import npad_oracle
+
+    rows = []
+    for n in sizes:
+        op = eff.ladder_test_hamiltonian_device(n)
+        st0 = eff.NPADState.from_operator(op)
+        for _ in range(2):
+            eff.eliminate_coupling(st0, 0, 1)
+        torch.cuda.synchronize()
+        lib.profile_read(reset=True)
+        lib.profile_enable(True)
+        reps = 5
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            out = eff.eliminate_coupling(st0, 0, 1)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / reps
+        lib.profile_enable(False)
+        prof = lib.profile_read(reset=True)
+        nnz = 3 * n - 3
+        # algorithmic bytes: the input CSR read and the new CSR written
+        # (int64 indptr, int32 indices, complex128 values)
+        byts = 2 * (8 * (n + 1) + 20 * nnz)
+        k = prof.get("npad_sparse_rotate")
+        kms = k[0] / k[1] if k else None
+        s_ms = prof["npad_sparse_stream"][0] / prof["npad_sparse_stream"][1] if "npad_sparse_stream" in prof else None
+        row = {"n": n, "nnz_in": nnz, "nnz_out": out.current.nnz, "ms_per_rotation_e2e": wall * 1e3,
+               "ms_kernels": kms, "ms_streaming_passes": s_ms,
+               "achieved_gbs_streaming": byts / (s_ms * 1e-3) / 1e9 if s_ms else None}
+        if n <= 10**6:
+            host = eff.ladder_test_hamiltonian(n).data
+            t0 = time.perf_counter()
+            npad_oracle.eliminate_sparse(host, 0, 1)
+            row["cpu_ms"] = (time.perf_counter() - t0) * 1e3
+        rows.append(row)
+        del op, st0, out
+    big = rows[-1]
+    return {"workload": "SURVEY 8(f) rank 1 — bench_givens (PAPER.md:180-183): one sparse Givens rotation on the "
+                        "ladder a^dag a + (a + a^dag), N = 1e5..1e8 (CSR on the device)",
+            "metric": "rotation time", "unit": "ms", "value": big["ms_per_rotation_e2e"], "higher_is_better": False,
+            "sizes": rows,
+            "roofline": {"bound": "hbm", "achieved": big["achieved_gbs_streaming"], "peak": peaks[0], "unit": "GB/s",
+                         "frac": (big["achieved_gbs_streaming"] / peaks[0]) if big["achieved_gbs_streaming"] else None,
+                         "note": "the two streaming passes (new indptr, shifted copy of every other row) of the "
+                                 "largest size; algorithmic bytes = input CSR read + output CSR write"},
+            "cpu_baseline": {"value": rows[1].get("cpu_ms"), "unit": "ms at N = 1e6", "cores": 1, "kind": "port",
+                             "sample": "oracle/npad_oracle.eliminate_sparse (scipy restatement of "
+                                       "_conjugate_sparse) at N = 1e5 and 1e6"}}
+
+
 # --------------------------------------------------------------- reference --
 
 def run_reference(args, world, rank):
@@ -591,7 +646,7 @@ def main():
 
     secondary = []
     if rank == 0 and world == 1 and args.secondary != "none":
-        want = {"npad60", "npad4096", "sweep", "magnus4096"} if args.secondary == "all" else set(
+        want = {"npad60", "npad4096", "sweep", "magnus4096", "givens"} if args.secondary == "all" else set(
             args.secondary.split(","))
         peaks = (hbm_peak, hbm_src)
         if "npad60" in want:
@@ -602,6 +657,8 @@ def main():
             secondary.append(sec_sweep(torch, eff, lib, args, peaks))
         if "magnus4096" in want:
             secondary.append(sec_magnus4096(torch, eff, lib, args, fp64))
+        if "givens" in want:
+            secondary.append(sec_givens(torch, eff, lib, args, peaks))
 
     if rank == 0:
         cpu_v, cpu_t = cpu_magnus_sample(__import__("paper_2411_09982_b200.models", fromlist=["x"]), 60000)

@@ -101,6 +101,28 @@ int qch_npad_run_batch_c128(void* d_h, int64_t batch, int64_t n, const int32_t* 
  * configs: for each b, params[4b..4b+3] =
  * {omega_q, alpha, omega_r, g}; H = wq n + a/2 n(n-1) (x) I + I (x) wr a^dag a
  * + g (b + b^dag) (x) (a + a^dag), index q*n_r + k.  d_h: (batch, nq*nr)^2. */
+/* _conjugate_sparse (npad.py:148-232) on a device CSR (indptr int64 (n+1),
+ * sorted int32 column indices, complex128 values, no explicit zeros): the
+ * NEW CSR of U H U^dag for the rotation (i < j; c = cos_half and
+ * s = -sin_half e^{i phase} as _block_params, npad.py:126-128), fill-in
+ * below 1e-15 * max_abs dropped.  Output capacity out_cap entries (the new
+ * nnz is at most nnz + 4 (len(row i) + len(row j)) + 8); *nnz_out (host)
+ * receives the new nnz.  Synchronous.  Bit-identical to the reference. */
+int qch_npad_sparse_rotate_c128(const int64_t* d_indptr, const int32_t* d_indices, const void* d_data, int64_t n,
+                                int64_t nnz, int64_t i, int64_t j, double cos_half, double s_re, double s_im,
+                                double max_abs, int64_t* d_out_indptr, int32_t* d_out_indices, void* d_out_data,
+                                int64_t out_cap, int64_t* nnz_out, void* stream);
+/* ladder_test_hamiltonian (models.py:194-209), the bench_givens operator
+ * a^dag a + (a + a^dag) on n levels, built on the device as a CSR:
+ * d_indptr (n+1) int64, d_indices / d_data (3n - 3; the zero diagonal entry (0,0) is
+ * not stored, as HermitianOperator eliminates explicit zeros). */
+int qch_build_ladder_csr_c128(int64_t n, int64_t* d_indptr, int32_t* d_indices, void* d_data, void* stream);
+/* HermitianOperator.entry on a device CSR: d_out (3 complex, device) =
+ * H[j,i], H[i,i], H[j,j] — the inputs of givens_rotation_matrix
+ * (npad.py:111-117). */
+int qch_npad_sparse_entries_c128(const int64_t* d_indptr, const int32_t* d_indices, const void* d_data, int64_t n,
+                                 int64_t i, int64_t j, void* d_out, void* stream);
+
 int qch_build_transmon_resonator_c128(void* d_h, int64_t batch, int64_t n_q, int64_t n_r,
                                       const double* d_params, void* stream);
 

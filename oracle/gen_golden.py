@@ -53,15 +53,64 @@ def random_hermitian(n: int, seed: int) -> np.ndarray:
     return (a + a.conj().T) / 2.0
 
 
+def sparse_cases(eff) -> None:
+    """10. Sparse CSR rotations (npad.py:148-232): the bench_givens ladder
+    (experiments.py:420-453), a sparse npad_run chain (pivot log + every
+    intermediate operator is replayable), and a fill-in drop case."""
+    import scipy.sparse as sps
+
+    out = {}
+    # (a) ladder a^dag a + (a + a^dag), N = 1000, the smallest coupling (0, 1)
+    lad = eff.ladder_test_hamiltonian(1000)
+    r = eff.eliminate_coupling(eff.NPADState.from_operator(lad), 0, 1).current.data
+    out.update(lad_indptr=lad.data.indptr, lad_indices=lad.data.indices, lad_data=lad.data.data,
+               lad_out_indptr=r.indptr, lad_out_indices=r.indices, lad_out_data=r.data)
+    # (b) random sparse Hermitian (bitwise), greedy npad_run for 40 rotations
+    rng = np.random.default_rng(5)
+    n = 200
+    a = sps.random(n, n, density=0.03, random_state=rng, dtype=np.complex128, data_rvs=lambda k: rng.standard_normal(k)
+                   + 1j * rng.standard_normal(k), format="csr")
+    h = sps.triu(a + a.conj().T, k=1)
+    h = (h + h.conj().T + sps.diags(np.linspace(0.0, 5.0, n))).tocsr().astype(np.complex128)
+    h.sum_duplicates()
+    h.sort_indices()
+    op = eff.HermitianOperator(h)
+    st, piv = _logged_run(eff, op, tol=1e-12, max_iter=40)
+    fin = st.current.data
+    out.update(rnd_indptr=h.indptr, rnd_indices=h.indices, rnd_data=h.data, rnd_pivots=piv,
+               rnd_out_indptr=fin.indptr, rnd_out_indices=fin.indices, rnd_out_data=fin.data)
+    # (c) exact cancellation: rows (p, q) of level 2 aligned with an eigenvector
+    # of the (0, 1) block, so one new coupling falls under the drop threshold
+    blk = np.array([[1.0, 0.3 - 0.4j], [0.3 + 0.4j, -0.5]])
+    w, vecs = np.linalg.eigh(blk)
+    pq = 0.7 * vecs[:, 0].conj()
+    dense = np.zeros((3, 3), dtype=complex)
+    dense[:2, :2] = blk
+    dense[2, 2] = 2.0
+    dense[0, 2], dense[1, 2] = pq[0], pq[1]
+    dense[2, 0], dense[2, 1] = np.conj(pq[0]), np.conj(pq[1])
+    hc = sps.csr_matrix(dense)
+    rc = eff.eliminate_coupling(eff.NPADState.from_operator(eff.HermitianOperator(hc, validate=False)), 0, 1)
+    rc = rc.current.data
+    out.update(can_dense=dense, can_out_indptr=rc.indptr, can_out_indices=rc.indices, can_out_data=rc.data)
+    np.savez_compressed(GOLD / "npad_sparse.npz", **out)
+    print("sparse: ladder nnz", lad.data.nnz, "->", r.nnz, "; random", h.nnz, "->", fin.nnz, "applied", st.applied,
+          "; cancel", hc.nnz, "->", rc.nnz)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
+    ap.add_argument("--only", default=None, help="'sparse': regenerate only the sparse CSR vectors")
     args = ap.parse_args()
     eff = _import_reference(args.ref)
     sys.path.insert(0, str(ROOT))
     from paper_2411_09982_b200 import models as M  # host builders only (numpy)
 
     GOLD.mkdir(parents=True, exist_ok=True)
+    if args.only == "sparse":
+        sparse_cases(eff)
+        return
 
     # 1. NPAD config 1: transmon 3 x resonator 20, full mode, tol 1e-12
     h = M.transmon_resonator_hamiltonian(3, 20).data
@@ -150,6 +199,7 @@ def main() -> None:
                         controls=np.stack([c.to_dense() for c in ch6.controls]), signals=grid6.signals,
                         t=np.array([grid6.t_start, grid6.t_end]), m=20, psi0=psi6, traj=traj6.amplitudes,
                         coeffs=eff.magnus_coefficients(grid6, 20))
+    sparse_cases(eff)
     print("wrote", sorted(p.name for p in GOLD.glob("*.npz")))
 
 

@@ -217,3 +217,109 @@ def eliminate_pairs(h0: np.ndarray, pairs, u0=None):
         if u is not None:
             rotate_unitary(u, i, j, c, s)
     return h, u
+
+
+# ---------------------------------------------------------------------------
+# Sparse CSR rotation (npad.py:148-232): the restatement the GPU sparse path
+# is checked against (and pinned to the reference by tests/golden/npad_sparse.npz).
+
+def _csr_entry(m, r: int, c: int) -> complex:
+    """HermitianOperator.entry on CSR (operators.py:101-102)."""
+    lo, hi = m.indptr[r], m.indptr[r + 1]
+    cols = m.indices[lo:hi]
+    pos = int(np.searchsorted(cols, c))
+    if pos < cols.size and cols[pos] == c:
+        return complex(m.data[lo + pos])
+    return 0j
+
+
+def sparse_rotation_scalars(m, i: int, j: int):
+    """givens_rotation_matrix (npad.py:101-123) on a CSR operator."""
+    v = _csr_entry(m, j, i)
+    g = abs(v)
+    phase = float(np.angle(v))
+    delta = (_csr_entry(m, i, i).real - _csr_entry(m, j, j).real) / 2.0
+    radius = math.hypot(delta, g)
+    sign = 1.0 if delta >= 0.0 else -1.0
+    cos_t = abs(delta) / radius
+    sin_t = sign * g / radius
+    cos_half = math.sqrt((1.0 + cos_t) / 2.0)
+    return cos_half, sin_t / (2.0 * cos_half), phase, delta == 0.0
+
+
+def _row_combination(m, i, j, wi, wj):
+    """npad.py:148-159."""
+    ci = m.indices[m.indptr[i]:m.indptr[i + 1]]
+    vi = m.data[m.indptr[i]:m.indptr[i + 1]]
+    cj = m.indices[m.indptr[j]:m.indptr[j + 1]]
+    vj = m.data[m.indptr[j]:m.indptr[j + 1]]
+    cols = np.concatenate([ci, cj])
+    vals = np.concatenate([wi * vi, wj * vj])
+    uniq, inv = np.unique(cols, return_inverse=True)
+    acc = np.zeros(uniq.size, dtype=np.complex128)
+    np.add.at(acc, inv, vals)
+    return uniq, acc
+
+
+def _get_at(cols, vals, k) -> complex:
+    pos = np.searchsorted(cols, k)
+    if pos < cols.size and cols[pos] == k:
+        return complex(vals[pos])
+    return 0.0
+
+
+def _set_at(cols, vals, k, value):
+    pos = int(np.searchsorted(cols, k))
+    if pos < cols.size and cols[pos] == k:
+        vals[pos] = value
+        return cols, vals
+    return np.insert(cols, pos, k), np.insert(vals, pos, value)
+
+
+def conjugate_sparse(m, i: int, j: int, cos_half: float, sin_half: float, phase: float, max_abs: float):
+    """_conjugate_sparse (npad.py:178-232), statement by statement: the new
+    CSR after U H U^dag on rows/columns i < j, fill-in below 1e-15 * max|H|
+    dropped (npad.py:33)."""
+    import scipy.sparse as sps
+
+    c, s = cos_half, -sin_half * np.exp(1j * phase)  # _block_params (npad.py:126-128)
+    ca, va = _row_combination(m, i, j, c, -np.conj(s))
+    cb, vb = _row_combination(m, i, j, s, c)
+    ai, aj = _get_at(ca, va, i), _get_at(ca, va, j)
+    bi, bj = _get_at(cb, vb, i), _get_at(cb, vb, j)
+    new_ai = (c * ai - s * aj).real
+    new_aj = np.conj(s) * ai + c * aj
+    new_bj = (np.conj(s) * bi + c * bj).real
+    ca, va = _set_at(ca, va, i, new_ai)
+    ca, va = _set_at(ca, va, j, new_aj)
+    cb, vb = _set_at(cb, vb, i, np.conj(new_aj))
+    cb, vb = _set_at(cb, vb, j, new_bj)
+    drop = 1e-15 * max_abs
+    keep_a = np.abs(va) > drop
+    keep_b = np.abs(vb) > drop
+    ca, va = ca[keep_a], va[keep_a]
+    cb, vb = cb[keep_b], vb[keep_b]
+    data = m.data.copy()
+    data[m.indptr[i]:m.indptr[i + 1]] = 0
+    data[m.indptr[j]:m.indptr[j + 1]] = 0
+    data[np.isin(m.indices, (i, j))] = 0
+    base = sps.csr_matrix((data, m.indices.copy(), m.indptr.copy()), shape=m.shape)
+    other_a = (ca != i) & (ca != j)
+    other_b = (cb != i) & (cb != j)
+    rows = np.concatenate([np.full(ca.size, i, dtype=np.int64), np.full(cb.size, j, dtype=np.int64),
+                           ca[other_a].astype(np.int64), cb[other_b].astype(np.int64)])
+    cols = np.concatenate([ca.astype(np.int64), cb.astype(np.int64), np.full(int(other_a.sum()), i, dtype=np.int64),
+                           np.full(int(other_b.sum()), j, dtype=np.int64)])
+    vals = np.concatenate([va, vb, np.conj(va[other_a]), np.conj(vb[other_b])])
+    delta = sps.csr_matrix((vals, (rows, cols)), shape=m.shape)
+    out = base + delta
+    out.eliminate_zeros()
+    out.sort_indices()
+    return out
+
+
+def eliminate_sparse(m, i: int, j: int):
+    """eliminate_coupling (npad.py:262-271) on a CSR operator."""
+    max_abs = float(np.max(np.abs(m.data))) if m.nnz else 0.0
+    ch, sh, ph, _ = sparse_rotation_scalars(m, i, j)
+    return conjugate_sparse(m, i, j, ch, sh, ph, max_abs)

@@ -70,6 +70,14 @@ PROTOTYPES = {
     "qch_magnus_shard_finish_c128": (c_int, [c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_int, P_int64, c_void_p]),
     "qch_magnus_shard_finish_async_c128": (
         c_int, [c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "qch_npad_sparse_rotate_c128": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_double, c_double, c_double, c_double,
+         c_void_p, c_void_p, c_void_p, c_int64, P_int64, c_void_p],
+    ),
+    "qch_build_ladder_csr_c128": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "qch_npad_sparse_entries_c128": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p,
+                                             c_void_p]),
     "qch_peak_kernel": (c_int, [c_int, c_int, c_int, c_void_p, ctypes.POINTER(c_double), c_void_p]),
     "qch_profile_enable": (None, [c_int]),
     "qch_profile_read": (c_int, [c_void_p, c_void_p, ctypes.c_char_p, c_int64, c_int, c_int]),

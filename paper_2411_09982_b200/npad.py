@@ -161,6 +161,59 @@ def _audit(d_u, applied: int, dim: int) -> None:
         raise UnitarityDrift(f"accumulated unitary drift {drift:.3e} after {applied} rotations")
 
 
+# -- sparse CSR path (npad.py:148-232) -------------------------------------------------
+
+def _is_sparse(op: HermitianOperator) -> bool:
+    return op.layout == "sparse"
+
+
+def _sparse_rotation(op: HermitianOperator, i: int, j: int) -> GivensRotation:
+    """givens_rotation_matrix (npad.py:101-123) on a sparse operator: the three
+    entries come from the device CSR, the scalars are formed exactly as the
+    reference forms them (Python / numpy scalar math)."""
+    import math
+
+    t = _lib.require_cuda()
+    ip, ix, dv = op.device_csr()
+    out = t.empty(3, dtype=t.complex128, device="cuda")
+    _lib.call("qch_npad_sparse_entries_c128", _lib.dptr(ip), _lib.dptr(ix), _lib.dptr(dv), op.dim, i, j,
+              _lib.dptr(out), _lib.stream_ptr())
+    v, hii, hjj = (complex(z) for z in _lib.to_host(out))
+    if v == 0:
+        raise ZeroCoupling(f"entry ({j}, {i}) is zero; nothing to eliminate")
+    g = abs(v)
+    phi = float(np.angle(v))
+    delta = (hii.real - hjj.real) / 2.0
+    r = math.hypot(delta, g)
+    sgn = 1.0 if delta >= 0.0 else -1.0
+    cos_t = abs(delta) / r
+    sin_t = sgn * g / r
+    cos_half = math.sqrt((1.0 + cos_t) / 2.0)
+    sin_half = sin_t / (2.0 * cos_half)
+    return GivensRotation(i, j, cos_half, sin_half, phi, degenerate=(delta == 0.0))
+
+
+def _sparse_transform(op: HermitianOperator, rot: GivensRotation) -> HermitianOperator:
+    """U H U^dag on the device CSR (qch_npad_sparse_rotate_c128): a new sparse
+    operator, bit-identical to the reference's _conjugate_sparse."""
+    t = _lib.require_cuda()
+    ip, ix, dv = op.device_csr()
+    nnz = int(dv.numel())
+    ends = _lib.to_host(ip[[rot.i, rot.i + 1, rot.j, rot.j + 1]])
+    cap = nnz + 4 * int((ends[1] - ends[0]) + (ends[3] - ends[2])) + 8
+    out_ip = t.empty(op.dim + 1, dtype=t.int64, device="cuda")
+    out_ix = t.empty(cap, dtype=t.int32, device="cuda")
+    out_dv = t.empty(cap, dtype=t.complex128, device="cuda")
+    s = -rot.sin_half * np.exp(1j * rot.phase)  # _block_params (npad.py:126-128)
+    nnz_out = ctypes.c_int64(0)
+    _lib.check(_lib.load().qch_npad_sparse_rotate_c128(
+        _lib.dptr(ip), _lib.dptr(ix), _lib.dptr(dv), op.dim, nnz, rot.i, rot.j, float(rot.cos_half), float(s.real),
+        float(s.imag), float(op.max_abs()), _lib.dptr(out_ip), _lib.dptr(out_ix), _lib.dptr(out_dv), cap,
+        ctypes.byref(nnz_out), _lib.stream_ptr()))
+    k = int(nnz_out.value)
+    return HermitianOperator._from_device_csr(out_ip, out_ix[:k], out_dv[:k], op.dim)
+
+
 # -- reference API -----------------------------------------------------------------
 
 def givens_rotation_matrix(op: HermitianOperator, i: int, j: int) -> GivensRotation:
@@ -169,6 +222,8 @@ def givens_rotation_matrix(op: HermitianOperator, i: int, j: int) -> GivensRotat
     ZeroCoupling when H[j, i] == 0; a degenerate pair (delta == 0) is flagged.
     """
     _check_pair(op, i, j)
+    if _is_sparse(op):
+        return _sparse_rotation(op, i, j)
     _, _, params, status = _device_params(op, [(i, j)])
     if status[0] != 0:
         raise ZeroCoupling(f"entry ({j}, {i}) is zero; nothing to eliminate")
@@ -179,6 +234,8 @@ def unitary_transformation(op: HermitianOperator, rot: GivensRotation) -> Hermit
     """U H U^dag for one rotation; only rows/columns i, j change (npad.py:235-241)."""
     if rot.j >= op.dim:
         raise IndexOutOfRange(f"rotation indices ({rot.i}, {rot.j}) exceed dim {op.dim}")
+    if _is_sparse(op):
+        return _sparse_transform(op, rot)
     d_pairs = _lib.to_device(np.array([[rot.i, rot.j]], dtype=np.int64))
     d_params = _lib.to_device(_params_from_rotations([rot]))
     new_op, _, _ = _apply(op, d_pairs, d_params, 1, None)
@@ -203,6 +260,14 @@ def eliminate_couplings(state: NPADState, pairs: Sequence[tuple[int, int]]) -> N
     op = state.current
     for i, j in pairs:
         _check_pair(op, i, j)
+    if _is_sparse(op) and state.accumulated_unitary is None:
+        # the reference's sparse branch: every rotation built from the input
+        # operator, applied in list order (npad.py:287-296)
+        rots = [_sparse_rotation(op, i, j) for i, j in pairs]
+        cur = op
+        for rot in rots:
+            cur = _sparse_transform(cur, rot)
+        return replace(state, current=cur, applied=state.applied + len(pairs))
     d_pairs, d_params, _, status = _device_params(op, pairs)
     bad = np.flatnonzero(status)
     if bad.size:

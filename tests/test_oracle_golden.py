@@ -56,3 +56,30 @@ def test_magnus_oracle(golden, case):
     if "hbar_head" in g:
         hb = magnus_oracle.effective_hamiltonians(g["drift"], g["controls"], g["signals"], t0, t1, m)
         np.testing.assert_array_equal(hb[:16], g["hbar_head"])
+
+
+def test_sparse_rotation_oracle_bit_exact(golden):
+    """The CSR rotation restatement (npad_oracle.conjugate_sparse) against the
+    reference's own _conjugate_sparse (npad.py:148-232): same structure, same
+    bits."""
+    import scipy.sparse as sps
+
+    g = golden("npad_sparse")
+
+    def csr(p, n):
+        return sps.csr_matrix((g[p + "_data"], g[p + "_indices"], g[p + "_indptr"]), shape=(n, n))
+
+    def same(a, b):
+        np.testing.assert_array_equal(a.indptr, b.indptr)
+        np.testing.assert_array_equal(a.indices, b.indices)
+        np.testing.assert_array_equal(a.data, b.data)
+
+    n_lad = g["lad_indptr"].size - 1
+    same(npad_oracle.eliminate_sparse(csr("lad", n_lad), 0, 1), csr("lad_out", n_lad))
+    n = g["rnd_indptr"].size - 1
+    m = csr("rnd", n)
+    for i, j in g["rnd_pivots"]:
+        m = npad_oracle.eliminate_sparse(m, int(i), int(j))
+    same(m, csr("rnd_out", n))
+    out = npad_oracle.eliminate_sparse(sps.csr_matrix(g["can_dense"]), 0, 1)
+    same(out, csr("can_out", 3))
