@@ -112,6 +112,12 @@ int qch_npad_sparse_rotate_c128(const int64_t* d_indptr, const int32_t* d_indice
                                 int64_t nnz, int64_t i, int64_t j, double cos_half, double s_re, double s_im,
                                 double max_abs, int64_t* d_out_indptr, int32_t* d_out_indices, void* d_out_data,
                                 int64_t out_cap, int64_t* nnz_out, void* stream);
+/* _largest_relevant (npad.py:300-317) on a device CSR: host out[3] =
+ * (i, j, numpy |H[j, i]|) of the largest strict-lower-triangle entry (subspace
+ * mode: d_mask n bytes, exactly one endpoint in the target), ties to the
+ * smallest (i, j); i = j = -1 when there is none.  n < 65536.  Synchronous. */
+int qch_npad_sparse_select_c128(const int64_t* d_indptr, const int32_t* d_indices, const void* d_data, int64_t n,
+                                const unsigned char* d_mask, int exact_keys, double* out, void* stream);
 /* ladder_test_hamiltonian (models.py:194-209), the bench_givens operator
  * a^dag a + (a + a^dag) on n levels, built on the device as a CSR:
  * d_indptr (n+1) int64, d_indices / d_data (3n - 3; the zero diagonal entry (0,0) is

@@ -75,6 +75,8 @@ PROTOTYPES = {
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_double, c_double, c_double, c_double,
          c_void_p, c_void_p, c_void_p, c_int64, P_int64, c_void_p],
     ),
+    "qch_npad_sparse_select_c128": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int, c_void_p,
+                                            c_void_p]),
     "qch_build_ladder_csr_c128": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "qch_npad_sparse_entries_c128": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p,
                                              c_void_p]),

@@ -476,3 +476,95 @@ extern "C" int qch_build_ladder_csr_c128(int64_t n, int64_t* d_indptr, int32_t* 
   note_launch(1);
   return QCH_OK;
 }
+
+// ---------------------------------------------------------------------------
+// _largest_relevant (npad.py:300-317) on a device CSR: the strict-lower-
+// triangle entry of largest numpy |z| (subspace mode: exactly one endpoint in
+// the target), ties to the smallest (c, r).  Thread per row, block argmax,
+// then one block over the block winners.
+#include "npad_select.cuh"
+
+namespace qch {
+namespace {
+
+constexpr int kSelThreads = 256;
+
+__device__ __forceinline__ Cand sel_shfl(const Cand& c, int src) {
+  Cand o;
+  o.q = __shfl_sync(kFull, c.q, src);
+  o.m = __shfl_sync(kFull, c.m, src);
+  o.cr = __shfl_sync(kFull, c.cr, src);
+  o.v.x = __shfl_sync(kFull, c.v.x, src);
+  o.v.y = __shfl_sync(kFull, c.v.y, src);
+  return o;
+}
+
+__device__ Cand sel_block_best(Cand c) {
+  __shared__ Cand s_w[kSelThreads / 32];
+  const int wl = warp_argmax(c);
+  const Cand w = (wl >= 0) ? sel_shfl(c, wl) : cand_none();
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = w;
+  __syncthreads();
+  Cand b = s_w[0];
+  for (int k = 1; k < kSelThreads / 32; ++k) cand_take(b, s_w[k]);
+  __syncthreads();
+  return b;
+}
+
+__global__ void sparse_select_kernel(const int64_t* indptr, const int32_t* indices, const double2* data, int64_t n,
+                                     const unsigned char* inT, int ek, Cand* part) {
+  Cand best = cand_none();
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r < n) {
+    for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) {
+      const int c = indices[e];
+      if (c >= r) break;  // sorted: the strict lower part comes first
+      if (inT != nullptr && inT[c] == inT[r]) continue;
+      const double2 v = data[e];
+      if (v.x == 0.0 && v.y == 0.0) continue;
+      cand_take(best, make_cand(v, ((unsigned)c << 16) | (unsigned)r, ek != 0));
+    }
+  }
+  const Cand b = sel_block_best(best);
+  if (threadIdx.x == 0) part[blockIdx.x] = b;
+}
+
+__global__ void sparse_select_final_kernel(const Cand* part, int64_t nparts, double* out) {
+  Cand best = cand_none();
+  for (int64_t k = threadIdx.x; k < nparts; k += blockDim.x) cand_take(best, part[k]);
+  const Cand b = sel_block_best(best);
+  if (threadIdx.x == 0) {
+    out[0] = (b.q > 0.0) ? (double)(b.cr >> 16) : -1.0;
+    out[1] = (b.q > 0.0) ? (double)(b.cr & 0xffffu) : -1.0;
+    out[2] = (b.q > 0.0) ? np_cabs(b.v.x, b.v.y) : 0.0;
+  }
+}
+
+}  // namespace
+}  // namespace qch
+
+// (i, j, |H[j, i]|) of the largest relevant coupling of a device CSR
+// (npad.py:300-317); i = j = -1 when there is none.  d_mask: n bytes, 1 for
+// target levels (null: full mode).  Synchronous; result in host out[3].
+// Indices must be < 65536 (the packed tie-break key).
+extern "C" int qch_npad_sparse_select_c128(const int64_t* d_indptr, const int32_t* d_indices, const void* d_data,
+                                           int64_t n, const unsigned char* d_mask, int exact_keys, double* out,
+                                           void* stream) {
+  if (n >= 65536) return fail(QCH_ERR_UNSUPPORTED, "sparse npad_run: dimension must be < 65536");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t blocks = (n + kSelThreads - 1) / kSelThreads;
+  void* ws = nullptr;
+  ensure_pool();
+  QCH_CUDA(cudaMallocAsync(&ws, sizeof(Cand) * blocks + 64, st));
+  Cand* part = (Cand*)ws;
+  double* d_out = (double*)(part + blocks);
+  sparse_select_kernel<<<(unsigned)std::max<int64_t>(1, blocks), kSelThreads, 0, st>>>(
+      d_indptr, d_indices, (const double2*)d_data, n, d_mask, exact_keys, part);
+  sparse_select_final_kernel<<<1, kSelThreads, 0, st>>>(part, std::max<int64_t>(1, blocks), d_out);
+  QCH_LAUNCH_CHECK("sparse_select_kernel");
+  note_launch(2);
+  QCH_CUDA(cudaMemcpyAsync(out, d_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  QCH_CUDA(cudaFreeAsync(ws, st));
+  QCH_CUDA(cudaStreamSynchronize(st));
+  return QCH_OK;
+}

@@ -295,11 +295,56 @@ def _target_tensor(target, dim: int):
     return _lib.to_device(arr), len(tset)
 
 
+def _npad_run_sparse(op, target, tol, max_iter, pivot_cap):
+    """The reference's greedy loop (npad.py:320-354) on a sparse operator: each
+    step selects the largest relevant coupling of the device CSR
+    (qch_npad_sparse_select_c128) and applies the sparse rotation — the
+    operator stays sparse and fill-in is dropped exactly as the reference's
+    _conjugate_sparse drops it."""
+    t = _lib.require_cuda()
+    d_target, n_target = _target_tensor(target, op.dim)
+    mask = None
+    if d_target is not None:
+        mask = t.zeros(op.dim, dtype=t.uint8, device="cuda")
+        if n_target:
+            mask[d_target[:n_target].long()] = 1
+    threshold = tol * op.max_abs()
+    ek = 1 if (op.max_abs() > 1e100 or (0.0 < threshold < 1e-140)) else 0
+    state = NPADState.from_operator(op)
+    cur = op
+    pivots = []
+    out = (ctypes.c_double * 3)()
+    applied = 0
+    converged = False
+    while True:
+        ip, ix, dv = cur.device_csr()
+        _lib.call("qch_npad_sparse_select_c128", _lib.dptr(ip), _lib.dptr(ix), _lib.dptr(dv), cur.dim,
+                  _lib.dptr(mask), ek, out, _lib.stream_ptr())
+        i, j, mag = int(out[0]), int(out[1]), float(out[2])
+        if i < 0 or mag < threshold:
+            converged = True
+            break
+        if applied >= max_iter:
+            break
+        if len(pivots) < pivot_cap:
+            pivots.append((i, j))
+        rot = _sparse_rotation(cur, i, j)
+        cur = _sparse_transform(cur, rot)
+        applied += 1
+    state = NPADState(current=cur, applied=applied, accumulated_unitary=None, converged=converged)
+    piv = np.asarray(pivots, dtype=np.int32).reshape(-1, 2)
+    return state, piv
+
+
 def _npad_run_device(op, target, tol, max_iter, track_unitary, pivot_cap=0):
     if tol <= 0:
         raise ValueError("tol must be positive")
     if max_iter is None:
         max_iter = 20 * op.dim * op.dim
+    if op.layout == "sparse" and not track_unitary:
+        if target is not None and any(int(k) >= op.dim for k in target):
+            raise IndexOutOfRange("target indices exceed operator dimension")
+        return _npad_run_sparse(op, target, tol, max_iter, pivot_cap)
     t = _lib.require_cuda()
     d_target, n_target = _target_tensor(target, op.dim)
     threshold = tol * op.max_abs()

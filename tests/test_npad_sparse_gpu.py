@@ -95,3 +95,46 @@ def test_device_ladder_builder(E):
         dev = E.ladder_test_hamiltonian_device(n)
         _same(dev.data, E.ladder_test_hamiltonian(n).data)
         assert dev.max_abs() == E.ladder_test_hamiltonian(n).max_abs()
+
+
+def test_sparse_npad_run_golden(E, golden):
+    # the reference's npad_run on a sparse operator, 40 greedy rotations:
+    # same pivots, same sparse result
+    g = golden("npad_sparse")
+    n = g["rnd_indptr"].size - 1
+    op = E.HermitianOperator(_csr(g, "rnd", n))
+    st, piv = E.npad_run_logged(op, tol=1e-12, max_iter=40)
+    assert st.current.layout == "sparse" and st.applied == 40 and not st.converged
+    np.testing.assert_array_equal(piv, g["rnd_pivots"])
+    _same(st.current.data, _csr(g, "rnd_out", n))
+
+
+@pytest.mark.parametrize("target", [None, [0, 3, 7], []])
+def test_sparse_npad_run_vs_oracle_to_convergence(E, target):
+    # sparse JC lattice-like operator: greedy chain to convergence vs the oracle
+    p = E.JCSiteParams(omega=1.0, qubit_freq=0.8, g=0.1, mu=0.3, n_max=10)
+    op = E.jc_onsite_hamiltonian(p)
+    m = op.data.tocsr()
+    st, piv = E.npad_run_logged(op, target, tol=1e-12)
+    # oracle: reference selection on the CSR, reference sparse rotation
+    thr = 1e-12 * float(np.max(np.abs(m.data)))
+    ref_piv = []
+    while True:
+        low = sps.tril(m, k=-1, format="coo")
+        r, c, v = low.row, low.col, low.data
+        keep = v != 0
+        if target is not None:
+            ts = np.asarray(sorted(target), dtype=np.int64)
+            keep &= np.isin(r, ts) ^ np.isin(c, ts)
+        r, c, v = r[keep], c[keep], v[keep]
+        if r.size == 0:
+            break
+        mags = np.abs(v)
+        k = np.lexsort((r, c, -mags))[0]
+        if mags[k] < thr:
+            break
+        ref_piv.append((int(c[k]), int(r[k])))
+        m = npad_oracle.eliminate_sparse(m, int(c[k]), int(r[k]))
+    assert st.converged
+    np.testing.assert_array_equal(piv.reshape(-1, 2), np.asarray(ref_piv, dtype=np.int32).reshape(-1, 2))
+    _same(st.current.data, m)
