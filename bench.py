@@ -397,7 +397,7 @@ def sec_npad4096(torch, eff, lib, args, peaks, rotations=None):
             "us_per_rotation_kernel": kms * 1e3 / st.applied,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks[0], "unit": "GB/s", "frac": ach / peaks[0],
                          "bytes_per_rotation": 96 * n, "note": "single greedy chain: latency-bound (see DESIGN.md)",
-                         "traffic": (traffic_from_profiles("npad_rows_kernel@npad4096") or 0) / 2000 * st.applied
+                         "traffic": (traffic_from_profiles("npad_coop_kernel@npad4096") or 0) / 2000 * st.applied
                          or None,
                          "traffic_note": "ncu DRAM bytes of a 2000-rotation launch (tools/prof_round.sh), scaled per "
                                          "rotation to this launch"},

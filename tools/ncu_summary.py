@@ -117,8 +117,9 @@ def summarise(out: Path, reps: list[str]):
         by = collections.defaultdict(list)
         for d in launches:
             if "dram read" in d and "dram write" in d:
-                by[d["kernel"].split("(")[0].split("<")[0].replace("void ", "").strip()].append(
-                    d["dram read"][0] + d["dram write"][0])
+                kname = d["kernel"].split("(")[0].split("<")[0].replace("void ", "").strip()
+                kname = kname.replace("unnamed>::", "").replace("(anonymous namespace)::", "")
+                by[kname].append(d["dram read"][0] + d["dram write"][0])
         for k, v in by.items():
             traffic[f"{k}@{name}"] = {"bytes_per_launch": sum(v) / len(v), "launches": len(v), "report": name}
         hl = hot_lines(rep)

@@ -68,6 +68,13 @@ def main():
             tr = mg.evolve_device(ch, grid, m, psi0, check=False, order=2)
         torch.cuda.synchronize()
         print("traj", tr.shape)
+    elif case == "givens":
+        n = arg or 10**7
+        op = eff.ladder_test_hamiltonian_device(n)
+        st0 = eff.NPADState.from_operator(op)
+        for _ in range(2):
+            out = eff.eliminate_coupling(st0, 0, 1)
+        print("nnz", out.current.nnz)
     elif case == "magnus4096":
         ch = eff.heisenberg_chain_hamiltonians(12)
         full = eff.synthetic_transfer_pulse(25.0, 4096 * 8 + 1, seed=7)

@@ -9,8 +9,10 @@ $NCU --set full --import-source on -k regex:'magnus_fused' -s 1 -c 1 -o $O/magnu
     python tools/prof_driver.py magnus2 > $O/magnus2.out 2>&1
 $NCU --set full --import-source on -k regex:npad_trows -s 1 -c 1 -o $O/sweep -f \
     python tools/prof_driver.py sweep 1024 > $O/sweep.out 2>&1
-$NCU --set full --import-source on -k regex:npad_rows -s 1 -c 1 -o $O/npad4096 -f \
+$NCU --set full --import-source on -k regex:npad_coop -s 1 -c 1 -o $O/npad4096 -f \
     python tools/prof_driver.py npad4096 2000 > $O/npad4096.out 2>&1
+$NCU --set full --import-source on -k regex:'copy_kernel|indptr_kernel' -s 2 -c 2 -o $O/givens -f \
+    python tools/prof_driver.py givens 10000000 > $O/givens.out 2>&1
 $NCU --set full --import-source on -k regex:npad_rows -s 1 -c 1 -o $O/npad60 -f \
     python tools/prof_driver.py npad60 > $O/npad60.out 2>&1
 $NCU --set full --import-source on -k regex:zgemm -s 2 -c 2 -o $O/zgemm4096 -f \
