@@ -191,6 +191,19 @@ int qch_magnus_evolve_async_c128(const void* d_h0, const void* d_hk, const void*
                                  const void* d_psi0, void* d_traj, void* d_props, int check, void* d_flags,
                                  void* stream);
 
+/* Replayed evolve (new API, EvolvePlan): like qch_magnus_evolve_async_c128
+ * but with a caller-owned self-cleaning workspace d_work of
+ * qch_magnus_plan_workspace_bytes(N, M) bytes, prepared once by
+ * qch_magnus_plan_workspace_init; the kernel's last block restores it after
+ * every launch, so each launch is a single kernel (one CUDA-graph node).
+ * One workspace per concurrently running evolve. */
+int64_t qch_magnus_plan_workspace_bytes(int64_t N, int64_t M);
+int qch_magnus_plan_workspace_init(void* d_work, int64_t N, int64_t M, void* stream);
+int qch_magnus_evolve_plan_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                                const double* d_sig, int64_t S, double t_start, double t_end, int64_t M, int order,
+                                const void* d_psi0, void* d_traj, void* d_props, int check, void* d_work,
+                                void* d_flags, void* stream);
+
 /* evolve (magnus.py:214-267) with HOST buffers — the reference-facing call:
  * h_h0 (N,N), h_hk (K,N,N), h_sig (K,S) row-major, h_psi0 (N) are read from
  * host memory, the trajectory (M+1, N) is written to h_traj.  For N <= 4 the

@@ -33,7 +33,9 @@ int zgemm_taylor(const double2* a, const double2* b, double2* t, double2* o, int
 int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st);
 int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st);
 int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const double2* d_psi0, double2* d_traj,
-                        int64_t* bad_index, unsigned long long* d_flags_out, cudaStream_t st);
+                        int64_t* bad_index, unsigned long long* d_flags_out, cudaStream_t st, void* d_work);
+size_t fused_ws_bytes(int64_t N, int64_t M, int nlaunch);
+int fused_ws_init(void* ws, int64_t N, int64_t M, cudaStream_t st);
 size_t shard_ws_bytes(int64_t N, int64_t M);
 int shard_prepare(const SmallArgs& base, int64_t N, int64_t M, void* d_work, double2* d_block, cudaStream_t st);
 int shard_finish(int64_t N, int64_t M, void* d_work, const double2* d_psi_start, double2* d_traj,
@@ -598,7 +600,7 @@ static int small_report(unsigned long long* d_bad, int check, int64_t* bad_index
 static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_comm_in, int64_t K, int64_t N,
                               const double* d_sig, int64_t S, double t_start, double t_end, int64_t M, int order,
                               const void* d_psi0, void* d_traj, void* d_props, int check, int64_t* bad_index,
-                              unsigned long long* d_flags_out, void* stream) {
+                              unsigned long long* d_flags_out, void* stream, void* d_work = nullptr) {
   if (M < 1) return fail(QCH_ERR_GRID, "need at least one interval");
   if ((S - 1) % M)
     return fail(QCH_ERR_GRID, std::to_string(M) + " intervals do not divide " + std::to_string(S - 1) + " sample steps");
@@ -620,7 +622,8 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
     g.dt_int = dt_int;
     g.check = check;
     g.ubuf = (double2*)d_props;
-    return fused_evolve_device(g, N, M, (const double2*)d_psi0, (double2*)d_traj, bad_index, d_flags_out, st);
+    return fused_evolve_device(g, N, M, (const double2*)d_psi0, (double2*)d_traj, bad_index, d_flags_out, st,
+                               d_work);
   }
 
   DevBuf flags(st);
@@ -720,6 +723,25 @@ extern "C" int qch_magnus_evolve_async_c128(const void* d_h0, const void* d_hk, 
   if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "asynchronous evolve: N <= 4 (fused pipeline)");
   return magnus_evolve_impl(d_h0, d_hk, d_comm, K, N, d_sig, S, t_start, t_end, M, order, d_psi0, d_traj, d_props,
                             check, nullptr, (unsigned long long*)d_flags, stream);
+}
+
+// Plan (replayed) evolve: a self-cleaning workspace owned by the caller, so a
+// launch is ONE kernel (no allocation / memset / copy nodes in the graph).
+extern "C" int64_t qch_magnus_plan_workspace_bytes(int64_t N, int64_t M) {
+  return N > 4 || M < 1 ? -1 : (int64_t)fused_ws_bytes(N, M, 1);
+}
+extern "C" int qch_magnus_plan_workspace_init(void* d_work, int64_t N, int64_t M, void* stream) {
+  if (N > 4 || M < 1) return fail(QCH_ERR_UNSUPPORTED, "plan workspace: N <= 4, M >= 1");
+  return fused_ws_init(d_work, N, M, (cudaStream_t)stream);
+}
+extern "C" int qch_magnus_evolve_plan_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K,
+                                           int64_t N, const double* d_sig, int64_t S, double t_start, double t_end,
+                                           int64_t M, int order, const void* d_psi0, void* d_traj, void* d_props,
+                                           int check, void* d_work, void* d_flags, void* stream) {
+  if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "plan evolve: N <= 4 (fused pipeline)");
+  if (d_work == nullptr || d_flags == nullptr) return fail(QCH_ERR_VALUE, "plan evolve needs a workspace and flags");
+  return magnus_evolve_impl(d_h0, d_hk, d_comm, K, N, d_sig, S, t_start, t_end, M, order, d_psi0, d_traj, d_props,
+                            check, nullptr, (unsigned long long*)d_flags, stream, d_work);
 }
 
 // ---------------------------------------------------------------------------

@@ -12,22 +12,33 @@
 //    product of its kR propagators;
 //  * warp-shuffle inclusive scan of the thread products (3x3 complex, later
 //    intervals multiplied on the left), then the 4 warp aggregates;
-//  * decoupled look-back across tiles (tile order = dynamic grab order, so
-//    every predecessor tile is owned by a running block): a tile publishes
-//    its aggregate, inspects 128 predecessors at once, takes the nearest one
-//    that has published its inclusive prefix, multiplies the aggregates in
-//    between with shuffle trees, and publishes its own inclusive prefix
-//    (block-wide windows keep the walk short when a whole wave of tiles
-//    finishes together);
-//  * psi at each thread's start = (thread prefix)(warp prefix) E psi0; each
-//    thread then applies its kR propagators sequentially (the reference's
-//    psi <- U psi), writing the trajectory rows and checking the norm.
+//  * two-level scan across tiles: a tile publishes its aggregate and arrives
+//    at its group (32 consecutive tiles); the group's LAST arrival (warp 0 of
+//    its block) scans the group's aggregates, looks back over groups
+//    (decoupled look-back, window of 512 groups, nearest published inclusive
+//    prefix), and publishes every tile's exclusive prefix E — the other
+//    tiles of the group just wait for their flag.  Each tile thus costs one
+//    matrix product on the cross-tile critical path instead of a fold over
+//    its predecessors;
+//  * psi at each thread's start = P_{lane-1} X_warp E psi0; each thread
+//    applies its first kR-1 propagators sequentially (the reference's
+//    psi <- U psi) and forms its last row as P_lane X_warp E psi0, writing
+//    the trajectory rows and checking the norm.
 // The ordered product is re-associated (scan), which moves results by
 // O(M eps) ~ 1e-12 relative at M = 1e5: inside the 1e-10 parity bar.
 //
-// A block grabs its next tile before computing the current one (to prefetch
-// its signals).  Still deadlock-free: the smallest unfinished tile belongs to
-// a block that is computing it, and its look-back only waits on smaller tiles.
+// Every collective region runs on a provably converged warp (warp index via
+// a shuffle, lead condition via a barrier reduction, no divergent code before
+// the shuffles): otherwise ptxas guards each shuffle with BRA.DIV and a
+// diverged warp takes the serialised WARPSYNC.COLLECTIVE path (measured: 5
+// shuffle rounds 3k -> 45k cycles).
+//
+// A block grabs its next tile right after its prefix arrives (the next
+// signal window streams in while the trajectory is written).  Deadlock-free:
+// a block waits only for its own group; groups hold at most half the
+// resident blocks when tiles outnumber them, so some resident block always
+// belongs to a fully grabbed group, and group look-backs wait only on
+// earlier groups.
 //
 // The signals and the trajectory may live in mapped page-locked host memory:
 // each tile stages its signal window with one coalesced pass and writes its
@@ -71,16 +82,43 @@ struct FusedArgs {
   int64_t M;            // intervals of the whole evolve
   int64_t tile_begin, tile_end;  // tiles of this launch
   int* tile_ctr;        // this launch's grab counter (zeroed)
-  int* flag;            // per tile: 0 none, 1 aggregate, 2 inclusive prefix
-  double2* agg;         // per tile N*N
-  double2* inc;         // per tile N*N
+  // two-level scan across tiles: groups of 2^gshift consecutive tiles; the
+  // last tile of a group to finish scans the group and looks back over groups
+  int gshift;
+  int* flag;            // per tile: 1 = its exclusive prefix (inc) is ready
+  double2* agg;         // per tile N*N: tile aggregate
+  double2* inc;         // per tile N*N: tile exclusive prefix
+  int* gcount;          // per group: arrivals
+  int* gflag;           // per group: 0 none, 1 aggregate, 2 inclusive prefix
+  double2* gagg;        // per group N*N
+  double2* ginc;        // per group N*N
+  // self-cleaning workspace (plan / host-buffer calls): the last block to
+  // finish copies the status words to flags_out (nullable) and returns the
+  // workspace to its initial state, so a launch needs no memset before it
+  int* done_ctr;                  // null: the caller zeroes the workspace per launch
+  unsigned long long* flags_out;  // (2,) first non-unitary interval, first norm drift
+  unsigned long long* stats;  // non-null (QCH_MAGNUS_STATS): per-block phase cycles, see fused_print_stats
 };
+
+// phase counters (thread 0 of each block, summed over the block's tiles):
+// 0 tiles, 1 wait signals, 2 propagators (thread 0), 3 product + scan + block
+// sync, 4 publish + look-back, 5 trajectory + write-out, 6 globaltimer start,
+// 7 globaltimer end
+constexpr int kStatW = 20;  // + 8 poll cycles, 9 look-back passes, 10 publish cycles, 11 fold cycles
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// acquire/release fence at gpu scope (lighter than __threadfence()'s
+// sequentially consistent fence)
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -169,50 +207,151 @@ __device__ __forceinline__ Mat<N> warp_ordered_product(Mat<N> m, int span, int l
   return shfl_mat<N>(m, 0);
 }
 
-// Exclusive prefix of tile t, E = A_{t-1} ... A_0, by block-wide decoupled
-// look-back: the 128 threads inspect 128 predecessors at once, take the
-// nearest one that has published its inclusive prefix, and multiply the
-// aggregates in between (warp shuffle trees, then the 4 warp results).
+// Exclusive prefix of tile t, E = A_{t-1} ... A_0, by decoupled look-back,
+// run by warp 0 alone over a window of up to kLookW predecessors per pass
+// (the other warps wait at the next barrier without taking issue slots or
+// FP64 pipe cycles — every idle lane of a tree round still costs a full warp
+// instruction, so a block-wide look-back in every tile was as expensive as
+// forming the propagators):
+//  * poll the window's flags (relaxed loads, 16 per lane in flight,
+//    __nanosleep back-off) until every predecessor nearer than the nearest
+//    published inclusive prefix has published its aggregate; one fence;
+//  * lane i folds the L consecutive predecessors at distances [i L, i L + L)
+//    (L = ceil(run / 32)), then a 5-round shuffle tree.
+// Walks further back only when the window holds no inclusive prefix.
+constexpr int kLookK = 16;           // flags per lane
+constexpr int kLookW = 32 * kLookK;  // window (predecessors per pass)
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <int N>
-__device__ Mat<N> block_lookback(const FusedArgs& g, int64_t t, Mat<N>* s_red, int* s_j) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ Mat<N> warp_lookback(const int* flag, const double2* agg, const double2* inc, int64_t t,
+                                unsigned long long* sacc) {
+  const int lane = threadIdx.x & 31;
   Mat<N> e = mat_eye<N>();
-  int64_t base = t - 1;
+  int64_t hi = t - 1;  // nearest predecessor not yet folded into e
   while (true) {
-    const int64_t p = base - tid;
-    int f = 3;  // before tile 0: identity prefix
-    if (p >= 0) {
-      do {
-        f = ld_acquire(g.flag + p);
-      } while (f == 0);
+    __syncwarp();
+    const long long cpoll = sacc != nullptr ? clock64() : 0;
+    // distance d = lane + 32 k; predecessor hi - d (< 0: identity prefix)
+    unsigned have = 0, incm = 0;  // bit k: aggregate / inclusive published
+    int ns = 32, j;
+    while (true) {
+#pragma unroll
+      for (int k = 0; k < kLookK; ++k) {
+        if (have & (1u << k)) continue;
+        const int64_t p = hi - (lane + 32 * k);
+        const int f = p >= 0 ? ld_relaxed(flag + p) : 3;
+        if (f != 0) have |= 1u << k;
+        if (f >= 2) incm |= 1u << k;
+      }
+      j = incm ? lane + 32 * (__ffs(incm) - 1) : kLookW;  // nearest inclusive of this lane
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) j = min(j, __shfl_xor_sync(0xffffffffu, j, o));
+      const int kneed = (j - lane + 31) / 32;  // k with lane + 32 k < j
+      const unsigned need = kneed >= 32 ? 0xffffffffu : ((1u << kneed) - 1u);
+      if (__all_sync(0xffffffffu, (have & need) == need)) break;
+      __nanosleep(ns);
+      ns = min(ns * 2, 256);
     }
-    if (tid == 0) *s_j = kFusedThreads;
-    __syncthreads();
-    if (f >= 2) atomicMin(s_j, tid);
-    __syncthreads();
-    const int j = *s_j;
+    fence_acq_rel();  // acquire side of the flags' release stores
+    if (sacc != nullptr && lane == 0) {
+      sacc[7] += clock64() - cpoll;
+      sacc[8] += 1;
+    }
+    __syncwarp();
+    const int run = min(j + 1, kLookW);  // predecessors folded in this pass
+    const int L = (run + 31) / 32;
     Mat<N> m = mat_eye<N>();
-    if (tid < j) {
-      ldcg_mat<N>(m, g.agg + p * N * N);
-    } else if (tid == j && f == 2) {
-      ldcg_mat<N>(m, g.inc + p * N * N);
+    const int d0 = lane * L;
+    const int qn = min(L, run - d0);
+#pragma unroll 1
+    for (int q = 0; q < qn; ++q) {
+      const int d = d0 + q;
+      const int64_t p = hi - d;
+      if (p < 0) break;  // identity prefix
+      Mat<N> x;
+      ldcg_mat<N>(x, (d < j ? agg : inc) + p * N * N);
+      m = q == 0 ? x : mat_mul_fma<N>(m, x);
     }
-    const int last = j < kFusedThreads ? j : kFusedThreads - 1;  // threads 0..last matter
-    if (warp * 32 <= last) {
-      const int span = std::min(32, last - warp * 32 + 1);
-      m = warp_ordered_product<N>(m, span, lane);
-      if (lane == 0) s_red[warp] = m;
-    }
-    __syncthreads();
-    const int nw = last / 32 + 1;
-    Mat<N> r = s_red[0];
-    for (int w = 1; w < nw; ++w) r = mat_mul_fma<N>(r, s_red[w]);
-    e = mat_mul_fma<N>(e, r);
-    __syncthreads();  // s_red / s_j reuse
-    if (j < kFusedThreads) break;
-    base -= kFusedThreads;
+    __syncwarp();
+    e = mat_mul_fma<N>(e, warp_ordered_product<N>(m, (run - 1) / L + 1, lane));
+    if (sacc != nullptr && lane == 0) sacc[10] += clock64() - cpoll;
+    if (j < kLookW) break;
+    hi -= kLookW;
   }
   return e;
+}
+
+// The last tile of a group to finish (warp 0 of its block) leads the group:
+// scan of the group's tile aggregates (lane i = tile gfirst + i), look-back
+// over groups, then every tile's exclusive prefix E = P_{i-1} GE and its flag.
+// P_{i-1} and the group aggregate wait in shared scratch (the tile's
+// trajectory staging area, free at this point) during the look-back, so the
+// look-back's matrices do not push the kernel into local-memory spills.
+template <int N>
+__device__ __forceinline__ void group_lead(const FusedArgs& g, int64_t gi, int64_t gfirst, int gsize,
+                                           double2* scratch, unsigned long long* sacc) {
+  const int lane = threadIdx.x & 31;
+  // reconverge the warp first: after the divergent publish and the barrier
+  // its lanes can still run as separate groups, and every shuffle below would
+  // take the compiler's serialised WARPSYNC.COLLECTIVE path (~250 cycles each)
+  __syncwarp();
+  fence_acq_rel();  // acquire: the group's aggregates
+  const long long cl0 = clock64();
+  {
+    Mat<N> pg = mat_eye<N>();
+    if (lane < gsize) ldcg_mat<N>(pg, g.agg + (gfirst + lane) * N * N);
+    __syncwarp();
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const Mat<N> q = shfl_up_mat<N>(pg, d);
+      if (lane >= d) pg = mat_mul_fma<N>(pg, q);
+    }
+    Mat<N> px = shfl_up_mat<N>(pg, 1);
+    if (lane == 0) px = mat_eye<N>();
+    st_mat<N>(scratch + lane * N * N, px);
+    if (lane == gsize - 1) {
+      st_mat<N>(scratch + 32 * N * N, pg);  // the group aggregate
+      if (gi == 0) {
+        stcg_mat<N>(g.ginc, pg);
+        st_release(g.gflag, 2);
+      } else {
+        stcg_mat<N>(g.gagg + gi * N * N, pg);
+        st_release(g.gflag + gi, 1);
+      }
+    }
+  }
+  const long long cl1 = clock64();
+  Mat<N> ge = mat_eye<N>();
+  if (gi > 0) {
+    ge = warp_lookback<N>(g.gflag, g.gagg, g.ginc, gi, sacc);
+    __syncwarp();
+    if (lane == 0) {
+      Mat<N> ga;
+      ld_mat<N>(ga, scratch + 32 * N * N);
+      stcg_mat<N>(g.ginc + gi * N * N, mat_mul_fma<N>(ga, ge));
+      st_release(g.gflag + gi, 2);
+    }
+  }
+  __syncwarp();
+  const long long cl2 = clock64();
+  if (lane < gsize) {
+    Mat<N> px;
+    ld_mat<N>(px, scratch + lane * N * N);
+    stcg_mat<N>(g.inc + (gfirst + lane) * N * N, mat_mul_fma<N>(px, ge));
+    st_release(g.flag + gfirst + lane, 1);
+  }
+  if (sacc != nullptr && lane == 0) {
+    sacc[11] += cl1 - cl0;
+    sacc[12] += cl2 - cl1;
+    sacc[13] += clock64() - cl2;
+    sacc[14] += 1;
+  }
 }
 
 template <int N>
@@ -223,7 +362,10 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
   double2* s_ops = fsm;
   const bool inl = g.s.h0 == nullptr;
   load_ops<N>(g.s, s_ops, inl ? g.opsv : nullptr, inl ? g.opsv + N * N : nullptr);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp index through a shuffle (as CUTLASS's canonical_warp_idx_sync): the
+  // compiler then knows it is warp-uniform, so shuffles under `warp == 0`
+  // compile to plain SHFL instead of the serialised WARPSYNC.COLLECTIVE path
+  const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   double2* s_u = fsm + ops_smem_bytes<N>(K, 2) / sizeof(double2) + (size_t)tid * kR * N * N;
   const size_t wstride = (((size_t)K * g.win + 1) & ~(size_t)1);  // doubles per window buffer (16 B multiple)
   double* s_sig0 = (double*)(fsm + ops_smem_bytes<N>(K, 2) / sizeof(double2) + (size_t)kFusedThreads * kR * N * N);
@@ -234,9 +376,9 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
   double2* s_traj_own = (double2*)(s_sig0 + (g.win > 0 ? 2 * wstride : 0));
   const double2* psi0p = g.psi0 ? g.psi0 : g.psi0v;
   __shared__ Mat<N> s_w[kFusedWarps];    // warp aggregates -> in-block exclusive warp prefixes
-  __shared__ Mat<N> s_red[kFusedWarps];  // look-back partials
+  __shared__ Mat<N> s_red[1];            // the tile aggregate
   __shared__ Mat<N> s_e;                 // exclusive prefix of the tile
-  __shared__ int s_tile, s_j;
+  __shared__ int s_tile;
 
   // the control samples of a tile: one coalesced pass into shared memory,
   // issued asynchronously (cp.async) one tile ahead, so that the fetch of the
@@ -257,6 +399,19 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
       while (ld_acquire(g.chunk_flag) < need) __nanosleep(200);
     }
   };
+  __shared__ unsigned long long st_acc[19];  // 6: previous clock, 7 poll, 8 passes, 9 publish
+  auto mark = [&](int ph) {
+    if (g.stats != nullptr && tid == 0) {
+      const unsigned long long c = clock64();
+      st_acc[ph] += c - st_acc[6];
+      st_acc[6] = c;
+    }
+  };
+  if (g.stats != nullptr && tid == 0) {
+    g.stats[blockIdx.x * kStatW + 6] = gtimer();
+    for (int q = 0; q < 19; ++q) st_acc[q] = 0;
+    st_acc[6] = clock64();
+  }
   if (tid == 0) {
     s_tile = atomicAdd(g.tile_ctr, 1);
     wait_chunk(g.tile_begin + s_tile);
@@ -266,24 +421,12 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
   if (g.win > 0 && t < g.tile_end) prefetch(t, s_sig0);
   for (int it = 0;; ++it) {
     if (t >= g.tile_end) break;
-    __syncthreads();  // everyone has read s_tile
-    if (tid == 0) {
-      s_tile = atomicAdd(g.tile_ctr, 1);  // grab the next tile now (order-safe, see header)
-      wait_chunk(g.tile_begin + s_tile);
-    }
-    __syncthreads();
-    const int64_t tn = g.tile_begin + s_tile;
     double* s_sig = s_sig0 + (it & 1) * wstride;
     double2* s_traj = traj_in_window ? (double2*)s_sig : s_traj_own;
-    if (g.win > 0) {
-      if (tn < g.tile_end) {
-        prefetch(tn, s_sig0 + ((it + 1) & 1) * wstride);
-        cp_wait<1>();
-      } else {
-        cp_wait<0>();
-      }
-    }
+    if (g.win > 0) cp_wait<0>();
     __syncthreads();
+    mark(1);
+    if (g.stats != nullptr && tid == 0) st_acc[0] += 1;
     const int64_t n0 = t * kTile + (int64_t)tid * kR;
     SmallArgs gl = g.s;
     int64_t nbase = 0;
@@ -300,12 +443,16 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
       const int64_t n = n0 + r;
       Mat<N> u = mat_eye<N>();
       if (n < g.M) {
-        u = expm_minus_i_fast<N>(interval_hbar<N>(gl, s_ops, n - nbase));
+        if (g.win > 0 && g.s.ca.sub == 4)
+          u = expm_minus_i_fast<N>(interval_hbar_fixed<N, 4>(g.s, s_ops, s_sig, g.win, n - nbase));
+        else
+          u = expm_minus_i_fast<N>(interval_hbar<N>(gl, s_ops, n - nbase));
         if (g.s.check && !validate_reg<N>(u)) atomicMin(g.s.bad, (unsigned long long)n);
         if (g.s.ubuf != nullptr) st_mat<N>(g.s.ubuf + n * N * N, u);
       }
       st_mat<N>(s_u + r * N * N, u);
     }
+    mark(2);
     Mat<N> p;
     ld_mat<N>(p, s_u);
 #pragma unroll 1
@@ -314,73 +461,106 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
       ld_mat<N>(u, s_u + r * N * N);
       p = mat_mul_fma<N>(u, p);
     }
-    // ---- warp inclusive scan: P_l = A_l ... A_0
+    // ---- warp inclusive scan: P_l = A_l ... A_0 (lanes reconverged after the
+    // per-lane Taylor degrees, so the shuffles take the converged fast path)
+    __syncwarp();
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const Mat<N> q = shfl_up_mat<N>(p, d);
       if (lane >= d) p = mat_mul_fma<N>(p, q);
     }
     if (lane == 31) s_w[warp] = p;
+    // P_lane replaces U_{kR-1} in shared memory: the last trajectory row of
+    // the thread is P_lane (X_warp E psi0), the earlier ones come from the
+    // neighbour's P_{lane-1} and U_0 .. U_{kR-2}; nothing stays in registers
+    // across the look-back
+    st_mat<N>(s_u + (kR - 1) * N * N, p);
     __syncthreads();
-    // ---- tile aggregate, in-block warp prefixes; publish; look-back
-    if (tid == 0) {
-      Mat<N> x = mat_eye<N>();
-      for (int w = 0; w < kFusedWarps; ++w) {
+    mark(3);
+    // ---- tile aggregate and in-block warp prefixes; arrive at the group
+    const int64_t gi = (t - g.tile_begin) >> g.gshift;
+    const int64_t gfirst = g.tile_begin + (gi << g.gshift);
+    const int gsize = (int)std::min<int64_t>(int64_t(1) << g.gshift, g.tile_end - gfirst);
+    // warp 0 forms the tile aggregate (all lanes, same values: no divergent
+    // region before the group lead's shuffles), lane 0 publishes it
+    bool last = false;
+    if (warp == 0) {
+      Mat<N> x = s_w[0];
+      __syncwarp();
+      if (lane == 0) s_w[0] = mat_eye<N>();
+#pragma unroll 1
+      for (int w = 1; w < kFusedWarps; ++w) {
         const Mat<N> a = s_w[w];
-        s_w[w] = x;  // exclusive prefix of warp w within the tile
-        x = (w == 0) ? a : mat_mul_fma<N>(a, x);
+        __syncwarp();
+        if (lane == 0) s_w[w] = x;  // exclusive prefix of warp w within the tile
+        x = mat_mul_fma<N>(a, x);
       }
-      if (t == 0) {
-        stcg_mat<N>(g.inc, x);
-        __threadfence();
-        st_release(g.flag, 2);
-      } else {
+      if (lane == 0) {
+        s_red[0] = x;  // the tile aggregate
         stcg_mat<N>(g.agg + t * N * N, x);
-        __threadfence();
-        st_release(g.flag + t, 1);
+        fence_acq_rel();  // release: the aggregate before the arrival
+        last = atomicAdd(g.gcount + gi, 1) == gsize - 1;  // last arrival of the group leads it
       }
-      s_red[0] = x;  // the tile aggregate, for the inclusive prefix below
+      __syncwarp();
     }
-    __syncthreads();
-    Mat<N> agg = s_red[0];
-    __syncthreads();
-    if (t > 0) {
-      const Mat<N> e = block_lookback<N>(g, t, s_red, &s_j);
-      if (tid == 0) {
-        stcg_mat<N>(g.inc + t * N * N, mat_mul_fma<N>(agg, e));
-        __threadfence();
-        st_release(g.flag + t, 2);
+    // block-uniform in the compiler's eyes (barrier reduction)
+    const bool lead = __syncthreads_or(last);
+    if (g.stats != nullptr && tid == 0) st_acc[9] += clock64() - st_acc[6];
+    if (warp == 0) {
+      if (lead) group_lead<N>(g, gi, gfirst, gsize, s_traj, g.stats != nullptr ? st_acc : nullptr);
+      const long long cw0 = clock64();
+      if (lane == 0) {
+        int ns = 32;
+        while (ld_relaxed(g.flag + t) == 0) {
+          __nanosleep(ns);
+          ns = min(ns * 2, 256);
+        }
+        fence_acq_rel();  // acquire: the prefix seen flagged
+        Mat<N> e;
+        ldcg_mat<N>(e, g.inc + t * N * N);
         s_e = e;
+        if (g.stats != nullptr) st_acc[15] += clock64() - cw0;
+        // grab the next tile only now: a block never holds an unstarted tile
+        // while it waits for its prefix
+        s_tile = atomicAdd(g.tile_ctr, 1);
+        wait_chunk(g.tile_begin + s_tile);
       }
-    } else if (tid == 0) {
-      s_e = mat_eye<N>();
     }
     __syncthreads();
+    const int64_t tn = g.tile_begin + s_tile;
+    // the next tile's signal window streams in while this tile's trajectory
+    // is formed and written
+    if (g.win > 0 && tn < g.tile_end) prefetch(tn, s_sig0 + ((it + 1) & 1) * wstride);
+    mark(4);
     if (g.pex != nullptr) {
       // prefix mode: the thread's start = (P_{lane-1} X_warp) E_t psi_start,
       // with psi_start known only after the ranks' exchange
-      Mat<N> pexm = shfl_up_mat<N>(p, 1);
-      if (lane == 0) pexm = mat_eye<N>();
+      Mat<N> pexm = mat_eye<N>();
+      if (lane > 0) ld_mat<N>(pexm, s_u - kR * N * N + (kR - 1) * N * N);
       st_mat<N>(g.pex + (t * kFusedThreads + tid) * N * N, mat_mul_fma<N>(pexm, s_w[warp]));
       if (tid == 0) {
         st_mat<N>(g.etile + t * N * N, s_e);
-        if (t == g.tile_end - 1) st_mat<N>(g.block_out, mat_mul_fma<N>(agg, s_e));
+        if (t == g.tile_end - 1) st_mat<N>(g.block_out, mat_mul_fma<N>(s_red[0], s_e));
       }
       __syncthreads();  // s_w / s_e reuse
       t = tn;
       continue;
     }
-    // ---- trajectory: psi at this thread's start = P_{lane-1} X_warp E psi0
-    cplx psi0[N], v[N], w[N];
+    // ---- trajectory: w = X_warp E psi0; the thread's start state is
+    // P_{lane-1} w, its last row P_lane w
+    cplx psi0[N], v[N], w[N], x[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) psi0[q] = d2c(psi0p[q]);
     mat_vec<N>(s_e, psi0, v);
     mat_vec<N>(s_w[warp], v, w);
-    Mat<N> pex = shfl_up_mat<N>(p, 1);
-    if (lane == 0) pex = mat_eye<N>();
-    mat_vec<N>(pex, w, v);
+    if (lane > 0) {
+      Mat<N> pex;
+      ld_mat<N>(pex, s_u - kR * N * N + (kR - 1) * N * N);
+      mat_vec<N>(pex, w, x);
+    } else {
 #pragma unroll
-    for (int q = 0; q < N; ++q) w[q] = v[q];
+      for (int q = 0; q < N; ++q) x[q] = w[q];
+    }
     if (t == 0 && tid == 0) {
 #pragma unroll
       for (int q = 0; q < N; ++q) g.traj[q] = c2d(psi0[q]);
@@ -391,11 +571,11 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
       if (n >= g.M) break;
       Mat<N> u;
       ld_mat<N>(u, s_u + r * N * N);
-      mat_vec<N>(u, w, v);
+      mat_vec<N>(u, r + 1 < kR ? x : w, v);
       double nrm2 = 0.0;
 #pragma unroll
       for (int q = 0; q < N; ++q) {
-        w[q] = v[q];
+        x[q] = v[q];
         nrm2 = fma(v[q].re, v[q].re, fma(v[q].im, v[q].im, nrm2));
         s_traj[(tid * kR + r) * N + q] = c2d(v[q]);
       }
@@ -411,7 +591,46 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
       for (int64_t q = tid; q < rows * N; q += kFusedThreads) dst[q] = s_traj[q];
     }
     __syncthreads();  // s_w / s_e / s_traj reuse
+    mark(5);
     t = tn;
+  }
+  if (g.done_ctr != nullptr) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (tid == 0) {
+      fence_acq_rel();
+      s_last = atomicAdd(g.done_ctr, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      fence_acq_rel();
+      const int64_t nt = g.tile_end - g.tile_begin;
+      for (int64_t q = tid; q < nt; q += kFusedThreads) {
+        g.flag[g.tile_begin + q] = 0;
+        g.gflag[q] = 0;
+        g.gcount[q] = 0;
+      }
+      if (tid == 0) {
+        if (g.flags_out != nullptr) {
+          g.flags_out[0] = g.s.bad[0];
+          g.flags_out[1] = g.s.bad[1];
+        }
+        g.s.bad[0] = ~0ull;
+        g.s.bad[1] = ~0ull;
+        *g.tile_ctr = 0;
+        *g.done_ctr = 0;
+      }
+    }
+  }
+  if (g.stats != nullptr && tid == 0) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) g.stats[blockIdx.x * kStatW + q] = st_acc[q];
+    g.stats[blockIdx.x * kStatW + 7] = gtimer();
+    g.stats[blockIdx.x * kStatW + 8] = st_acc[7];
+    g.stats[blockIdx.x * kStatW + 9] = st_acc[8];
+    g.stats[blockIdx.x * kStatW + 10] = st_acc[9];
+    g.stats[blockIdx.x * kStatW + 11] = st_acc[10];
+    for (int q = 11; q < 19; ++q) g.stats[blockIdx.x * kStatW + q + 1] = st_acc[q];
   }
 }
 
@@ -457,10 +676,62 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
   int64_t slots = (int64_t)blocks_per_sm * sm_count();
   if (g.stream_blocks_per_sm > 0) slots = std::min<int64_t>(slots, (int64_t)g.stream_blocks_per_sm * sm_count());
   const int grid = (int)std::min<int64_t>(tiles, slots);
+  // group size: 32 tiles, or at most half the resident blocks when the tiles
+  // outnumber them (a block waits for its group, so the unfinished top group
+  // must never hold every resident block)
+  g.gshift = 5;
+  if (tiles > grid)
+    while (g.gshift > 0 && (1 << g.gshift) > grid / 2) --g.gshift;
+  static const bool want_stats = getenv("QCH_MAGNUS_STATS") != nullptr;
+  static unsigned long long* d_stats = nullptr;
+  g.stats = nullptr;
+  if (want_stats) {
+    if (d_stats == nullptr) QCH_CUDA(cudaMalloc(&d_stats, sizeof(unsigned long long) * kStatW * 4096));
+    if (grid <= 4096) g.stats = d_stats;
+  }
   void* pr = prof_begin("magnus_fused_kernel", st);
   magnus_fused_kernel<N><<<grid, kFusedThreads, smem, st>>>(g);
   prof_end(pr, st);
   QCH_LAUNCH_CHECK("magnus_fused_kernel");
+  if (g.stats != nullptr) {
+    std::vector<unsigned long long> h((size_t)kStatW * grid);
+    QCH_CUDA(cudaMemcpyAsync(h.data(), d_stats, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    QCH_CUDA(cudaStreamSynchronize(st));
+    double sum[6] = {0, 0, 0, 0, 0, 0}, mx[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long t0 = ~0ull, t1 = 0, s_last = 0, e_first = ~0ull;
+    for (int b = 0; b < grid; ++b) {
+      for (int q = 0; q < 6; ++q) {
+        sum[q] += (double)h[b * kStatW + q];
+        mx[q] = std::max(mx[q], (double)h[b * kStatW + q]);
+      }
+      t0 = std::min(t0, h[b * kStatW + 6]);
+      s_last = std::max(s_last, h[b * kStatW + 6]);
+      e_first = std::min(e_first, h[b * kStatW + 7]);
+      t1 = std::max(t1, h[b * kStatW + 7]);
+    }
+    double ext[4] = {0, 0, 0, 0};
+    for (int b = 0; b < grid; ++b)
+      for (int q = 0; q < 4; ++q) ext[q] += (double)h[b * kStatW + 8 + q];
+    const double tiles = sum[0] > 0 ? sum[0] : 1;
+    fprintf(stderr,
+            "[qch magnus stats] look-back per tile: publish %.0f cycles, poll %.0f cycles, poll+fold %.0f cycles, "
+            "passes %.2f\n",
+            ext[2] / tiles, ext[0] / tiles, ext[3] / tiles, ext[1] / tiles);
+    double ld[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < grid; ++b)
+      for (int q = 0; q < 8; ++q) ld[q] += (double)h[b * kStatW + 12 + q];
+    const double nl = ld[3] > 0 ? ld[3] : 1;
+    fprintf(stderr,
+            "[qch magnus stats] group leaders %.0f: scan %.0f, look-back %.0f, prefixes %.0f cycles; tile wait for "
+            "prefix %.0f cycles\n",
+            ld[3], ld[0] / nl, ld[1] / nl, ld[2] / nl, ld[4] / tiles);
+    fprintf(stderr,
+            "[qch magnus stats] grid %d smem %zu tiles %.0f | cycles/tile: wait %.0f (max %.0f) prop %.0f (max %.0f) "
+            "scan %.0f (max %.0f) lookback %.0f (max %.0f) traj %.0f (max %.0f) | block start spread %.2f us, "
+            "first end %.2f us, last end %.2f us\n",
+            grid, smem, sum[0], sum[1] / tiles, mx[1], sum[2] / tiles, mx[2], sum[3] / tiles, mx[3], sum[4] / tiles,
+            mx[4], sum[5] / tiles, mx[5], (s_last - t0) * 1e-3, (e_first - t0) * 1e-3, (t1 - t0) * 1e-3);
+  }
   note_launch(1);
   return QCH_OK;
 }
@@ -477,15 +748,16 @@ int fused_launch_any(int n, FusedArgs& g, cudaStream_t st) {
 int64_t fused_tiles(int64_t M) { return (M + kTile - 1) / kTile; }
 int64_t fused_tile_intervals() { return kTile; }
 
-// workspace: flags (ntiles int) | counters (nlaunch int) | bad (2 ull) | agg | inc
+// workspace: [tile flags | counters | group flags | group arrivals | done]
+// (zeroed) | bad (2 ull, all ones) | agg | inc | gagg | ginc
 size_t fused_ws_bytes(int64_t N, int64_t M, int nlaunch) {
   const int64_t nt = fused_tiles(M);
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  return al(sizeof(int) * (nt + nlaunch)) + al(16) + 2 * al(sizeof(double2) * N * N * nt);
+  return al(sizeof(int) * (3 * nt + nlaunch + 1)) + al(16) + 4 * al(sizeof(double2) * N * N * nt);
 }
 size_t fused_ws_zero_bytes(int64_t M, int nlaunch) {
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  return al(sizeof(int) * (fused_tiles(M) + nlaunch)) + al(16);
+  return al(sizeof(int) * (3 * fused_tiles(M) + nlaunch + 1));
 }
 void fused_carve(void* ws, int64_t N, int64_t M, int nlaunch, FusedArgs* g, int** ctr) {
   const int64_t nt = fused_tiles(M);
@@ -493,14 +765,19 @@ void fused_carve(void* ws, int64_t N, int64_t M, int nlaunch, FusedArgs* g, int*
   unsigned char* p = (unsigned char*)ws;
   g->flag = (int*)p;
   *ctr = g->flag + nt;
-  p += al(sizeof(int) * (nt + nlaunch));
+  g->gflag = *ctr + nlaunch;
+  g->gcount = g->gflag + nt;
+  g->done_ctr = nullptr;  // set by the self-cleaning callers
+  g->flags_out = nullptr;
+  p += al(sizeof(int) * (3 * nt + nlaunch + 1));
   g->s.bad = (unsigned long long*)p;
   p += al(16);
+  const size_t mb = al(sizeof(double2) * N * N * nt);
   g->agg = (double2*)p;
-  p += al(sizeof(double2) * N * N * nt);
-  g->inc = (double2*)p;
+  g->inc = (double2*)(p + mb);
+  g->gagg = (double2*)(p + 2 * mb);
+  g->ginc = (double2*)(p + 3 * mb);
 }
-
 
 namespace {
 struct Trace {
@@ -531,6 +808,10 @@ struct Pipe {
   cudaStream_t in = nullptr;  // copy stream of the host-buffer call
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int* d_flag = nullptr;      // chunk counter (cudaMalloc: stream memory ops reject pool memory)
+  void* ws = nullptr;         // self-cleaning fused workspace of the host-buffer call
+  size_t ws_bytes = 0;
+  int64_t ws_n = 0, ws_m = 0;
+  bool ws_dirty = true;
 };
 Pipe& pipe_for_device() {
   static Pipe pipes[64];
@@ -538,7 +819,7 @@ Pipe& pipe_for_device() {
   cudaGetDevice(&dev);
   Pipe& p = pipes[dev & 63];
   if (p.h_flags == nullptr) {
-    cudaMallocHost(&p.h_flags, 2 * sizeof(unsigned long long));
+    cudaHostAlloc(&p.h_flags, 2 * sizeof(unsigned long long), cudaHostAllocMapped);
     cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&p.ev0, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&p.ev1, cudaEventDisableTiming);
@@ -579,12 +860,26 @@ void* mapped_ptr(const void* h) {
 }
 }  // namespace
 
+// Initial state of a self-cleaning workspace (zero counters, all-ones status
+// words); the kernel's last block restores it after every launch.
+int fused_ws_init(void* ws, int64_t N, int64_t M, cudaStream_t st) {
+  FusedArgs g;
+  int* ctr = nullptr;
+  fused_carve(ws, N, M, 1, &g, &ctr);
+  QCH_CUDA(cudaMemsetAsync(ws, 0, fused_ws_zero_bytes(M, 1), st));
+  QCH_CUDA(cudaMemsetAsync(g.s.bad, 0xff, 2 * sizeof(unsigned long long), st));
+  return QCH_OK;
+}
+static int* fused_done_ptr(const FusedArgs& g, int64_t M) { return g.gcount + fused_tiles(M); }
+
 // Device-buffer fused evolve (N <= 4).  d_flags_out non-null: copy the two
 // status words there and return without synchronising (async evolve).
+// d_work non-null: a self-cleaning workspace (fused_ws_init) — the launch is
+// then the only operation (no allocation, memset or copy around it).
 int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const double2* d_psi0, double2* d_traj,
-                        int64_t* bad_index, unsigned long long* d_flags_out, cudaStream_t st) {
+                        int64_t* bad_index, unsigned long long* d_flags_out, cudaStream_t st, void* d_work) {
   FBuf ws(st);
-  QCH_CUDA(ws.alloc(fused_ws_bytes(N, M, 1)));
+  if (d_work == nullptr) QCH_CUDA(ws.alloc(fused_ws_bytes(N, M, 1)));
   FusedArgs g;
   g.s = base;
   g.stream_blocks_per_sm = 0;
@@ -594,9 +889,14 @@ int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const doubl
   g.etile = nullptr;
   g.block_out = nullptr;
   int* ctr = nullptr;
-  fused_carve(ws.p, N, M, 1, &g, &ctr);
-  QCH_CUDA(cudaMemsetAsync(ws.p, 0, fused_ws_zero_bytes(M, 1), st));
-  QCH_CUDA(cudaMemsetAsync(g.s.bad, 0xff, 2 * sizeof(unsigned long long), st));
+  fused_carve(d_work ? d_work : ws.p, N, M, 1, &g, &ctr);
+  if (d_work != nullptr) {
+    g.done_ctr = fused_done_ptr(g, M);
+    g.flags_out = d_flags_out;
+  } else {
+    QCH_CUDA(cudaMemsetAsync(ws.p, 0, fused_ws_zero_bytes(M, 1), st));
+    QCH_CUDA(cudaMemsetAsync(g.s.bad, 0xff, 2 * sizeof(unsigned long long), st));
+  }
   g.psi0 = d_psi0;
   g.traj = d_traj;
   g.M = M;
@@ -604,6 +904,10 @@ int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const doubl
   g.tile_end = fused_tiles(M);
   g.tile_ctr = ctr;
   if (int rc = fused_launch_any((int)N, g, st)) return rc;
+  if (d_work != nullptr) {
+    if (d_flags_out) return QCH_OK;
+    return fail(QCH_ERR_VALUE, "a self-cleaning workspace needs a flags buffer");
+  }
   if (d_flags_out) {
     QCH_CUDA(cudaMemcpyAsync(d_flags_out, g.s.bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
     return QCH_OK;
@@ -810,19 +1114,34 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   const bool sig_map = pinned_sig && !sig_stream && !(smode != nullptr && strcmp(smode, "copy") == 0);
   const double* sig = sig_map ? (const double*)mapped_ptr(h_sig) : nullptr;
   double2* traj = getenv("QCH_NOMAP_TRAJ") ? nullptr : (double2*)mapped_ptr(h_traj);
-  const size_t b_ws = al(fused_ws_bytes(N, M, 1));
-  const size_t b_flag = 256;
   const size_t b_sig = sig ? 0 : al(sizeof(double) * Kd * S);
   const size_t b_traj = traj ? 0 : al(sizeof(double2) * N * (M + 1));
   FBuf dev(st);
-  QCH_CUDA(dev.alloc(b_ws + b_flag + b_sig + b_traj));
-  double* d_sig = (double*)((unsigned char*)dev.p + b_ws + b_flag);
-  double2* d_traj = (double2*)((unsigned char*)dev.p + b_ws + b_flag + b_sig);
+  if (b_sig + b_traj > 0) QCH_CUDA(dev.alloc(b_sig + b_traj));
+  double* d_sig = (double*)dev.p;
+  double2* d_traj = (double2*)((unsigned char*)dev.p + b_sig);
   if (sig == nullptr) {
     if (K > 0 && !sig_stream) QCH_CUDA(cudaMemcpyAsync(d_sig, h_sig, sizeof(double) * K * S, cudaMemcpyHostToDevice, st));
     sig = d_sig;
   }
   if (traj == nullptr) traj = d_traj;
+  Pipe& pp = pipe_for_device();
+  // the device's self-cleaning workspace (grown on demand; the call is not
+  // re-entrant on one device, see qcheff.h)
+  const size_t b_ws = fused_ws_bytes(N, M, 1);
+  if (pp.ws_bytes < b_ws || pp.ws_dirty || pp.ws_n != N || pp.ws_m != M) {  // the layout depends on (N, M)
+    if (pp.ws != nullptr && pp.ws_bytes < b_ws) {
+      QCH_CUDA(cudaFree(pp.ws));
+      pp.ws = nullptr;
+    }
+    if (pp.ws == nullptr) {
+      QCH_CUDA(cudaMalloc(&pp.ws, b_ws));
+      pp.ws_bytes = b_ws;
+    }
+    pp.ws_dirty = true;  // until the initialisation below is known to have run
+    pp.ws_n = N;
+    pp.ws_m = M;
+  }
   tr.mark("buffers");
   const int64_t sub = (S - 1) / M;
   FusedArgs g;
@@ -835,9 +1154,11 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   if (const char* e = getenv("QCH_STREAM_BPS")) g.stream_blocks_per_sm = atoi(e);
 
   int* ctr = nullptr;
-  fused_carve(dev.p, N, M, 1, &g, &ctr);
-  QCH_CUDA(cudaMemsetAsync(dev.p, 0, fused_ws_zero_bytes(M, 1), st));
-  QCH_CUDA(cudaMemsetAsync(g.s.bad, 0xff, 2 * sizeof(unsigned long long), st));
+  fused_carve(pp.ws, N, M, 1, &g, &ctr);
+  if (pp.ws_dirty)
+    if (int rc = fused_ws_init(pp.ws, N, M, st)) return rc;
+  g.done_ctr = fused_done_ptr(g, M);
+  g.flags_out = (unsigned long long*)mapped_ptr(pp.h_flags);  // status words straight into page-locked memory
   g.s.ca = CoefArgs{sig, (int)K, S, M, (int)sub, (t_end - t_start) / (double)(S - 1)};
   g.s.h0 = nullptr;  // operators inline (g.opsv)
   g.s.hk = nullptr;
@@ -857,7 +1178,6 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   g.pex = nullptr;
   g.etile = nullptr;
   g.block_out = nullptr;
-  Pipe& pp = pipe_for_device();
   if (sig_stream) {
     const int64_t tiles = fused_tiles(M);
     int nch = (int)std::min<int64_t>(8, tiles);
@@ -883,11 +1203,11 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   }
   if (int rc = fused_launch_any((int)N, g, st)) return rc;
   if (sig_stream) QCH_CUDA(cudaStreamWaitEvent(st, pp.ev1, 0));  // copies retired before the buffers are freed
-  QCH_CUDA(cudaMemcpyAsync(pp.h_flags, g.s.bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   if (traj == d_traj)
     QCH_CUDA(cudaMemcpyAsync(h_traj, d_traj, sizeof(double2) * N * (M + 1), cudaMemcpyDeviceToHost, st));
   tr.mark("enqueued");
   QCH_CUDA(cudaStreamSynchronize(st));
+  pp.ws_dirty = false;  // the kernel ran to completion: workspace clean again
   tr.mark("synchronized");
   const unsigned long long b0 = pp.h_flags[0], b1 = pp.h_flags[1];
   if (check && b0 != ~0ull) {

@@ -362,8 +362,13 @@ __device__ __forceinline__ Mat<N> expm_minus_i_fast(const Mat<N>& hb) {
       nb *= scl;
     }
   }
-  int m = kTaylorOrder;
-  while (m > 1 && nb <= kTheta[m - 1]) --m;
+  // smallest degree m >= 1 with nb > kTheta[m-1] (kTheta increasing): count
+  // the thresholds below nb with independent compares (a dependent
+  // compare-and-load loop sat on the critical path of every interval)
+  int m = 0;
+#pragma unroll
+  for (int q = 0; q < kTaylorOrder; ++q) m += nb > kTheta[q] ? 1 : 0;
+  m = max(m, 1);
   if (!(nb == nb)) m = kTaylorOrder;
   const Mat<N> a2 = mat_mul_fma<N>(a, a);
   int j = m >> 1;
@@ -497,6 +502,87 @@ __device__ __forceinline__ Mat<N> interval_hbar(const SmallArgs& g, const double
           for (int c = 0; c < N; ++c)
             x.v[r][c] = cadd(x.v[r][c], rmul(w, d2c(s_ops[(1 + K + q) * N * N + r * N + c])));
       }
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) hb.v[r][c] = cadd(hb.v[r][c], mkc(QMUL(0.5, x.v[r][c].im), QMUL(-0.5, x.v[r][c].re)));
+  }
+  return hb;
+}
+
+// interval_hbar for a compile-time samples-per-interval SUB with the signal
+// window in shared memory (the fused kernel's staged window; `sig` must point
+// into shared memory so the loads are LDS): each control's SUB+1 samples are
+// loaded once into registers and the coefficients are formed from them with
+// exactly the operation order of coef1 / coef_alpha / coef_beta.
+template <int N, int SUB>
+__device__ __forceinline__ Mat<N> interval_hbar_fixed(const SmallArgs& g, const double2* s_ops, const double* sig,
+                                                      int64_t S, int64_t nl) {
+  const int K = g.ca.K;
+  const double h = g.ca.dt, h2 = QDIV(h, 2.0), hh6 = QDIV(QMUL(h, h), 6.0);
+  Mat<N> hb, x;
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+      hb.v[r][c] = rmul(g.dt_int, d2c(s_ops[r * N + c]));
+      x.v[r][c] = mkc(0, 0);
+    }
+  const bool o2 = g.order >= 2;
+  for (int k = 0; k < K; ++k) {
+    double u[SUB + 1];
+#pragma unroll
+    for (int q = 0; q <= SUB; ++q) u[q] = sig[k * S + nl * SUB + q];
+    const double w = QMUL(h2, np_pairwise([&](int q) { return QADD(u[q], u[q + 1]); }, SUB));
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int c = 0; c < N; ++c) hb.v[r][c] = cadd(hb.v[r][c], rmul(w, d2c(s_ops[(1 + k) * N * N + r * N + c])));
+    if (o2) {
+      double run = 0.0, acc = 0.0, lin = 0.0;
+#pragma unroll
+      for (int q = 0; q < SUB; ++q) {
+        const double tau = QMUL(h2, QADD(u[q], u[q + 1]));
+        acc = QADD(acc, QSUB(QMUL(h, run), QMUL(QMUL((double)q, h), tau)));
+        lin = QADD(lin, QSUB(u[q + 1], u[q]));
+        run = QADD(run, tau);
+      }
+      const double a = QSUB(acc, QMUL(hh6, lin));
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int c = 0; c < N; ++c)
+          x.v[r][c] = cadd(x.v[r][c], rmul(a, d2c(s_ops[(1 + K + k) * N * N + r * N + c])));
+    }
+  }
+  if (o2) {
+    int q2 = K;
+    for (int k = 0; k < K; ++k) {
+      double uk[SUB + 1];
+#pragma unroll
+      for (int q = 0; q <= SUB; ++q) uk[q] = sig[k * S + nl * SUB + q];
+      for (int l = k + 1; l < K; ++l, ++q2) {
+        double ul[SUB + 1];
+#pragma unroll
+        for (int q = 0; q <= SUB; ++q) ul[q] = sig[l * S + nl * SUB + q];
+        double sk = 0.0, sl = 0.0, acc = 0.0, cr = 0.0;
+#pragma unroll
+        for (int q = 0; q < SUB; ++q) {
+          const double tk = QMUL(h2, QADD(uk[q], uk[q + 1]));
+          const double tl = QMUL(h2, QADD(ul[q], ul[q + 1]));
+          acc = QADD(acc, QSUB(QMUL(tk, sl), QMUL(tl, sk)));
+          cr = QADD(cr, QSUB(QMUL(uk[q], ul[q + 1]), QMUL(ul[q], uk[q + 1])));
+          sk = QADD(sk, tk);
+          sl = QADD(sl, tl);
+        }
+        const double b = QSUB(acc, QMUL(hh6, cr));
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int c = 0; c < N; ++c)
+            x.v[r][c] = cadd(x.v[r][c], rmul(b, d2c(s_ops[(1 + K + q2) * N * N + r * N + c])));
+      }
+    }
 #pragma unroll
     for (int r = 0; r < N; ++r)
 #pragma unroll

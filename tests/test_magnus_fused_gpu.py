@@ -158,3 +158,59 @@ def test_host_call_signal_modes(E, mode, monkeypatch):
     monkeypatch.setenv("QCH_SIG_MODE", mode)
     got = E.evolve(ch, g2, m, psi0, order=2)
     assert rel_fro(got.amplitudes, _oracle(ch, grid, m, psi0, 2)) <= 1e-10
+
+
+def test_evolve_plan_flags_every_replay(E):
+    # the plan's self-cleaning workspace: status words are recomputed on every
+    # replay (the kernel's last block resets them), a bad plan keeps raising
+    m = 2048
+    ch, grid = E.driven_transmon(3, intervals=m, sub=4, t_final=10.0)
+    bad = ch.drift.data.copy()
+    bad[1, 1] += 0.5j
+    chb = E.ControlledHamiltonian(E.HermitianOperator(bad, validate=False), ch.controls)
+    psi0 = np.array([1, 0, 0], dtype=complex)
+    plan = E.EvolvePlan(chb, grid, m, psi0, order=2, check=False)
+    for _ in range(3):
+        plan.run()
+        with pytest.raises(E.NormDrift):
+            plan.check()
+    good = E.EvolvePlan(ch, grid, m, psi0, order=2, check=True)
+    for _ in range(3):
+        good.run()
+        good.check()
+
+
+def test_evolve_plan_many_waves(E):
+    # more tiles than resident blocks: groups of tiles, look-back over groups,
+    # workspace reused across replays
+    import torch
+
+    m = 1_000_000
+    ch, grid = E.driven_transmon(3, intervals=m, sub=4, t_final=500.0)
+    psi0 = np.array([1, 0, 0], dtype=complex)
+    plan = E.EvolvePlan(ch, grid, m, psi0, order=2, check=True)
+    outs = []
+    for _ in range(3):
+        outs.append(plan.run().clone())
+    plan.check()
+    from paper_2411_09982_b200 import magnus as mg
+
+    want = mg.evolve_device(ch, grid, m, torch.tensor(psi0, device="cuda"), check=True, order=2)
+    for o in outs:
+        assert rel_fro(o.cpu().numpy(), want.cpu().numpy()) <= 1e-12
+    sub = 20_000
+    ref = _oracle(ch, E.ControlGrid(grid.t_start, grid.t_start + (grid.t_end - grid.t_start) * sub / m,
+                                    grid.signals[:, : sub * 4 + 1]), sub, psi0, 2)
+    assert rel_fro(outs[-1][: sub + 1].cpu().numpy(), ref) <= 1e-10
+
+
+def test_host_call_workspace_relayout(E):
+    # the host call's cached workspace is re-initialised when (N, M) change
+    psi0 = np.array([1, 0, 0], dtype=complex)
+    for m in (1000, 3000, 1000, 257, 3000):
+        ch, grid = E.driven_transmon(3, intervals=m, sub=4, t_final=10.0)
+        got = E.evolve(ch, grid, m, psi0, order=2)
+        assert rel_fro(got.amplitudes, _oracle(ch, grid, m, psi0, 2)) <= 1e-10
+    ch2, grid2 = E.driven_transmon(2, intervals=500, sub=4, t_final=10.0)
+    got = E.evolve(ch2, grid2, 500, np.array([1, 0], dtype=complex), order=1)
+    assert rel_fro(got.amplitudes, _oracle(ch2, grid2, 500, np.array([1, 0], dtype=complex), 1)) <= 1e-10
