@@ -206,15 +206,17 @@ int qch_magnus_evolve_plan_c128(const void* d_h0, const void* d_hk, const void* 
 
 /* evolve (magnus.py:214-267) with HOST buffers — the reference-facing call:
  * h_h0 (N,N), h_hk (K,N,N), h_sig (K,S) row-major, h_psi0 (N) are read from
- * host memory, the trajectory (M+1, N) is written to h_traj.  For N <= 4 the
- * transfers are pipelined in chunks against the single-pass fused kernel
- * (H2D of chunk c+1 || kernel on chunk c || D2H of chunk c-1); pinned host
- * buffers give full overlap, pageable ones are staged by the driver.
- * Synchronous.  Errors as qch_magnus_evolve_c128.  Not re-entrant on one
- * device (shares the device's side streams). */
+ * host memory, the trajectory (M+1, N) is written to h_traj.  For N <= 4 ONE
+ * single-pass fused kernel does everything: page-locked h_sig / h_traj are
+ * read and written by the kernel itself over the host link (zero copy, the
+ * transfers overlap the arithmetic); pageable buffers are staged by the
+ * driver.  h_times (nullable, M+1 doubles) receives np.linspace(t_start,
+ * t_end, M+1) bit for bit (magnus.py:263), filled on the host while the
+ * kernel runs.  Synchronous.  Errors as qch_magnus_evolve_c128.  Not
+ * re-entrant on one device (shares the device's workspace and side streams). */
 int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, int64_t K, int64_t N, const double* h_sig,
                                 int64_t S, double t_start, double t_end, int64_t M, int order, const void* h_psi0,
-                                void* h_traj, int check, int64_t* bad_index, void* stream);
+                                void* h_traj, int check, int64_t* bad_index, double* h_times, void* stream);
 
 /* ------------------------------------------------------------ GEMM ------- */
 

@@ -98,7 +98,7 @@ PROTOTYPES = {
     "qch_magnus_evolve_host_c128": (
         c_int,
         [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int, c_void_p,
-         c_void_p, c_int, P_int64, c_void_p],
+         c_void_p, c_int, P_int64, c_void_p, c_void_p],
     ),
     "qch_zgemm_batched": (
         c_int,

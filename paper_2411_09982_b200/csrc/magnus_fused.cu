@@ -95,6 +95,7 @@ struct FusedArgs {
   // self-cleaning workspace (plan / host-buffer calls): the last block to
   // finish copies the status words to flags_out (nullable) and returns the
   // workspace to its initial state, so a launch needs no memset before it
+  int sched_static;               // 1: static round-robin tiles (see the kernel), 0: dynamic grabbing
   int* done_ctr;                  // null: the caller zeroes the workspace per launch
   unsigned long long* flags_out;  // (2,) first non-unitary interval, first norm drift
   unsigned long long* stats;  // non-null (QCH_MAGNUS_STATS): per-block phase cycles, see fused_print_stats
@@ -383,12 +384,17 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
   // the control samples of a tile: one coalesced pass into shared memory,
   // issued asynchronously (cp.async) one tile ahead, so that the fetch of the
   // next window — possibly from mapped host memory over the host link —
-  // overlaps this tile's arithmetic
+  // overlaps this tile's arithmetic.  Warps 1-3 issue the host-link traffic
+  // (window reads, trajectory writes): warp 0 runs the fenced publish / group
+  // protocol, and a fence waits for the issuing thread's own outstanding
+  // accesses — an in-flight window read over PCIe cost ~45k cycles per fence
   auto prefetch = [&](int64_t tt, double* buf) {
     const int64_t s0 = tt * kTile * (int64_t)g.s.ca.sub;
     const int64_t cnt = std::min<int64_t>(g.win, g.s.ca.S - s0);
     for (int k = 0; k < K; ++k)
-      for (int64_t q = tid; q < cnt; q += kFusedThreads) cp_async8(buf + k * g.win + q, g.s.ca.sig + k * g.s.ca.S + s0 + q);
+      if (warp > 0)
+        for (int64_t q = tid - 32; q < cnt; q += kFusedThreads - 32)
+          cp_async8(buf + k * g.win + q, g.s.ca.sig + k * g.s.ca.S + s0 + q);
     cp_commit();
   };
 
@@ -412,19 +418,30 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
     for (int q = 0; q < 19; ++q) st_acc[q] = 0;
     st_acc[6] = clock64();
   }
-  if (tid == 0) {
+  // tile schedule: static round robin (block b: tiles b, b + grid, ...; the
+  // next window is known, so it is prefetched while the current tile is
+  // computed — the host-link mode) or dynamic grabbing (load balance)
+  const bool stat = g.sched_static != 0;
+  if (!stat && tid == 0) {
     s_tile = atomicAdd(g.tile_ctr, 1);
     wait_chunk(g.tile_begin + s_tile);
   }
   __syncthreads();
-  int64_t t = g.tile_begin + s_tile;
+  int64_t t = stat ? g.tile_begin + blockIdx.x : g.tile_begin + s_tile;
+  // the first window; later ones are requested as the previous one lands
+  const int64_t G = gridDim.x;
   if (g.win > 0 && t < g.tile_end) prefetch(t, s_sig0);
   for (int it = 0;; ++it) {
     if (t >= g.tile_end) break;
-    double* s_sig = s_sig0 + (it & 1) * wstride;
+    double* s_sig = s_sig0 + (size_t)(it & 1) * wstride;
     double2* s_traj = traj_in_window ? (double2*)s_sig : s_traj_own;
+    const int64_t t_next = t + G;  // static schedule
     if (g.win > 0) cp_wait<0>();
     __syncthreads();
+    // static schedule: request the next round's window only now that this
+    // one has landed, so the host link serves the windows round by round (in
+    // tile order) instead of interleaving every block's rounds
+    if (stat && g.win > 0 && t_next < g.tile_end) prefetch(t_next, s_sig0 + (size_t)((it + 1) & 1) * wstride);
     mark(1);
     if (g.stats != nullptr && tid == 0) st_acc[0] += 1;
     const int64_t n0 = t * kTile + (int64_t)tid * kR;
@@ -520,17 +537,19 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
         ldcg_mat<N>(e, g.inc + t * N * N);
         s_e = e;
         if (g.stats != nullptr) st_acc[15] += clock64() - cw0;
-        // grab the next tile only now: a block never holds an unstarted tile
-        // while it waits for its prefix
-        s_tile = atomicAdd(g.tile_ctr, 1);
-        wait_chunk(g.tile_begin + s_tile);
+        // dynamic schedule: grab the next tile only now — a block never
+        // holds an unstarted tile while it waits for its prefix
+        if (!stat) {
+          s_tile = atomicAdd(g.tile_ctr, 1);
+          wait_chunk(g.tile_begin + s_tile);
+        }
       }
     }
     __syncthreads();
-    const int64_t tn = g.tile_begin + s_tile;
-    // the next tile's signal window streams in while this tile's trajectory
-    // is formed and written
-    if (g.win > 0 && tn < g.tile_end) prefetch(tn, s_sig0 + ((it + 1) & 1) * wstride);
+    const int64_t tn = stat ? t_next : g.tile_begin + s_tile;
+    // dynamic schedule: the next tile's signal window streams in while this
+    // tile's trajectory is formed and written
+    if (!stat && g.win > 0 && tn < g.tile_end) prefetch(tn, s_sig0 + (size_t)((it + 1) & 1) * wstride);
     mark(4);
     if (g.pex != nullptr) {
       // prefix mode: the thread's start = (P_{lane-1} X_warp) E_t psi_start,
@@ -588,7 +607,8 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
       const int64_t row0 = t * kTile + 1;
       const int64_t rows = std::min<int64_t>(kTile, g.M - t * kTile);
       double2* dst = g.traj + row0 * N;
-      for (int64_t q = tid; q < rows * N; q += kFusedThreads) dst[q] = s_traj[q];
+      if (warp > 0)
+        for (int64_t q = tid - 32; q < rows * N; q += kFusedThreads - 32) dst[q] = s_traj[q];
     }
     __syncthreads();  // s_w / s_e / s_traj reuse
     mark(5);
@@ -649,15 +669,24 @@ static int64_t fused_window(int K, int sub) {
 template <int N>
 static int fused_launch(FusedArgs& g, cudaStream_t st) {
   g.win = fused_window(g.s.ca.K, g.s.ca.sub);
+  const int64_t tiles = g.tile_end - g.tile_begin;
+  if (tiles <= 0) return QCH_OK;
+  if (const char* e = getenv("QCH_SCHED")) g.sched_static = strcmp(e, "static") == 0 ? 1 : 0;
+  if (g.chunk_flag != nullptr) g.sched_static = 0;  // chunked signals: tiles taken in arrival order
+  static int smem_optin = 0;
+  if (smem_optin == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    QCH_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    QCH_CUDA(cudaFuncGetAttributes(&fa, magnus_fused_kernel<N>));
+    smem_optin -= (int)fa.sharedSizeBytes;  // dynamic share of the opt-in maximum
+    QCH_CUDA(cudaFuncSetAttribute(magnus_fused_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
+  }
   const size_t wbytes = (((size_t)g.s.ca.K * g.win + 1) & ~(size_t)1) * sizeof(double);
   const size_t tbytes = sizeof(double2) * (size_t)kTile * N;
-  const size_t smem = fused_smem<N>(g.s.ca.K) + 2 * wbytes + (g.win > 0 && wbytes >= tbytes ? 0 : tbytes);
-  static bool attr = false;
-  if (!attr) {
-    QCH_CUDA(cudaFuncSetAttribute(magnus_fused_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(fused_smem<N>(8) + 2 * kStageMax + 32 + sizeof(double2) * kTile * N)));
-    attr = true;
-  }
+  const size_t sbase = fused_smem<N>(g.s.ca.K) + (g.win > 0 && wbytes >= tbytes ? 0 : tbytes);
+  const size_t smem = sbase + (g.win > 0 ? 2 * wbytes : 0);
   static size_t occ_smem[4] = {0, 0, 0, 0};
   static int occ_val[4] = {0, 0, 0, 0};
   int blocks_per_sm = 0;
@@ -671,8 +700,6 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
     occ_val[slot & 3] = blocks_per_sm;
     ++slot;
   }
-  const int64_t tiles = g.tile_end - g.tile_begin;
-  if (tiles <= 0) return QCH_OK;
   int64_t slots = (int64_t)blocks_per_sm * sm_count();
   if (g.stream_blocks_per_sm > 0) slots = std::min<int64_t>(slots, (int64_t)g.stream_blocks_per_sm * sm_count());
   const int grid = (int)std::min<int64_t>(tiles, slots);
@@ -680,8 +707,8 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
   // outnumber them (a block waits for its group, so the unfinished top group
   // must never hold every resident block)
   g.gshift = 5;
-  if (tiles > grid)
-    while (g.gshift > 0 && (1 << g.gshift) > grid / 2) --g.gshift;
+  if (tiles > grid)  // static schedule: group <= grid suffices; dynamic: <= grid / 2
+    while (g.gshift > 0 && (1 << g.gshift) > (g.sched_static ? grid : grid / 2)) --g.gshift;
   static const bool want_stats = getenv("QCH_MAGNUS_STATS") != nullptr;
   static unsigned long long* d_stats = nullptr;
   g.stats = nullptr;
@@ -689,9 +716,17 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
     if (d_stats == nullptr) QCH_CUDA(cudaMalloc(&d_stats, sizeof(unsigned long long) * kStatW * 4096));
     if (grid <= 4096) g.stats = d_stats;
   }
+  static const bool trace = getenv("QCH_TRACE") != nullptr;
+  const auto tl0 = std::chrono::steady_clock::now();
   void* pr = prof_begin("magnus_fused_kernel", st);
+  const auto tl1 = std::chrono::steady_clock::now();
   magnus_fused_kernel<N><<<grid, kFusedThreads, smem, st>>>(g);
+  const auto tl2 = std::chrono::steady_clock::now();
   prof_end(pr, st);
+  if (trace)
+    fprintf(stderr, "[qch trace] fused launch: prof %.1f us, <<<>>> %.1f us (params %zu B, grid %d, smem %zu)\n",
+            std::chrono::duration<double, std::micro>(tl1 - tl0).count(),
+            std::chrono::duration<double, std::micro>(tl2 - tl1).count(), sizeof(g), grid, smem);
   QCH_LAUNCH_CHECK("magnus_fused_kernel");
   if (g.stats != nullptr) {
     std::vector<unsigned long long> h((size_t)kStatW * grid);
@@ -767,6 +802,7 @@ void fused_carve(void* ws, int64_t N, int64_t M, int nlaunch, FusedArgs* g, int*
   *ctr = g->flag + nt;
   g->gflag = *ctr + nlaunch;
   g->gcount = g->gflag + nt;
+  g->sched_static = 0;
   g->done_ctr = nullptr;  // set by the self-cleaning callers
   g->flags_out = nullptr;
   p += al(sizeof(int) * (3 * nt + nlaunch + 1));
@@ -1059,10 +1095,39 @@ extern "C" int qch_magnus_evolve_c128(const void* d_h0, const void* d_hk, const 
 // trajectory written to host memory.  For N <= 4 one fused launch streams the
 // page-locked buffers over the host link itself (zero-copy), so transfers and
 // compute overlap; pageable buffers are staged through device memory.
+// np.linspace(t0, t1, n) bit for bit (numpy/_core/function_base.py):
+// step = (t1 - t0) / (n - 1); y_i = i * step + t0 (two roundings, no FMA);
+// a zero (underflowed) step takes numpy's (i / div) * delta branch; the last
+// point is t1 exactly.
+static void np_linspace(double t0, double t1, int64_t n, double* y) {
+  if (n <= 0) return;
+  const int64_t div = n - 1;
+  volatile double delta = t1 - t0;
+  if (div > 0) {
+    const double step = delta / (double)div;
+    if (step == 0.0) {
+      for (int64_t i = 0; i < n; ++i) {
+        volatile double q = (double)i / (double)div;
+        volatile double r = q * delta;
+        y[i] = r + t0;
+      }
+    } else {
+      for (int64_t i = 0; i < n; ++i) {
+        volatile double r = (double)i * step;
+        y[i] = r + t0;
+      }
+    }
+    y[n - 1] = t1;
+  } else {
+    volatile double r = 0.0 * delta;
+    y[0] = r + t0;
+  }
+}
+
 extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, int64_t K, int64_t N,
                                            const double* h_sig, int64_t S, double t_start, double t_end, int64_t M,
                                            int order, const void* h_psi0, void* h_traj, int check,
-                                           int64_t* bad_index, void* stream) {
+                                           int64_t* bad_index, double* h_times, void* stream) {
   if (M < 1) return fail(QCH_ERR_GRID, "need at least one interval");
   if ((S - 1) % M)
     return fail(QCH_ERR_GRID, std::to_string(M) + " intervals do not divide " + std::to_string(S - 1) + " sample steps");
@@ -1095,6 +1160,7 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
                                         d_traj, nullptr, check, bad_index, stream))
       return rc;
     QCH_CUDA(cudaMemcpyAsync(h_traj, d_traj, sizeof(double2) * N * (M + 1), cudaMemcpyDeviceToHost, st));
+    if (h_times) np_linspace(t_start, t_end, M + 1, h_times);
     QCH_CUDA(cudaStreamSynchronize(st));
     return QCH_OK;
   }
@@ -1158,7 +1224,12 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   if (pp.ws_dirty)
     if (int rc = fused_ws_init(pp.ws, N, M, st)) return rc;
   g.done_ctr = fused_done_ptr(g, M);
+  tr.mark("workspace");
   g.flags_out = (unsigned long long*)mapped_ptr(pp.h_flags);  // status words straight into page-locked memory
+  tr.mark("flags ptr");
+  // host-link I/O: static tile schedule, so each block prefetches its next
+  // signal window while it computes the current tile
+  g.sched_static = g.stream_blocks_per_sm > 0 ? 1 : 0;
   g.s.ca = CoefArgs{sig, (int)K, S, M, (int)sub, (t_end - t_start) / (double)(S - 1)};
   g.s.h0 = nullptr;  // operators inline (g.opsv)
   g.s.hk = nullptr;
@@ -1201,11 +1272,15 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
     g.tiles_per_chunk = tpc;
     g.stream_blocks_per_sm = 0;
   }
+  tr.mark("args");
   if (int rc = fused_launch_any((int)N, g, st)) return rc;
+  tr.mark("launched");
   if (sig_stream) QCH_CUDA(cudaStreamWaitEvent(st, pp.ev1, 0));  // copies retired before the buffers are freed
   if (traj == d_traj)
     QCH_CUDA(cudaMemcpyAsync(h_traj, d_traj, sizeof(double2) * N * (M + 1), cudaMemcpyDeviceToHost, st));
   tr.mark("enqueued");
+  if (h_times) np_linspace(t_start, t_end, M + 1, h_times);  // on the host while the kernel runs
+  tr.mark("times");
   QCH_CUDA(cudaStreamSynchronize(st));
   pp.ws_dirty = false;  // the kernel ran to completion: workspace clean again
   tr.mark("synchronized");

@@ -214,3 +214,14 @@ def test_host_call_workspace_relayout(E):
     ch2, grid2 = E.driven_transmon(2, intervals=500, sub=4, t_final=10.0)
     got = E.evolve(ch2, grid2, 500, np.array([1, 0], dtype=complex), order=1)
     assert rel_fro(got.amplitudes, _oracle(ch2, grid2, 500, np.array([1, 0], dtype=complex), 1)) <= 1e-10
+
+
+@pytest.mark.parametrize("t0,t1,m", [(0.0, 100.0, 100_000), (-3.7, 12.9, 777), (1e-3, 1e-3 + 1e-9, 1000),
+                                     (0.1, 0.7, 3)])
+def test_host_call_times_are_linspace(E, t0, t1, m):
+    # times come from the C-ABI call (filled on the host during the kernel),
+    # bit for bit np.linspace (magnus.py:263)
+    ch, grid = E.driven_transmon(3, intervals=m, sub=4, t_final=10.0)
+    g2 = E.ControlGrid(t0, t1, grid.signals)
+    out = E.evolve(ch, g2, m, np.array([1, 0, 0], dtype=complex), order=1, check=False)
+    np.testing.assert_array_equal(out.times, np.linspace(t0, t1, m + 1))

@@ -23,8 +23,31 @@ def main():
     sig_p = torch.empty(grid.signals.shape, dtype=torch.float64).pin_memory()
     sig_p.numpy()[:] = grid.signals
     g2 = eff.ControlGrid(grid.t_start, grid.t_end, sig_p.numpy())
-    for env in ({}, {"QCH_SIG_CHUNKS": "4"}, {"QCH_SIG_CHUNKS": "16"}, {"QCH_SIG_CHUNKS": "32"},
-                {"QCH_SIG_MODE": "map"}, {"QCH_SIG_MODE": "copy"}, {"QCH_NOMAP_TRAJ": "1"},
+    # transfer floor on this box: H2D of the signals || D2H of a trajectory
+    d_sig = torch.empty(grid.signals.shape, dtype=torch.float64, device="cuda")
+    d_tr = torch.empty((m + 1, 3), dtype=torch.complex128, device="cuda")
+    h_tr = torch.empty((m + 1, 3), dtype=torch.complex128).pin_memory()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for name, fn in (("H2D 6.4 MB", lambda: d_sig.copy_(sig_p, non_blocking=True)),
+                     ("D2H 4.8 MB", lambda: h_tr.copy_(d_tr, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(20):
+            fn()
+        torch.cuda.synchronize()
+        print(f"{name:60s} wall {(time.perf_counter() - t0) / 20 * 1e6:8.1f} us")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(20):
+        with torch.cuda.stream(s1):
+            d_sig.copy_(sig_p, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_tr.copy_(d_tr, non_blocking=True)
+        torch.cuda.synchronize()
+    print(f"{'H2D || D2H':60s} wall {(time.perf_counter() - t0) / 20 * 1e6:8.1f} us")
+    for env in ({}, {"QCH_STREAM_BPS": "2"}, {"QCH_STREAM_BPS": "3"}, {"QCH_SIG_MODE": "stream"},
+                {"QCH_SIG_MODE": "copy"}, {"QCH_NOMAP_TRAJ": "1"},
                 {"QCH_SIG_MODE": "copy", "QCH_NOMAP_TRAJ": "1"}):
         os.environ.update(env)
         for _ in range(3):
@@ -43,6 +66,9 @@ def main():
         print(f"{str(sorted(env.items())):60s} wall {wall:8.1f} us   kernel {k[0] / k[1] * 1e3:8.1f} us")
         for key in env:
             del os.environ[key]
+    os.environ["QCH_MAGNUS_STATS"] = "1"
+    for _ in range(2):
+        eff.evolve(ch, g2, m, psi0, order=2, check=False)
 
 
 if __name__ == "__main__":
