@@ -785,6 +785,7 @@ int npad_launch2(NpadJob2* jobs, int njobs, const NpadCommon2& cm, bool herm, bo
     if (d != nullptr && strcmp(d, "cta") == 0) return npad_launch_trows_cta(jobs, njobs, cm, st);
     if ((d == nullptr || strcmp(d, "block") != 0) && many) return npad_launch_trows_warp(jobs, njobs, cm, st);
   }
+  if (npad_full_warp_ok(cm, herm, trows)) return npad_launch_full_warp(jobs, njobs, cm, st);
   if (trows) {
     switch (cpt) {
       case 1: return launch_trows_t<1>(jobs, njobs, cm, threads, st);
