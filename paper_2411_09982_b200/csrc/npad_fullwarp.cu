@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
   long long applied = job->applied;
   const double thr = job->threshold;
   int status = 0;
+  long long cyc[5] = {0, 0, 0, 0, 0}, nresc = 0;  // select, scalars, rotate, rows i/j, rescans
+  long long c0 = clock64();
   while (true) {
     Cand best = rb[0];
     cand_take(best, rb[1]);
@@ -101,6 +103,11 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       status = 1;
       break;
     }
+    long long c1 = 0;
+    if (cm.stats) {
+      c1 = clock64();
+      cyc[0] += c1 - c0;
+    }
     const int i = (int)(piv.cr >> 16), j = (int)(piv.cr & 0xffffu);  // i < j
     const cplx v = d2c(piv.v);
     const double hii = hs[i * kPitch + i].x, hjj = hs[j * kPitch + j].x;
@@ -111,6 +118,11 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
     if (lane == 0 && job->pivots != nullptr && applied < job->pivot_cap) {
       job->pivots[2 * applied] = i;
       job->pivots[2 * applied + 1] = j;
+    }
+    long long c2 = 0;
+    if (cm.stats) {
+      c2 = clock64();
+      cyc[1] += c2 - c1;
     }
     Cand pi = cand_none(), pj = cand_none();
     bool resc[2] = {false, false};
@@ -154,6 +166,11 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       hs[j * kPitch + j] = c2d(blk.jj);
       cand_take(pj, make_cand(c2d(blk.ji), ((unsigned)i << 16) | (unsigned)j, ek));
     }
+    long long c3 = 0;
+    if (cm.stats) {
+      c3 = clock64();
+      cyc[2] += c3 - c2;
+    }
     // rows i, j: reduced from the fresh values
     const Cand bi = warp_best(pi);
     const Cand bj = warp_best(pj);
@@ -168,6 +185,12 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
     __syncwarp();  // the rotated rows / columns visible to the rescans
     // rows whose argmax column was i or j: whole-warp rescans
     unsigned m0 = __ballot_sync(kFull, resc[0]), m1 = __ballot_sync(kFull, resc[1]);
+    long long c4 = 0;
+    if (cm.stats) {
+      c4 = clock64();
+      cyc[3] += c4 - c3;
+      nresc += __popc(m0) + __popc(m1);
+    }
     while (m0 | m1) {
       int r;
       if (m0) {
@@ -190,6 +213,16 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       }
     }
     ++applied;
+    if (cm.stats) {
+      c0 = clock64();
+      cyc[4] += c0 - c4;
+    }
+  }
+  if (cm.stats && lane == 0) {
+    const double a = applied > 0 ? (double)applied : 1.0;
+    printf("npad full-warp n=%d: %lld rotations, cycles/rotation select %.0f scalars %.0f rotate %.0f rows-ij %.0f "
+           "rescans %.0f (%.2f rows)\n",
+           n, applied, cyc[0] / a, cyc[1] / a, cyc[2] / a, cyc[3] / a, cyc[4] / a, nresc / a);
   }
 
   __syncwarp();
