@@ -510,6 +510,55 @@ def sec_magnus4096(torch, eff, lib, args, fp64, n_int=2):
                                        "OpenBLAS); not re-timed here (42 h full run)"}}
 
 
+def sec_midsize(torch, eff, lib, args, fp64, L=8, n_int=2048):
+    """dense propagation at mid-size N (8-spin Heisenberg
+    chain, N = 256) with the reference's default check=True."""
+    from oracle import magnus_oracle
+    from paper_2411_09982_b200 import magnus as mg
+
+    n = 1 << L
+    ch = eff.heisenberg_chain_hamiltonians(L)
+    pulse = eff.synthetic_transfer_pulse(25.0, n_int * 8 + 1, seed=7)
+    grid = eff.ControlGrid(0.0, 25.0, pulse.signals)
+    psi0 = np.zeros(n, dtype=complex)
+    psi0[0] = 1
+    d_psi = lib.to_device(psi0)
+    ch.device_operators()
+
+    def step():
+        mg.evolve_device(ch, grid, n_int, d_psi, check=True, order=2)
+
+    step()
+    lib.profile_read(reset=True)
+    lib.profile_enable(True)
+    ms = time_steps(torch, step, 3, lambda: None, 1)
+    lib.profile_enable(False)
+    prof = lib.profile_read(reset=True)
+    per = sum(ms) / len(ms)
+    g_ms = sum(v[0] for k, v in prof.items() if k.startswith("zgemm")) / 3
+    g_cnt = sum(v[1] for k, v in prof.items() if k.startswith("zgemm")) / 3
+    fl = g_cnt * n_int * 8 * n**3
+    ach = fl / (g_ms * 1e-3) / 1e12 if g_ms else None
+    chain_ms = prof.get("chain_grid_kernel", (0.0, 1))[0] / 3
+    # CPU: the oracle (numpy restatement of evolve, 18-term Taylor, order 2) on 8 intervals
+    k_cpu = 8
+    d0 = ch.drift.to_dense()
+    ctr = np.stack([c.to_dense() for c in ch.controls])
+    sub_sig = grid.signals[:, : k_cpu * 8 + 1]
+    t0 = time.perf_counter()
+    magnus_oracle.evolve(d0, ctr, sub_sig, 0.0, 25.0 * k_cpu / n_int, k_cpu, psi0, order=2)
+    cpu = k_cpu / (time.perf_counter() - t0)
+    return {"workload": f"SURVEY 8(f) rank 2: Magnus, {L}-spin Heisenberg chain (dim {n}), {n_int} intervals, "
+                        f"order 2, check=True",
+            "metric": "Magnus intervals/s", "unit": "intervals/s", "value": n_int / (per * 1e-3),
+            "ms_per_step": per, "gemm_ms": g_ms, "chain_ms": chain_ms,
+            "roofline": {"bound": "tensor", "kernel": "zgemm_kernel (DMMA)", "achieved": ach, "peak": fp64.get("dmma"),
+                         "unit": "TFLOP/s", "frac": (ach / fp64["dmma"]) if ach and fp64.get("dmma") else None,
+                         "flops_basis": "executed GEMM flops (8N^3 per complex GEMM)"},
+            "cpu_baseline": {"value": cpu, "unit": "intervals/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{k_cpu} intervals, oracle/magnus_oracle.evolve (numpy/OpenBLAS)"}}
+
+
 def sec_givens(torch, eff, lib, args, peaks, sizes=(10**5, 10**6, 10**7, 10**8)):
     """SURVEY 8(f) rank 1 / the paper's Fig. 4 protocol (bench_givens,
     experiments.py:420-453): ONE Givens rotation eliminating the smallest
@@ -646,7 +695,7 @@ def main():
 
     secondary = []
     if rank == 0 and world == 1 and args.secondary != "none":
-        want = {"npad60", "npad4096", "sweep", "magnus4096", "givens"} if args.secondary == "all" else set(
+        want = {"npad60", "npad4096", "sweep", "magnus4096", "givens", "midsize"} if args.secondary == "all" else set(
             args.secondary.split(","))
         peaks = (hbm_peak, hbm_src)
         if "npad60" in want:
@@ -659,6 +708,8 @@ def main():
             secondary.append(sec_magnus4096(torch, eff, lib, args, fp64))
         if "givens" in want:
             secondary.append(sec_givens(torch, eff, lib, args, peaks))
+        if "midsize" in want:
+            secondary.append(sec_midsize(torch, eff, lib, args, fp64))
 
     if rank == 0:
         cpu_v, cpu_t = cpu_magnus_sample(__import__("paper_2411_09982_b200.models", fromlist=["x"]), 60000)

@@ -44,6 +44,28 @@ def test_expm_batch_and_validate(E):
         E.UnitaryPropagator(2 * np.eye(3, dtype=complex)).validate()
 
 
+@pytest.mark.parametrize("n", [17, 100, 300])
+def test_validate_determinant_branch(E, n):
+    # expm.py:40-47 checks ||UU^dag - I||_F <= 1e-10 N AND ||det U| - 1| <= 1e-8.
+    # The device evaluates |det U| from tr(UU^dag) and ||UU^dag - I||_F (no
+    # LU); the decisions must equal numpy's on both sides of each bound.
+    rng = np.random.default_rng(n)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    for eps in (0.0, 2e-12, 3e-10, 2e-9):
+        u = (1.0 + eps) * q
+        defect_ok = np.linalg.norm(u @ u.conj().T - np.eye(n)) <= 1e-10 * n
+        det_ok = abs(abs(np.linalg.det(u)) - 1.0) <= 1e-8
+        if defect_ok and det_ok:
+            E.UnitaryPropagator(u).validate()
+        else:
+            with pytest.raises(E.NonFinite):
+                E.UnitaryPropagator(u).validate()
+    if n >= 100:  # scale passes the defect bound but not the determinant bound
+        u = (1.0 + 3e-10) * q
+        assert np.linalg.norm(u @ u.conj().T - np.eye(n)) <= 1e-10 * n
+        assert abs(abs(np.linalg.det(u)) - 1.0) > 1e-8
+
+
 @pytest.mark.parametrize("case", ["magnus_transmon_m2000", "magnus_spin6_m20"])
 def test_evolve_order1_vs_reference_golden(E, golden, case):
     g = golden(case)
