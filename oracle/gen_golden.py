@@ -98,10 +98,42 @@ def sparse_cases(eff) -> None:
           "; cancel", hc.nnz, "->", rc.nnz)
 
 
+def experiment_cases(eff) -> None:
+    """11. The reference's experiment runners (experiments.py:233-411) on small
+    configs: JCH Mott lobes, driven qubit, spin-chain trajectory and error
+    sweep.  Wall-time columns are not produced by these modes."""
+    import importlib
+
+    ex = importlib.import_module("effham.experiments")
+    out = {}
+    cases = {
+        "jch": (ex.run_jch_mott, ex.JchMottConfig, dict(n_lobes=2, grid_points=7, n_max=5)),
+        "qubit": (ex.run_driven_qubit, ex.DrivenQubitConfig,
+                  dict(t_final=20.0, samples=4001, m_magnus=20, m_reference=400)),
+        "qubit_sin2": (ex.run_driven_qubit, ex.DrivenQubitConfig,
+                       dict(envelope="sin2", drive_ratio=0.5, t_final=30.0, samples=6001, m_magnus=30,
+                            m_reference=600)),
+        "chain_traj": (ex.run_spin_chain, ex.SpinChainConfig,
+                       dict(mode="trajectory", length=5, samples=4001, m_magnus=40, rk_steps=100)),
+        "chain_sweep": (ex.run_spin_chain, ex.SpinChainConfig,
+                        dict(mode="error-sweep", length=4, samples=3201, sweep_m=[5, 10, 20], m_reference=160,
+                             sweep_rk=[100, 200], rk_reference=800)),
+    }
+    for name, (fn, cls, cfgd) in cases.items():
+        fields, rows = fn(ex.config_from_dict(cls, cfgd))
+        for f in fields:
+            vals = [r[f] for r in rows]
+            out[f"{name}__{f}"] = np.array(vals)
+        out[f"{name}__cfg"] = np.array(repr(cfgd))
+        print("experiments:", name, len(rows), "rows")
+    np.savez_compressed(GOLD / "experiments.npz", **out)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
-    ap.add_argument("--only", default=None, help="'sparse': regenerate only the sparse CSR vectors")
+    ap.add_argument("--only", default=None,
+                    help="'sparse' / 'experiments': regenerate only those vectors")
     args = ap.parse_args()
     eff = _import_reference(args.ref)
     sys.path.insert(0, str(ROOT))
@@ -110,6 +142,9 @@ def main() -> None:
     GOLD.mkdir(parents=True, exist_ok=True)
     if args.only == "sparse":
         sparse_cases(eff)
+        return
+    if args.only == "experiments":
+        experiment_cases(eff)
         return
 
     # 1. NPAD config 1: transmon 3 x resonator 20, full mode, tol 1e-12
@@ -200,6 +235,7 @@ def main() -> None:
                         t=np.array([grid6.t_start, grid6.t_end]), m=20, psi0=psi6, traj=traj6.amplitudes,
                         coeffs=eff.magnus_coefficients(grid6, 20))
     sparse_cases(eff)
+    experiment_cases(eff)
     print("wrote", sorted(p.name for p in GOLD.glob("*.npz")))
 
 

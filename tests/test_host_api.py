@@ -104,3 +104,26 @@ def test_infidelity_and_states():
         eff.infidelity(a, np.array([1, 0, 0], dtype=complex))
     with pytest.raises(ValueError):
         eff.StateVector([1.0, 1.0])
+
+
+def test_experiment_configs_validate():
+    from paper_2411_09982_b200 import errors, experiments as X
+
+    with pytest.raises(errors.ConfigError):
+        X.config_from_dict(X.JchMottConfig, {"bogus": 1})
+    with pytest.raises(errors.ConfigError):
+        X.config_from_dict(X.DrivenQubitConfig, {"m_magnus": 7})
+    with pytest.raises(errors.ConfigError):
+        X.config_from_dict(X.SpinChainConfig, {"mode": "timing", "repeats": 2})
+    cfg = X.config_from_dict(X.SpinChainConfig, {"mode": "error-sweep"})
+    assert cfg.samples == 16001
+    assert X.relative_error(1.0, 0.0) == 1.0 / 1e-300
+    assert X.state_distance([1, 0], [0, 1]) == pytest.approx(np.sqrt(2))
+
+
+def test_experiment_csv(tmp_path):
+    from paper_2411_09982_b200 import experiments as X
+
+    p = tmp_path / "out.csv"
+    X.write_csv(p, ["a", "b"], [{"a": 1, "b": 0.1}, {"a": 2, "b": 1e-300}])
+    assert p.read_text() == "a,b\n1,0.1\n2,1e-300\n"
