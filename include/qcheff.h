@@ -218,6 +218,17 @@ int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, int64_t K, i
                                 int64_t S, double t_start, double t_end, int64_t M, int order, const void* h_psi0,
                                 void* h_traj, int check, int64_t* bad_index, double* h_times, void* stream);
 
+/* Fixed-step RK4 comparator (reference.py:11-65): psi' = -i H(t) psi with
+ * H(t) = H0 + sum_k u_k(t) H_k read off grid samples (2*steps | S-1), all
+ * steps in one call.  The operators come as ONE union-pattern CSR
+ * (d_indptr int64 (n+1), d_indices int32 (nnz), d_vals complex128
+ * (nnz, K+1): the H0 value then H_1..H_K at each stored position);
+ * d_sig (K, S) f64; d_traj (steps+1, n) receives psi0 and every step.
+ * Synchronous. */
+int qch_rk4_evolve_c128(const int64_t* d_indptr, const int* d_indices, const void* d_vals, int64_t n, int64_t K,
+                        const double* d_sig, int64_t S, double t_start, double t_end, int64_t steps,
+                        const void* d_psi0, void* d_traj, void* stream);
+
 /* ------------------------------------------------------------ GEMM ------- */
 
 /* Batched complex128 GEMM on the FP64 tensor pipe (DMMA, mma.sync f64):

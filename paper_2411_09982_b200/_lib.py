@@ -89,6 +89,8 @@ PROTOTYPES = {
          c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p],
     ),
     "qch_magnus_plan_workspace_bytes": (c_int64, [c_int64, c_int64]),
+    "qch_rk4_evolve_c128": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double,
+                                    c_double, c_int64, c_void_p, c_void_p, c_void_p]),
     "qch_magnus_plan_workspace_init": (c_int, [c_void_p, c_int64, c_int64, c_void_p]),
     "qch_magnus_evolve_plan_c128": (
         c_int,
