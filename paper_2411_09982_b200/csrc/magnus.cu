@@ -286,6 +286,103 @@ __global__ void __launch_bounds__(kChainThreads) chain_grid_kernel(const double2
   }
 }
 
+// The ordered product for N <= 64 in ONE CTA: the propagators stream
+// through a 3-stage shared-memory ring by TMA bulk copies (one
+// cp.async.bulk of n*n*16 contiguous bytes per interval, completion on an
+// mbarrier), so up to three intervals' propagators are in flight while the
+// state advances — one SM alone could not keep enough plain loads in flight
+// to cover HBM latency at one propagator per step.  Warp w owns rows
+// 8w..8w+7, lane l columns l and l+32; the state lives in shared memory.
+constexpr int kChainStages = 3;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(256) chain_cta64_kernel(const double2* __restrict__ u, int n, int64_t mb,
+                                                          const double2* __restrict__ psi_in,
+                                                          double2* __restrict__ traj_rows, int64_t m0,
+                                                          unsigned long long* bad_norm) {
+  extern __shared__ __align__(128) double2 s_ring[];  // kChainStages x n x n
+  __shared__ __align__(8) unsigned long long s_bar[kChainStages];
+  __shared__ double2 s_x[2][64];
+  __shared__ double s_nrm[2][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nn = (int64_t)n * n;
+  const unsigned bytes = (unsigned)(nn * sizeof(double2));
+  if (threadIdx.x < 64) s_x[0][threadIdx.x] = threadIdx.x < n ? psi_in[threadIdx.x] : make_double2(0.0, 0.0);
+  if (threadIdx.x >= 64 && threadIdx.x < 128) s_x[1][threadIdx.x - 64] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kChainStages; ++q)
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[q])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t m) {  // thread 0: propagator m into its stage
+    if (m >= mb) return;
+    const int q = (int)(m % kChainStages);
+    const unsigned bar = smem_u32(&s_bar[q]);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(s_ring + (int64_t)q * nn)),
+        "l"(u + m * nn), "r"(bytes), "r"(bar)
+        : "memory");
+  };
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kChainStages; ++q) issue(q);
+  for (int64_t m = 0; m < mb; ++m) {
+    const int q = (int)(m % kChainStages);
+    const unsigned par = (unsigned)((m / kChainStages) & 1);
+    asm volatile(
+        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(
+            smem_u32(&s_bar[q])),
+        "r"(par)
+        : "memory");
+    const double2* um = s_ring + (int64_t)q * nn;
+    const double2* x = s_x[m & 1];
+    const double2 x0 = x[lane], x1 = x[lane + 32];
+    double yr[8], yi[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int r = warp * 8 + k;
+      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+      if (r < n) {
+        if (lane < n) a0 = um[r * n + lane];
+        if (lane + 32 < n) a1 = um[r * n + lane + 32];
+      }
+      yr[k] = fma(a0.x, x0.x, fma(-a0.y, x0.y, fma(a1.x, x1.x, -a1.y * x1.y)));
+      yi[k] = fma(a0.x, x0.y, fma(a0.y, x0.x, fma(a1.x, x1.y, a1.y * x1.x)));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        yr[k] += __shfl_xor_sync(0xffffffffu, yr[k], off);
+        yi[k] += __shfl_xor_sync(0xffffffffu, yi[k], off);
+      }
+    if (lane == 0) {
+      double part = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int r = warp * 8 + k;
+        if (r < n) {
+          s_x[(m + 1) & 1][r] = make_double2(yr[k], yi[k]);
+          __stcg(traj_rows + m * n + r, make_double2(yr[k], yi[k]));
+          part += yr[k] * yr[k] + yi[k] * yi[k];
+        }
+      }
+      s_nrm[m & 1][warp] = part;
+    }
+    __syncthreads();  // stage q fully read; the new state visible
+    if (threadIdx.x == 0) {
+      issue(m + kChainStages);
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += s_nrm[m & 1][w];
+      if (!(fabs(sqrt(t) - 1.0) <= 1e-6)) atomicMin(bad_norm, (unsigned long long)(m0 + m));
+    }
+  }
+}
+
 // tr(U U^dag) = sum |U_ij|^2, one CTA per matrix (for |det U|, see below)
 __global__ void abs_sq_kernel(const double2* __restrict__ u, int64_t nn, double* __restrict__ out) {
   const double2* m = u + (int64_t)blockIdx.x * nn;
@@ -668,7 +765,21 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
         }
       }
       double2* traj_rows = (double2*)d_traj + (m0 + 1) * N;
-      {
+      if (N <= 64) {
+        void* pr = prof_begin("chain_cta64_kernel", st);
+        const size_t ring = sizeof(double2) * kChainStages * (size_t)N * N;
+        static bool attr64 = false;
+        if (!attr64) {
+          QCH_CUDA(cudaFuncSetAttribute(chain_cta64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(sizeof(double2) * kChainStages * 64 * 64)));
+          attr64 = true;
+        }
+        chain_cta64_kernel<<<1, 256, ring, st>>>(u, (int)N, cm, psi, traj_rows, m0, bad_norm);
+        prof_end(pr, st);
+        QCH_LAUNCH_CHECK("chain_cta64_kernel");
+        note_launch(1);
+        QCH_CUDA(cudaMemcpyAsync(psi, traj_rows + (cm - 1) * N, sizeof(double2) * N, cudaMemcpyDeviceToDevice, st));
+      } else {
         // rows per CTA: one CTA for small N, up to one per SM for large N
         static const int64_t gdiv = getenv("QCH_CHAIN_DIV") ? atoll(getenv("QCH_CHAIN_DIV")) : 1024;
         const int G = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), N * N / gdiv));
