@@ -707,6 +707,7 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
   // outnumber them (a block waits for its group, so the unfinished top group
   // must never hold every resident block)
   g.gshift = 5;
+  if (const char* e = getenv("QCH_GROUP_SHIFT")) g.gshift = std::max(0, std::min(5, atoi(e)));
   if (tiles > grid)  // static schedule: group <= grid suffices; dynamic: <= grid / 2
     while (g.gshift > 0 && (1 << g.gshift) > (g.sched_static ? grid : grid / 2)) --g.gshift;
   static const bool want_stats = getenv("QCH_MAGNUS_STATS") != nullptr;
