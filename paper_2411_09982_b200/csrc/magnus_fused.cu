@@ -98,7 +98,7 @@ struct FusedArgs {
   int sched_static;               // 1: static round-robin tiles (see the kernel), 0: dynamic grabbing
   int* done_ctr;                  // null: the caller zeroes the workspace per launch
   unsigned long long* flags_out;  // (2,) first non-unitary interval, first norm drift
-  unsigned long long* stats;  // non-null (QCH_MAGNUS_STATS): per-block phase cycles, see fused_print_stats
+  unsigned long long* stats;  // non-null (QCH_MAGNUS_STATS): per-block phase cycles, printed by fused_launch
 };
 
 // phase counters (thread 0 of each block, summed over the block's tiles):
