@@ -99,6 +99,7 @@ struct FusedArgs {
   int* done_ctr;                  // null: the caller zeroes the workspace per launch
   unsigned long long* flags_out;  // (2,) first non-unitary interval, first norm drift
   unsigned long long* stats;  // non-null (QCH_MAGNUS_STATS): per-block phase cycles, printed by fused_launch
+  unsigned long long* tstamp;  // non-null (QCH_MAGNUS_STATS=2): per tile globaltimer at window / prefix / end
 };
 
 // phase counters (thread 0 of each block, summed over the block's tiles):
@@ -444,6 +445,7 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
     if (stat && g.win > 0 && t_next < g.tile_end) prefetch(t_next, s_sig0 + (size_t)((it + 1) & 1) * wstride);
     mark(1);
     if (g.stats != nullptr && tid == 0) st_acc[0] += 1;
+    if (g.tstamp != nullptr && tid == 0) g.tstamp[t * 4 + 0] = gtimer();
     const int64_t n0 = t * kTile + (int64_t)tid * kR;
     SmallArgs gl = g.s;
     int64_t nbase = 0;
@@ -551,6 +553,7 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
     // tile's trajectory is formed and written
     if (!stat && g.win > 0 && tn < g.tile_end) prefetch(tn, s_sig0 + (size_t)((it + 1) & 1) * wstride);
     mark(4);
+    if (g.tstamp != nullptr && tid == 0) g.tstamp[t * 4 + 1] = gtimer();
     if (g.pex != nullptr) {
       // prefix mode: the thread's start = (P_{lane-1} X_warp) E_t psi_start,
       // with psi_start known only after the ranks' exchange
@@ -612,6 +615,10 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
     }
     __syncthreads();  // s_w / s_e / s_traj reuse
     mark(5);
+    if (g.tstamp != nullptr && tid == 0) {
+      g.tstamp[t * 4 + 2] = gtimer();
+      g.tstamp[t * 4 + 3] = blockIdx.x;
+    }
     t = tn;
   }
   if (g.done_ctr != nullptr) {
@@ -711,8 +718,15 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
   if (tiles > grid)  // static schedule: group <= grid suffices; dynamic: <= grid / 2
     while (g.gshift > 0 && (1 << g.gshift) > (g.sched_static ? grid : grid / 2)) --g.gshift;
   static const bool want_stats = getenv("QCH_MAGNUS_STATS") != nullptr;
+  static const bool want_ts = want_stats && atoi(getenv("QCH_MAGNUS_STATS")) >= 2;
   static unsigned long long* d_stats = nullptr;
+  static unsigned long long* d_ts = nullptr;
   g.stats = nullptr;
+  g.tstamp = nullptr;
+  if (want_ts && tiles <= 65536) {
+    if (d_ts == nullptr) QCH_CUDA(cudaMalloc(&d_ts, sizeof(unsigned long long) * 4 * 65536));
+    g.tstamp = d_ts;
+  }
   if (want_stats) {
     if (d_stats == nullptr) QCH_CUDA(cudaMalloc(&d_stats, sizeof(unsigned long long) * kStatW * 4096));
     if (grid <= 4096) g.stats = d_stats;
@@ -757,6 +771,17 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
     for (int b = 0; b < grid; ++b)
       for (int q = 0; q < 8; ++q) ld[q] += (double)h[b * kStatW + 12 + q];
     const double nl = ld[3] > 0 ? ld[3] : 1;
+    if (g.tstamp != nullptr) {  // per-tile timeline for tools/tstamp_view.py
+      std::vector<unsigned long long> ts((size_t)4 * tiles);
+      QCH_CUDA(cudaMemcpy(ts.data(), d_ts, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      if (FILE* f = fopen("gpurun_out/magnus_tstamp.csv", "w")) {
+        fprintf(f, "tile,block,window_ns,prefix_ns,end_ns\n");
+        for (int64_t q = 0; q < tiles; ++q)
+          fprintf(f, "%lld,%llu,%lld,%lld,%lld\n", (long long)q, ts[q * 4 + 3], (long long)(ts[q * 4] - t0),
+                  (long long)(ts[q * 4 + 1] - t0), (long long)(ts[q * 4 + 2] - t0));
+        fclose(f);
+      }
+    }
     fprintf(stderr,
             "[qch magnus stats] group leaders %.0f: scan %.0f, look-back %.0f, prefixes %.0f cycles; tile wait for "
             "prefix %.0f cycles\n",
@@ -804,6 +829,7 @@ void fused_carve(void* ws, int64_t N, int64_t M, int nlaunch, FusedArgs* g, int*
   g->gflag = *ctr + nlaunch;
   g->gcount = g->gflag + nt;
   g->sched_static = 0;
+  g->tstamp = nullptr;
   g->done_ctr = nullptr;  // set by the self-cleaning callers
   g->flags_out = nullptr;
   p += al(sizeof(int) * (3 * nt + nlaunch + 1));
