@@ -348,8 +348,12 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   QCH_CUDA(cudaGetDevice(&dev));
   QCH_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return QCH_ERR_UNSUPPORTED;
-  int G = sm_count();
-  if (const char* e = getenv("QCH_NPAD_COOP_CTAS")) G = std::max(1, std::min(G, atoi(e)));
+  // CTAs: the per-rotation time is mostly fixed latency (row reads, the
+  // record exchange), and every extra CTA adds a record to the exchange —
+  // measured: dim 1024 best at 16-32 CTAs (7.9 us/rot vs 9.9 at 148), dim
+  // 4096 at 32 (9.7 vs 11.2)
+  int G = std::max(16, std::min(sm_count(), n / 128));
+  if (const char* e = getenv("QCH_NPAD_COOP_CTAS")) G = std::max(1, std::min(sm_count(), atoi(e)));
   const int rows_per = (n + G - 1) / G;
   G = (n + rows_per - 1) / rows_per;
   const size_t smem = npad_coop_smem(n, rows_per);
