@@ -69,6 +69,7 @@ struct CoopArgs {
   long long pivot_cap;
   long long* out_applied;
   int* out_status;
+  long long* stats;  // non-null (QCH_NPAD_STATS): CTA 0 phase cycles [wait, combine, scalars, rotate, rescan, publish], rescans
 };
 
 __device__ __forceinline__ int ld_acq(const int* p) {
@@ -128,8 +129,17 @@ __device__ __forceinline__ Cand block_best_p(const Cand& c, Cand* s_part) {
   return b;
 }
 
-template <bool EK>
+constexpr int kClusterMax = 16;
+
+// CL: the G CTAs form ONE thread-block cluster; records travel through
+// distributed shared memory (each CTA writes its record into every CTA's
+// s_rec) and the per-rotation barrier is barrier.cluster (release/acquire at
+// cluster scope, which also orders the CTAs' global matrix writes) instead of
+// polling epoch-flagged records in global memory.
+template <bool EK, bool CL>
 __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid_constant__ CoopArgs a) {
+  namespace cg = cooperative_groups;
+  __shared__ CoopRec s_rec[CL ? 2 : 1][CL ? kClusterMax : 1];
   const int tid = threadIdx.x, lane = tid & 31;
   const int G = gridDim.x, g = blockIdx.x;
   const int n = a.n;
@@ -165,7 +175,15 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     Cand own = cand_none();
     for (int k = tid; k < nr; k += kCoopThreads) cand_take(own, s_row[k]);
     own = block_best_p(own, s_part);
-    if (tid == 0) {
+    if (CL) {
+      if (tid < G) {
+        CoopRec* r = cg::this_cluster().map_shared_rank(&s_rec[0][g], tid);
+        r->own = own;
+        r->pi = cand_none();
+        r->pj = cand_none();
+      }
+      cg::this_cluster().sync();
+    } else if (tid == 0) {
       a.rec[g].own = own;
       a.rec[g].pi = cand_none();
       a.rec[g].pj = cand_none();
@@ -174,17 +192,29 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     }
   }
 
+  long long cyc[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long ck = clock64();
+  auto tick = [&](int k) {
+    if (a.stats != nullptr) {
+      const long long c2 = clock64();
+      cyc[k] += c2 - ck;
+      ck = c2;
+    }
+  };
   while (true) {
     // ---- phase B: combine the records, pick the pivot (every CTA)
     // (waiting for every CTA's record of this epoch is the grid barrier: the
     // acquire makes each publisher's matrix writes visible)
-    CoopRec* rec = a.rec + (size_t)(applied & 1) * G;
-    if (tid < 32) {
-      for (int k = tid; k < G; k += 32)
-        while (ld_acq(&rec[k].epoch) != (int)applied) {
-        }
+    const CoopRec* rec = CL ? s_rec[applied & 1] : a.rec + (size_t)(applied & 1) * G;
+    if (!CL) {
+      if (tid < 32) {
+        for (int k = tid; k < G; k += 32)
+          while (ld_acq(&a.rec[(size_t)(applied & 1) * G + k].epoch) != (int)applied) {
+          }
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    tick(0);
     Cand cown = cand_none(), cpi = cand_none(), cpj = cand_none();
     for (int k = tid; k < G; k += kCoopThreads) {
       cown = rec[k].own;
@@ -212,6 +242,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       status = 1;
       break;
     }
+    tick(1);
     const int i = (int)(piv.cr >> 16), j = (int)(piv.cr & 0xffffu);
     if (g == 0 && tid == 0 && a.pivots != nullptr && applied < a.pivot_cap) {
       a.pivots[2 * applied] = i;
@@ -225,6 +256,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     givens_fast(v, hii, hjj, &c, &s);
     const Block2 blk = rotate_block(c, s, mkc(hii, 0.0), cconj(v), v, mkc(hjj, 0.0));
 
+    tick(2);
     // ---- phase A: own columns of rows i, j; mirrored columns = own rows
     if (tid == 0) s_nresc = 0;
     __syncthreads();
@@ -268,8 +300,10 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     s_dg[i] = blk.ii.re;  // every thread writes the same value
     s_dg[j] = blk.jj.re;
     __syncthreads();  // own rows' new entries written and visible to the CTA
+    tick(3);
     // rescans of own rows whose best sat in column i or j (whole CTA per row)
     const int nresc = s_nresc;
+    cyc[6] += nresc;
     for (int q = 0; q < nresc; ++q) {
       const int x = s_resc[q];
       const double2* __restrict__ row = h + (size_t)x * n;
@@ -306,6 +340,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       b = block_best_p(b, s_part);
       if (tid == 0) s_row[x - r0] = b;
     }
+    tick(4);
     // best over own rows other than i, j (their state arrives with the next phase B)
     Cand own = cand_none();
     for (int k = tid; k < nr; k += kCoopThreads) {
@@ -314,7 +349,15 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     }
     block_best3(own, ppi, ppj, s_part);
     ++applied;
-    if (tid == 0) {
+    if (CL) {
+      if (tid < G) {
+        CoopRec* r = cg::this_cluster().map_shared_rank(&s_rec[applied & 1][g], tid);
+        r->own = own;
+        r->pi = ppi;
+        r->pj = ppj;
+      }
+      cg::this_cluster().sync();  // release/acquire: records and matrix writes
+    } else if (tid == 0) {
       CoopRec* w = a.rec + (size_t)(applied & 1) * G + g;
       w->own = own;
       w->pi = ppi;
@@ -324,7 +367,10 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     }
     pi_row = i;
     pj_row = j;
+    tick(5);
   }
+  if (a.stats != nullptr && g == 0 && tid == 0)
+    for (int k = 0; k < 7; ++k) a.stats[k] = cyc[k];
   if (g == 0 && tid == 0) {
     *a.out_applied = applied;
     *a.out_status = status;
@@ -358,11 +404,44 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   G = (n + rows_per - 1) / rows_per;
   const size_t smem = npad_coop_smem(n, rows_per);
   if (smem > (size_t)max_smem_optin()) return QCH_ERR_UNSUPPORTED;
-  auto kern = ek ? npad_coop_kernel<true> : npad_coop_kernel<false>;
+  // one cluster of G <= 16 CTAs when the device can place it (QCH_NPAD_COOP_CLUSTER=0 disables)
+  const char* ce = getenv("QCH_NPAD_COOP_CLUSTER");
+  bool cl = (ce == nullptr || atoi(ce) != 0) && G <= kClusterMax;
+  auto kern = ek ? (cl ? npad_coop_kernel<true, true> : npad_coop_kernel<true, false>)
+                 : (cl ? npad_coop_kernel<false, true> : npad_coop_kernel<false, false>);
   QCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  QCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCoopThreads, smem));
-  if (per_sm < 1) return QCH_ERR_UNSUPPORTED;
+  if (cl) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      cl = false;
+    } else {
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = dim3(G);
+      qc.blockDim = dim3(kCoopThreads);
+      qc.dynamicSmemBytes = smem;
+      cudaLaunchAttribute qa;
+      qa.id = cudaLaunchAttributeClusterDimension;
+      qa.val.clusterDim.x = G;
+      qa.val.clusterDim.y = 1;
+      qa.val.clusterDim.z = 1;
+      qc.attrs = &qa;
+      qc.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)kern, &qc) != cudaSuccess || ncl < 1) {
+        cudaGetLastError();
+        cl = false;
+      }
+    }
+    if (!cl) {
+      kern = ek ? npad_coop_kernel<true, false> : npad_coop_kernel<false, false>;
+      QCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+  }
+  if (!cl) {
+    int per_sm = 0;
+    QCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCoopThreads, smem));
+    if (per_sm < 1) return QCH_ERR_UNSUPPORTED;
+  }
 
   void* ws = nullptr;
   ensure_pool();
@@ -383,10 +462,33 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   a.out_status = (int*)(a.out_applied + 1);
   a.pivots = pivots;
   a.pivot_cap = pivot_cap;
+  a.stats = nullptr;
+  static long long* d_cstats = nullptr;
+  if (getenv("QCH_NPAD_STATS")) {
+    if (d_cstats == nullptr) QCH_CUDA(cudaMalloc(&d_cstats, 8 * sizeof(long long)));
+    a.stats = d_cstats;
+  }
   QCH_CUDA(cudaMemsetAsync(ws, 0xff, sizeof(CoopRec) * 2 * G, st));  // epochs = -1
-  void* args[] = {&a};
   void* pr = prof_begin("npad_run_kernel", st);
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kCoopThreads), args, smem, st);
+  cudaError_t e;
+  if (cl) {
+    cudaLaunchConfig_t qc = {};
+    qc.gridDim = dim3(G);
+    qc.blockDim = dim3(kCoopThreads);
+    qc.dynamicSmemBytes = smem;
+    qc.stream = st;
+    cudaLaunchAttribute qa;
+    qa.id = cudaLaunchAttributeClusterDimension;
+    qa.val.clusterDim.x = G;
+    qa.val.clusterDim.y = 1;
+    qa.val.clusterDim.z = 1;
+    qc.attrs = &qa;
+    qc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&qc, kern, a);
+  } else {
+    void* args[] = {&a};
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kCoopThreads), args, smem, st);
+  }
   prof_end(pr, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -402,6 +504,15 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   QCH_CUDA(cudaStreamSynchronize(st));
   *applied = ap;
   *status = stt;
+  if (a.stats != nullptr && ap > 0) {
+    long long hs[7];
+    QCH_CUDA(cudaMemcpy(hs, a.stats, sizeof hs, cudaMemcpyDeviceToHost));
+    fprintf(stderr,
+            "[qch npad coop] G=%d cluster=%d: cycles/rotation wait %.0f combine %.0f scalars %.0f rotate %.0f "
+            "rescans %.0f (%.2f rows) publish %.0f\n",
+            G, cl ? 1 : 0, (double)hs[0] / ap, (double)hs[1] / ap, (double)hs[2] / ap, (double)hs[3] / ap,
+            (double)hs[4] / ap, (double)hs[6] / ap, (double)hs[5] / ap);
+  }
   return QCH_OK;
 }
 
