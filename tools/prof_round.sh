@@ -13,8 +13,10 @@ $NCU --set full --import-source on -k regex:npad_coop -s 1 -c 1 -o $O/npad4096 -
     python tools/prof_driver.py npad4096 2000 > $O/npad4096.out 2>&1
 $NCU --set full --import-source on -k regex:'copy_kernel|indptr_kernel' -s 2 -c 2 -o $O/givens -f \
     python tools/prof_driver.py givens 10000000 > $O/givens.out 2>&1
-$NCU --set full --import-source on -k regex:npad_rows -s 1 -c 1 -o $O/npad60 -f \
+$NCU --set full --import-source on -k regex:npad_full_warp -s 1 -c 1 -o $O/npad60 -f \
     python tools/prof_driver.py npad60 > $O/npad60.out 2>&1
 $NCU --set full --import-source on -k regex:zgemm -s 2 -c 2 -o $O/zgemm4096 -f \
     python tools/prof_driver.py magnus4096 > $O/zgemm4096.out 2>&1
+$NCU --set full --import-source on -k regex:chain_cta64 -s 1 -c 1 -o $O/midsize -f \
+    python tools/midsize_probe.py > $O/midsize.out 2>&1
 ls -la $O
