@@ -225,3 +225,28 @@ def test_host_call_times_are_linspace(E, t0, t1, m):
     g2 = E.ControlGrid(t0, t1, grid.signals)
     out = E.evolve(ch, g2, m, np.array([1, 0, 0], dtype=complex), order=1, check=False)
     np.testing.assert_array_equal(out.times, np.linspace(t0, t1, m + 1))
+
+
+@pytest.mark.parametrize("sub,k", [(1, 2), (2, 1), (4, 1), (8, 2), (16, 2), (5, 3)])
+def test_samples_per_interval_and_controls(E, sub, k):
+    # the fused kernel's window staging (sub*256+1 samples per control up to
+    # 24 KB), the fixed-SUB register path (sub = 4) and the unstaged global
+    # path (large windows), for 1-3 controls, orders 1 and 2, host and plan
+    rng = np.random.default_rng(100 * sub + k)
+
+    def herm(scale):
+        a = rng.standard_normal((3, 3)) + 1j * rng.standard_normal((3, 3))
+        return (a + a.conj().T) * scale
+
+    ch = E.ControlledHamiltonian(E.HermitianOperator(herm(0.5)), [E.HermitianOperator(herm(0.2)) for _ in range(k)])
+    m = 3001
+    grid = E.ControlGrid(0.0, 30.0, np.sin(np.outer(np.arange(1, k + 1), np.linspace(0, 9, m * sub + 1))))
+    psi0 = np.array([0.6, 0.8j, 0.0])
+    for order in (1, 2):
+        ref = _oracle(ch, grid, m, psi0, order)
+        got = E.evolve(ch, grid, m, psi0, order=order)
+        assert rel_fro(got.amplitudes, ref) <= 1e-10, (sub, k, order)
+        plan = E.EvolvePlan(ch, grid, m, psi0, order=order, check=True)
+        plan.run()
+        plan.check()
+        assert rel_fro(plan.run().cpu().numpy(), ref) <= 1e-10, (sub, k, order, "plan")
