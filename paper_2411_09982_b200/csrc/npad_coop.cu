@@ -95,27 +95,36 @@ __device__ __forceinline__ Cand warp_best(Cand c) {
   const int wl = warp_argmax(c);
   return (wl >= 0) ? shfl_cand_p(c, wl) : cand_none();
 }
-// three block-wide bests at once (every thread gets them; one barrier pair);
-// s_part: 3 * kCoopWarps entries
+// three block-wide bests at once (every thread gets them; one barrier pair):
+// per-warp bests, then warp 0 reduces the kCoopWarps partials of each with
+// a warp argmax (instead of a serial cross-warp chain in every thread);
+// s_part: 3 * kCoopWarps + 3 entries
 __device__ __forceinline__ void block_best3(Cand& a, Cand& b, Cand& c, Cand* s_part) {
   const Cand wa = warp_best(a), wb = warp_best(b), wc = warp_best(c);
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
+  const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  if (lane == 0) {
     s_part[w] = wa;
     s_part[kCoopWarps + w] = wb;
     s_part[2 * kCoopWarps + w] = wc;
   }
   __syncthreads();
-  a = s_part[0];
-  b = s_part[kCoopWarps];
-  c = s_part[2 * kCoopWarps];
-#pragma unroll
-  for (int k = 1; k < kCoopWarps; ++k) {
-    cand_take(a, s_part[k]);
-    cand_take(b, s_part[kCoopWarps + k]);
-    cand_take(c, s_part[2 * kCoopWarps + k]);
+  if (w == 0) {
+    Cand x = lane < kCoopWarps ? s_part[lane] : cand_none();
+    Cand y = lane < kCoopWarps ? s_part[kCoopWarps + lane] : cand_none();
+    Cand z = lane < kCoopWarps ? s_part[2 * kCoopWarps + lane] : cand_none();
+    x = warp_best(x);
+    y = warp_best(y);
+    z = warp_best(z);
+    if (lane == 0) {
+      s_part[3 * kCoopWarps] = x;
+      s_part[3 * kCoopWarps + 1] = y;
+      s_part[3 * kCoopWarps + 2] = z;
+    }
   }
   __syncthreads();
+  a = s_part[3 * kCoopWarps];
+  b = s_part[3 * kCoopWarps + 1];
+  c = s_part[3 * kCoopWarps + 2];
 }
 // block-wide best (every thread gets it); s_part: kCoopWarps entries
 __device__ __forceinline__ Cand block_best_p(const Cand& c, Cand* s_part) {
@@ -141,6 +150,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
   namespace cg = cooperative_groups;
   __shared__ CoopRec s_rec[CL ? 2 : 1][CL ? kClusterMax : 1];
   const int tid = threadIdx.x, lane = tid & 31;
+  const int warp_u = __shfl_sync(0xffffffffu, tid >> 5, 0);  // provably warp-uniform (converged shuffles)
   const int G = gridDim.x, g = blockIdx.x;
   const int n = a.n;
   constexpr bool ek = EK;
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
   double* s_dg = (double*)smem;                  // full diagonal copy
   Cand* s_row = (Cand*)(smem + (((size_t)8 * n + 15) & ~(size_t)15));  // best candidate of each own row
   Cand* s_part = s_row + a.rows_per;             // [kCoopWarps] reduction scratch
-  int* s_resc = (int*)(s_part + 3 * kCoopWarps);  // own rows to rescan
+  int* s_resc = (int*)(s_part + 3 * kCoopWarps + 3);  // own rows to rescan
   __shared__ int s_nresc;
   double2* __restrict__ h = a.h;
 
@@ -215,13 +225,29 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       __syncthreads();
     }
     tick(0);
+    // the G records are reduced by warp 0 alone (one barrier; a block-wide
+    // reduction of at most G <= 148 records cost two barriers and a serial
+    // cross-warp combine in every thread)
     Cand cown = cand_none(), cpi = cand_none(), cpj = cand_none();
-    for (int k = tid; k < G; k += kCoopThreads) {
-      cown = rec[k].own;
-      cpi = rec[k].pi;
-      cpj = rec[k].pj;
+    if (warp_u == 0) {
+      for (int k = lane; k < G; k += 32) {
+        cand_take(cown, rec[k].own);
+        cand_take(cpi, rec[k].pi);
+        cand_take(cpj, rec[k].pj);
+      }
+      cown = warp_best(cown);
+      cpi = warp_best(cpi);
+      cpj = warp_best(cpj);
+      if (lane == 0) {
+        s_part[0] = cown;
+        s_part[1] = cpi;
+        s_part[2] = cpj;
+      }
     }
-    block_best3(cown, cpi, cpj, s_part);
+    __syncthreads();
+    cown = s_part[0];
+    cpi = s_part[1];
+    cpj = s_part[2];
     // the new candidates of the last rotation's rows i, j (their owners keep them)
     if (pi_row >= r0 && pi_row < r1 && tid == 0) s_row[pi_row - r0] = cpi;
     if (pj_row >= r0 && pj_row < r1 && tid == 0) s_row[pj_row - r0] = cpj;
@@ -380,7 +406,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
 }  // namespace
 
 size_t npad_coop_smem(int n, int rows_per) {
-  return (((size_t)8 * n + 15) & ~(size_t)15) + sizeof(Cand) * (rows_per + 3 * kCoopWarps) + (size_t)4 * rows_per + 64;
+  return (((size_t)8 * n + 15) & ~(size_t)15) + sizeof(Cand) * (rows_per + 3 * kCoopWarps + 3) + (size_t)4 * rows_per +
+         64;
 }
 
 // Run the greedy full-diagonal chain of ONE bitwise-Hermitian matrix on the
@@ -394,11 +421,14 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   QCH_CUDA(cudaGetDevice(&dev));
   QCH_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   if (!coop) return QCH_ERR_UNSUPPORTED;
-  // CTAs: the per-rotation time is mostly fixed latency (row reads, the
-  // record exchange), and every extra CTA adds a record to the exchange —
-  // measured: dim 1024 best at 16-32 CTAs (7.9 us/rot vs 9.9 at 148), dim
-  // 4096 at 32 (9.7 vs 11.2)
-  int G = std::max(16, std::min(sm_count(), n / 128));
+  // CTAs: the per-rotation time is mostly fixed latency (row reads, block
+  // reductions, the record exchange), and every extra CTA adds a record to the
+  // exchange.  Best measured: one 16-CTA cluster (records through DSMEM,
+  // barrier.cluster) — dim 1024 5.6 us/rot, dim 4096 6.6 us/rot (32 CTAs
+  // with global records: 7.9; 148: 11.2).  Without cluster support: n/128.
+  int G = std::min(kClusterMax, std::max(1, n / 64));
+  if (const char* ce = getenv("QCH_NPAD_COOP_CLUSTER"); ce != nullptr && atoi(ce) == 0)
+    G = std::max(16, std::min(sm_count(), n / 128));
   if (const char* e = getenv("QCH_NPAD_COOP_CTAS")) G = std::max(1, std::min(sm_count(), atoi(e)));
   const int rows_per = (n + G - 1) / G;
   G = (n + rows_per - 1) / rows_per;
