@@ -45,7 +45,7 @@ namespace {
 
 constexpr int kCoopThreads = 256;
 constexpr int kCoopWarps = kCoopThreads / 32;
-constexpr int kRescanBatch = 8;  // loads in flight per thread in a row rescan
+constexpr int kRescanBatch = 16;  // loads in flight per thread in a row rescan (a dim-4096 row in one batch)
 
 struct CoopRec {
   Cand own;   // best over the CTA's rows other than i, j
