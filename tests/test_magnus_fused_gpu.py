@@ -250,3 +250,17 @@ def test_samples_per_interval_and_controls(E, sub, k):
         plan.run()
         plan.check()
         assert rel_fro(plan.run().cpu().numpy(), ref) <= 1e-10, (sub, k, order, "plan")
+
+
+@pytest.mark.parametrize("m", [1, 2, 255, 256, 257, 8191, 8193])
+def test_interval_counts_around_tiles(E, m):
+    # partial tiles, single-tile groups, exactly one tile, one group boundary
+    ch, grid = E.driven_transmon(3, intervals=m, sub=4, t_final=0.05 * m)
+    psi0 = np.array([1, 0, 0], dtype=complex)
+    ref = _oracle(ch, grid, m, psi0, 2)
+    assert rel_fro(E.evolve(ch, grid, m, psi0, order=2).amplitudes, ref) <= 1e-10
+    plan = E.EvolvePlan(ch, grid, m, psi0, order=2, check=True)
+    for _ in range(2):
+        out = plan.run()
+    plan.check()
+    assert rel_fro(out.cpu().numpy(), ref) <= 1e-10
