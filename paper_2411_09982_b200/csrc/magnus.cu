@@ -44,12 +44,15 @@ int shard_finish(int64_t N, int64_t M, void* d_work, const double2* d_psi_start,
 __global__ void coeff_kernel(CoefArgs a, int order, double* __restrict__ c1, double* __restrict__ c2) {
   int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (n >= a.M) return;
-  double l1[kMaxK], l2[kMaxK + kMaxK * (kMaxK - 1) / 2];
-  interval_coeffs(a, n, order, l1, l2);
-  for (int k = 0; k < a.K; ++k) c1[n * a.K + k] = l1[k];
+  // one coefficient at a time (any number of controls): the same operation
+  // order as interval_coeffs — first order, then alpha_k, then beta_kl (k<l)
+  for (int k = 0; k < a.K; ++k) c1[n * a.K + k] = coef1(a, n, k);
   if (order >= 2) {
-    int nc = a.K + a.K * (a.K - 1) / 2;
-    for (int k = 0; k < nc; ++k) c2[n * nc + k] = l2[k];
+    const int nc = a.K + a.K * (a.K - 1) / 2;
+    for (int k = 0; k < a.K; ++k) c2[n * nc + k] = coef_alpha(a, n, k);
+    int q = a.K;
+    for (int k = 0; k < a.K; ++k)
+      for (int l = k + 1; l < a.K; ++l, ++q) c2[n * nc + q] = coef_beta(a, n, k, l);
   }
 }
 
@@ -87,20 +90,38 @@ __global__ void assemble_kernel(const double2* __restrict__ h0, const double2* _
                                 const double* __restrict__ c2, int64_t m0, int64_t mb, double dt_int, int order,
                                 double2* __restrict__ out) {
   const int ncomm = K + K * (K - 1) / 2;
+  if (K <= kMaxK) {  // operator entries held in registers
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
+      cplx d = d2c(h0[e]);
+      cplx ops[kMaxK];
+      for (int k = 0; k < K; ++k) ops[k] = d2c(hk[k * nn + e]);
+      cplx cm[kMaxK + kMaxK * (kMaxK - 1) / 2];
+      if (order >= 2)
+        for (int q = 0; q < ncomm; ++q) cm[q] = d2c(comm[q * nn + e]);
+      for (int64_t m = 0; m < mb; ++m) {
+        const int64_t gm = m0 + m;
+        cplx v = np_rmul(dt_int, d);
+        for (int k = 0; k < K; ++k) v = cadd(v, np_rmul(c1[gm * K + k], ops[k]));
+        if (order >= 2) {
+          cplx x = mkc(0, 0);
+          for (int q = 0; q < ncomm; ++q) x = cadd(x, np_rmul(c2[gm * ncomm + q], cm[q]));
+          v = cadd(v, np_cmul(mkc(0.0, -0.5), x));
+        }
+        out[m * nn + e] = c2d(v);
+      }
+    }
+    return;
+  }
+  // any number of controls: operator entries re-read (cached) per interval
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
-    cplx d = d2c(h0[e]);
-    cplx ops[kMaxK];
-    for (int k = 0; k < K; ++k) ops[k] = d2c(hk[k * nn + e]);
-    cplx cm[kMaxK + kMaxK * (kMaxK - 1) / 2];
-    if (order >= 2)
-      for (int q = 0; q < ncomm; ++q) cm[q] = d2c(comm[q * nn + e]);
+    const cplx d = d2c(h0[e]);
     for (int64_t m = 0; m < mb; ++m) {
       const int64_t gm = m0 + m;
       cplx v = np_rmul(dt_int, d);
-      for (int k = 0; k < K; ++k) v = cadd(v, np_rmul(c1[gm * K + k], ops[k]));
+      for (int k = 0; k < K; ++k) v = cadd(v, np_rmul(c1[gm * K + k], d2c(__ldg(hk + k * nn + e))));
       if (order >= 2) {
         cplx x = mkc(0, 0);
-        for (int q = 0; q < ncomm; ++q) x = cadd(x, np_rmul(c2[gm * ncomm + q], cm[q]));
+        for (int q = 0; q < ncomm; ++q) x = cadd(x, np_rmul(c2[gm * ncomm + q], d2c(__ldg(comm + q * nn + e))));
         v = cadd(v, np_cmul(mkc(0.0, -0.5), x));
       }
       out[m * nn + e] = c2d(v);
@@ -543,7 +564,6 @@ extern "C" int qch_magnus_coefficients(const double* d_sig, int64_t K, int64_t S
   if (M < 1) return fail(QCH_ERR_GRID, "need at least one interval");
   if ((S - 1) % M) return fail(QCH_ERR_GRID, std::to_string(M) + " intervals do not divide " + std::to_string(S - 1) +
                                                  " sample steps");
-  if (K > kMaxK) return fail(QCH_ERR_UNSUPPORTED, "at most 8 control channels");
   if (K == 0) return QCH_OK;
   CoefArgs a{d_sig, (int)K, S, M, (int)((S - 1) / M), dt};
   cudaStream_t st = (cudaStream_t)stream;
@@ -583,7 +603,6 @@ extern "C" int qch_magnus_commutators_c128(const void* d_h0, const void* d_hk, i
 extern "C" int qch_magnus_assemble_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
                                         const double* d_c1, const double* d_c2, int64_t m0, int64_t mb, double dt_int,
                                         int order, void* d_hbar, void* stream) {
-  if (K > kMaxK) return fail(QCH_ERR_UNSUPPORTED, "at most 8 control channels");
   cudaStream_t st = (cudaStream_t)stream;
   assemble_kernel<<<grid_for(N * N), 256, 0, st>>>((const double2*)d_h0, (const double2*)d_hk,
                                                     (const double2*)d_comm, (int)K, N * N, d_c1, d_c2, m0, mb, dt_int,
@@ -686,15 +705,16 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
   if (M < 1) return fail(QCH_ERR_GRID, "need at least one interval");
   if ((S - 1) % M)
     return fail(QCH_ERR_GRID, std::to_string(M) + " intervals do not divide " + std::to_string(S - 1) + " sample steps");
-  if (K > kMaxK) return fail(QCH_ERR_UNSUPPORTED, "at most 8 control channels");
   if (order != 1 && order != 2) return fail(QCH_ERR_VALUE, "order must be 1 or 2");
+  if (K > kMaxK && d_work != nullptr)
+    return fail(QCH_ERR_UNSUPPORTED, "replayed (plan) evolve: at most 8 control channels");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nn = N * N;
   const int ncomm = (int)(K + K * (K - 1) / 2);
   const double dt = (t_end - t_start) / (double)(S - 1);  // ControlGrid.dt, magnus.py:87-88
   const double dt_int = (t_end - t_start) / (double)M;     // magnus.py:199
   CoefArgs ca{d_sig, (int)K, S, M, (int)((S - 1) / M), dt};
-  if (N <= 4) {
+  if (N <= 4 && K <= kMaxK) {  // the fused single-pass kernel; more controls take the generic path
     SmallArgs g;
     g.ca = ca;
     g.h0 = (const double2*)d_h0;
@@ -715,7 +735,7 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
   QCH_CUDA(cudaMemsetAsync(bad_u, 0xff, sizeof(unsigned long long) * 2, st));
   DevBuf comm(st);
   const void* d_comm = d_comm_in;
-  if (order >= 2 && ncomm > 0 && d_comm == nullptr && N > 4) {
+  if (order >= 2 && ncomm > 0 && d_comm == nullptr) {  // (the fused path forms its own)
     QCH_CUDA(comm.alloc(sizeof(double2) * nn * ncomm));
     if (int rc = qch_magnus_commutators_c128(d_h0, d_hk, K, N, comm.p, stream)) return rc;
     d_comm = comm.p;
@@ -826,7 +846,8 @@ extern "C" int qch_magnus_evolve_async_c128(const void* d_h0, const void* d_hk, 
                                             int64_t N, const double* d_sig, int64_t S, double t_start, double t_end,
                                             int64_t M, int order, const void* d_psi0, void* d_traj, void* d_props,
                                             int check, void* d_flags, void* stream) {
-  if (N > 4) return fail(QCH_ERR_UNSUPPORTED, "asynchronous evolve: N <= 4 (fused pipeline)");
+  if (N > 4 || K > kMaxK)
+    return fail(QCH_ERR_UNSUPPORTED, "asynchronous evolve: N <= 4 and at most 8 controls (fused pipeline)");
   return magnus_evolve_impl(d_h0, d_hk, d_comm, K, N, d_sig, S, t_start, t_end, M, order, d_psi0, d_traj, d_props,
                             check, nullptr, (unsigned long long*)d_flags, stream);
 }

@@ -1158,7 +1158,6 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   if (M < 1) return fail(QCH_ERR_GRID, "need at least one interval");
   if ((S - 1) % M)
     return fail(QCH_ERR_GRID, std::to_string(M) + " intervals do not divide " + std::to_string(S - 1) + " sample steps");
-  if (K > 8) return fail(QCH_ERR_UNSUPPORTED, "at most 8 control channels");
   if (order != 1 && order != 2) return fail(QCH_ERR_VALUE, "order must be 1 or 2");
   if (N < 1) return fail(QCH_ERR_VALUE, "dimension must be at least 1");
   cudaStream_t st = (cudaStream_t)stream;
@@ -1167,7 +1166,7 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   const int64_t Kd = std::max<int64_t>(K, 1);
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
 
-  if (N > 4) {  // generic path: upload, device evolve, download
+  if (N > 4 || K > kMaxK) {  // generic path: upload, device evolve, download
     FBuf dev(st);
     const size_t b_ops = al(sizeof(double2) * nn * (1 + Kd)), b_psi = al(sizeof(double2) * N),
                  b_sig = al(sizeof(double) * Kd * S), b_traj = al(sizeof(double2) * N * (M + 1));

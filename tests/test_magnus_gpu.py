@@ -166,3 +166,29 @@ def test_zgemm_dmma_vs_numpy(E):
         _lib.call("qch_zgemm_batched", _lib.dptr(da), _lib.dptr(db), _lib.dptr(dc), m, n, k, b, m * k, k * n, m * n,
                   _lib.stream_ptr())
         assert rel_fro(dc.cpu().numpy(), a @ bb) <= 1e-14
+
+
+@pytest.mark.parametrize("n,k", [(3, 10), (6, 9)])
+def test_many_controls_generic_path(E, n, k):
+    # more than 8 controls: the fused kernel's limit; these take the generic
+    # device path (coefficients one at a time, assembly without register
+    # arrays) — reference semantics for any K
+    rng = np.random.default_rng(10 * n + k)
+
+    def herm(scale):
+        a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        return (a + a.conj().T) * scale
+
+    ch = E.ControlledHamiltonian(E.HermitianOperator(herm(0.5)), [E.HermitianOperator(herm(0.05)) for _ in range(k)])
+    m, sub = 200, 3
+    grid = E.ControlGrid(0.0, 10.0, np.cos(np.outer(np.arange(1, k + 1), np.linspace(0, 4, m * sub + 1))))
+    psi0 = np.zeros(n, complex)
+    psi0[0] = 1
+    d0 = ch.drift.data
+    ctr = np.stack([c.data for c in ch.controls])
+    for order in (1, 2):
+        ref = magnus_oracle.evolve(d0, ctr, grid.signals, grid.t_start, grid.t_end, m, psi0, order=order)
+        got = E.evolve(ch, grid, m, psi0, order=order)
+        assert rel_fro(got.amplitudes, ref) <= 1e-10
+    np.testing.assert_array_equal(E.magnus_coefficients(grid, m),
+                                  magnus_oracle.first_order_coefficients(grid.signals, grid.t_start, grid.t_end, m))
