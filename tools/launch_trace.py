@@ -1,3 +1,5 @@
+"""Launch-call timing of the fused Magnus kernel (device path, then host-buffer
+path): QCH_TRACE=1 python tools/launch_trace.py"""
 import sys, numpy as np, torch
 sys.path.insert(0, "/root/repo")
 import paper_2411_09982_b200 as eff

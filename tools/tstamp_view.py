@@ -1,3 +1,5 @@
+"""Print a few rows of the per-tile timeline written by QCH_MAGNUS_STATS=2
+(gpurun_out/magnus_tstamp.csv): window landed, prefix known, tile done (us)."""
 import numpy as np
 d = np.genfromtxt('gpurun_out/magnus_tstamp.csv', delimiter=',', names=True)
 w, p, e = d['window_ns']/1e3, d['prefix_ns']/1e3, d['end_ns']/1e3
