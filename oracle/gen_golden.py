@@ -129,11 +129,47 @@ def experiment_cases(eff) -> None:
     np.savez_compressed(GOLD / "experiments.npz", **out)
 
 
+def large_cases(eff) -> None:
+    """12. The reference itself at the BASELINE sizes: config 4 sweep points
+    (dim 1024, subspace mode, to convergence) and the first rotations of
+    config 3 (dim 4096, full mode).  Stored: pivots, counts, the final
+    diagonal and a few final rows (the full matrices are 16 / 256 MiB)."""
+    sys.path.insert(0, str(ROOT))
+    from paper_2411_09982_b200 import models as M
+
+    out = {}
+    pts = M.sweep_points(32, 32)
+    tgt = M.sweep_target(256)
+    for k, idx in enumerate((0, 31, 1023)):
+        wq, al, wr, g = pts[idx]
+        h = M.transmon_resonator_hamiltonian(4, 256, omega_q=wq, alpha=al, omega_r=wr, g=g).data
+        st, piv = _logged_run(eff, eff.HermitianOperator(h), tgt, tol=1e-12)
+        fin = st.current.data
+        out[f"sweep{k}_point"] = pts[idx]
+        out[f"sweep{k}_pivots"] = piv
+        out[f"sweep{k}_applied"] = st.applied
+        out[f"sweep{k}_converged"] = st.converged
+        out[f"sweep{k}_diag"] = np.real(np.diag(fin)).copy()
+        out[f"sweep{k}_rows"] = fin[[0, 4, 256, 700]].copy()
+        print("sweep point", idx, st.applied, st.converged, flush=True)
+    h = M.transmon_resonator_hamiltonian(4, 1024).data
+    st, piv = _logged_run(eff, eff.HermitianOperator(h), tol=1e-12, max_iter=60)
+    fin = st.current.data
+    out["c3_pivots"] = piv
+    out["c3_applied"] = st.applied
+    out["c3_diag"] = np.real(np.diag(fin)).copy()
+    rows = sorted({int(r) for r in piv.ravel()[:6]} | {0, 4095})
+    out["c3_rows_idx"] = np.array(rows)
+    out["c3_rows"] = fin[rows].copy()
+    print("config 3 first", st.applied, "rotations", flush=True)
+    np.savez_compressed(GOLD / "npad_large_ref.npz", **out)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg/src")
     ap.add_argument("--only", default=None,
-                    help="'sparse' / 'experiments': regenerate only those vectors")
+                    help="'sparse' / 'experiments' / 'large': regenerate only those vectors")
     args = ap.parse_args()
     eff = _import_reference(args.ref)
     sys.path.insert(0, str(ROOT))
@@ -145,6 +181,9 @@ def main() -> None:
         return
     if args.only == "experiments":
         experiment_cases(eff)
+        return
+    if args.only == "large":
+        large_cases(eff)
         return
 
     # 1. NPAD config 1: transmon 3 x resonator 20, full mode, tol 1e-12
