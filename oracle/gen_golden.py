@@ -164,6 +164,17 @@ def large_cases(eff) -> None:
     print("config 3 first", st.applied, "rotations", flush=True)
     np.savez_compressed(GOLD / "npad_large_ref.npz", **out)
 
+    # config 2 at full size, order 1 (the reference has no second order):
+    # every 1000th trajectory row and the last one
+    ch, grid = M.driven_transmon(3, intervals=100_000, sub=4)
+    rch = eff.ControlledHamiltonian(eff.HermitianOperator(ch.drift.data),
+                                    [eff.HermitianOperator(c.data) for c in ch.controls])
+    rgrid = eff.ControlGrid(grid.t_start, grid.t_end, grid.signals)
+    tr = eff.evolve(rch, rgrid, 100_000, np.array([1, 0, 0], dtype=complex), check=False)
+    np.savez_compressed(GOLD / "magnus_config2_order1_ref.npz", rows=tr.amplitudes[::1000].copy(),
+                        last=tr.amplitudes[-1].copy(), times=tr.times[::1000].copy())
+    print("config 2 order 1 reference trajectory sampled", flush=True)
+
 
 def main() -> None:
     ap = argparse.ArgumentParser()

@@ -264,3 +264,17 @@ def test_interval_counts_around_tiles(E, m):
         out = plan.run()
     plan.check()
     assert rel_fro(out.cpu().numpy(), ref) <= 1e-10
+
+
+def test_config2_full_size_order1_vs_reference_itself(E):
+    # BASELINE config 2 workload at order 1 against the reference's own evolve
+    # (tests/golden/magnus_config2_order1_ref.npz: every 1000th row)
+    from pathlib import Path
+
+    g = np.load(Path(__file__).parent / "golden" / "magnus_config2_order1_ref.npz")
+    m = 100_000
+    ch, grid = E.driven_transmon(3, intervals=m, sub=4)
+    got = E.evolve(ch, grid, m, np.array([1, 0, 0], dtype=complex), order=1, check=False)
+    assert rel_fro(got.amplitudes[::1000], g["rows"]) <= 1e-10
+    assert rel_fro(got.amplitudes[-1], g["last"]) <= 1e-10
+    np.testing.assert_array_equal(got.times[::1000], g["times"])
