@@ -175,6 +175,21 @@ def large_cases(eff) -> None:
                         last=tr.amplitudes[-1].copy(), times=tr.times[::1000].copy())
     print("config 2 order 1 reference trajectory sampled", flush=True)
 
+    # config 5 (12-spin Heisenberg chain, dim 4096): the first 2 of its 4096
+    # intervals, order 1 (36.7 s per interval on the reference)
+    ch5 = M.heisenberg_chain_hamiltonians(12)
+    full = M.synthetic_transfer_pulse(25.0, 4096 * 8 + 1, seed=7)
+    sig5 = full.signals[:, : 2 * 8 + 1]
+    rch5 = eff.ControlledHamiltonian(eff.HermitianOperator(ch5.drift.data),
+                                     [eff.HermitianOperator(c.data) for c in ch5.controls])
+    rgrid5 = eff.ControlGrid(0.0, 25.0 * 2 / 4096, sig5)
+    psi5 = np.zeros(4096, dtype=complex)
+    psi5[0] = 1.0
+    tr5 = eff.evolve(rch5, rgrid5, 2, psi5, check=False)
+    np.savez_compressed(GOLD / "magnus_config5_first2_ref.npz", traj=tr5.amplitudes, signals=sig5,
+                        t_end=25.0 * 2 / 4096)
+    print("config 5 first 2 intervals", flush=True)
+
 
 def main() -> None:
     ap = argparse.ArgumentParser()

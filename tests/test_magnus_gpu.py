@@ -192,3 +192,17 @@ def test_many_controls_generic_path(E, n, k):
         assert rel_fro(got.amplitudes, ref) <= 1e-10
     np.testing.assert_array_equal(E.magnus_coefficients(grid, m),
                                   magnus_oracle.first_order_coefficients(grid.signals, grid.t_start, grid.t_end, m))
+
+
+def test_config5_first_intervals_vs_reference_itself(E):
+    # BASELINE config 5 (12-spin Heisenberg chain, dim 4096) through the DMMA
+    # path: its first 2 intervals at order 1 against the reference's evolve
+    from pathlib import Path
+
+    g = np.load(Path(__file__).parent / "golden" / "magnus_config5_first2_ref.npz")
+    ch = E.heisenberg_chain_hamiltonians(12)
+    grid = E.ControlGrid(0.0, float(g["t_end"]), g["signals"])
+    psi0 = np.zeros(4096, dtype=complex)
+    psi0[0] = 1.0
+    got = E.evolve(ch, grid, 2, psi0, order=1, check=True)
+    assert rel_fro(got.amplitudes, g["traj"]) <= 1e-10
