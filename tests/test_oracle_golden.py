@@ -83,3 +83,25 @@ def test_sparse_rotation_oracle_bit_exact(golden):
     same(m, csr("rnd_out", n))
     out = npad_oracle.eliminate_sparse(sps.csr_matrix(g["can_dense"]), 0, 1)
     same(out, csr("can_out", 3))
+
+
+def test_npad_oracle_at_baseline_sizes(golden):
+    # the oracle against the reference itself at config-4 / config-3 sizes
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from paper_2411_09982_b200 import models as M
+
+    g = golden("npad_large_ref")
+    tgt = M.sweep_target(256)
+    k = 0  # the 148-rotation point (the others: tests/test_npad_large_ref_gpu.py)
+    wq, al, wr, gg = g[f"sweep{k}_point"]
+    h = M.transmon_resonator_hamiltonian(4, 256, omega_q=wq, alpha=al, omega_r=wr, g=gg).data
+    ref = npad_oracle.run_incremental(h, tgt, tol=1e-12)
+    np.testing.assert_array_equal(ref["pivots"], g[f"sweep{k}_pivots"])
+    np.testing.assert_array_equal(np.real(np.diag(ref["h"])), g[f"sweep{k}_diag"])
+    h = M.transmon_resonator_hamiltonian(4, 1024).data
+    ref = npad_oracle.run_incremental(h, tol=1e-12, max_iter=int(g["c3_applied"]))
+    np.testing.assert_array_equal(ref["pivots"], g["c3_pivots"])
+    np.testing.assert_array_equal(ref["h"][g["c3_rows_idx"]], g["c3_rows"])
