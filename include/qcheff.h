@@ -131,6 +131,18 @@ int qch_npad_sparse_entries_c128(const int64_t* d_indptr, const int32_t* d_indic
 
 int qch_build_transmon_resonator_c128(void* d_h, int64_t batch, int64_t n_q, int64_t n_r,
                                       const double* d_params, void* stream);
+/* spin_chain_hamiltonians (models.py:288-325), the drift built on the device
+ * as a CSR: d_indptr (2^L + 1) int64, d_indices / d_data (capacity 2^L; the
+ * diagonal's exact zeros are not stored, as scipy's diags -> csr drops them),
+ * *nnz (host) = stored entries.  1 <= length <= 30.  Synchronous. */
+int qch_build_spin_chain_drift_c128(int64_t length, double qubit_freq, double j_nn, double g_nnn,
+                                    int64_t* d_indptr, int32_t* d_indices, void* d_data, int64_t* nnz,
+                                    void* stream);
+/* The chain's global controls sum_j sx_j and sum_j sy_j (models.py:311-320)
+ * on the device: two CSRs of L 2^L entries each, sorted columns.
+ * Asynchronous. */
+int qch_build_global_xy_c128(int64_t length, int64_t* d_indptr_x, int32_t* d_indices_x, void* d_data_x,
+                             int64_t* d_indptr_y, int32_t* d_indices_y, void* d_data_y, void* stream);
 
 /* -------------------------------------------------------------- Magnus --- */
 

@@ -78,6 +78,10 @@ PROTOTYPES = {
     "qch_npad_sparse_select_c128": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int, c_void_p,
                                             c_void_p]),
     "qch_build_ladder_csr_c128": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "qch_build_spin_chain_drift_c128": (c_int, [c_int64, c_double, c_double, c_double, c_void_p, c_void_p, c_void_p,
+                                                P_int64, c_void_p]),
+    "qch_build_global_xy_c128": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                         c_void_p]),
     "qch_npad_sparse_entries_c128": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p,
                                              c_void_p]),
     "qch_peak_kernel": (c_int, [c_int, c_int, c_int, c_void_p, ctypes.POINTER(c_double), c_void_p]),
