@@ -34,7 +34,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "npad_run.h"
 #include "npad_select.cuh"
@@ -44,6 +46,7 @@ namespace qch {
 namespace {
 
 constexpr int kCoopThreads = 256;
+constexpr int kMaxCoopCtas = 1024;  // stats buffer rows (G <= SM count)
 constexpr int kCoopWarps = kCoopThreads / 32;
 constexpr int kRescanBatch = 16;  // loads in flight per thread in a row rescan (a dim-4096 row in one batch)
 
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     }
   }
 
-  long long cyc[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long ck = clock64();
   auto tick = [&](int k) {
     if (a.stats != nullptr) {
@@ -374,6 +377,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       if (x != i && x != j) cand_take(own, s_row[k]);
     }
     block_best3(own, ppi, ppj, s_part);
+    tick(7);
     ++applied;
     if (CL) {
       if (tid < G) {
@@ -395,8 +399,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     pj_row = j;
     tick(5);
   }
-  if (a.stats != nullptr && g == 0 && tid == 0)
-    for (int k = 0; k < 7; ++k) a.stats[k] = cyc[k];
+  if (a.stats != nullptr && tid == 0)
+    for (int k = 0; k < 8; ++k) a.stats[8 * g + k] = cyc[k];
   if (g == 0 && tid == 0) {
     *a.out_applied = applied;
     *a.out_status = status;
@@ -495,7 +499,7 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   a.stats = nullptr;
   static long long* d_cstats = nullptr;
   if (getenv("QCH_NPAD_STATS")) {
-    if (d_cstats == nullptr) QCH_CUDA(cudaMalloc(&d_cstats, 8 * sizeof(long long)));
+    if (d_cstats == nullptr) QCH_CUDA(cudaMalloc(&d_cstats, 8 * kMaxCoopCtas * sizeof(long long)));
     a.stats = d_cstats;
   }
   QCH_CUDA(cudaMemsetAsync(ws, 0xff, sizeof(CoopRec) * 2 * G, st));  // epochs = -1
@@ -535,13 +539,21 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   *applied = ap;
   *status = stt;
   if (a.stats != nullptr && ap > 0) {
-    long long hs[7];
-    QCH_CUDA(cudaMemcpy(hs, a.stats, sizeof hs, cudaMemcpyDeviceToHost));
-    fprintf(stderr,
-            "[qch npad coop] G=%d cluster=%d: cycles/rotation wait %.0f combine %.0f scalars %.0f rotate %.0f "
-            "rescans %.0f (%.2f rows) publish %.0f\n",
-            G, cl ? 1 : 0, (double)hs[0] / ap, (double)hs[1] / ap, (double)hs[2] / ap, (double)hs[3] / ap,
-            (double)hs[4] / ap, (double)hs[6] / ap, (double)hs[5] / ap);
+    std::vector<long long> hs(8 * (size_t)G);
+    QCH_CUDA(cudaMemcpy(hs.data(), a.stats, hs.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    // CTA 0, then the max over CTAs of each phase (the slowest CTA sets the barrier)
+    for (int row = 0; row < 2; ++row) {
+      double v[8];
+      for (int k = 0; k < 8; ++k) {
+        v[k] = (double)hs[k] / ap;
+        if (row == 1)
+          for (int q = 1; q < G; ++q) v[k] = std::max(v[k], (double)hs[8 * q + k] / ap);
+      }
+      fprintf(stderr,
+              "[qch npad coop] G=%d cluster=%d %s: cycles/rotation wait %.0f combine %.0f scalars %.0f rotate %.0f "
+              "rescans %.0f (%.2f rows) own-best %.0f publish %.0f\n",
+              G, cl ? 1 : 0, row == 0 ? "CTA 0" : "max  ", v[0], v[1], v[2], v[3], v[4], v[6], v[7], v[5]);
+    }
   }
   return QCH_OK;
 }
