@@ -228,11 +228,13 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       __syncthreads();
     }
     tick(0);
-    // the G records are reduced by warp 0 alone (one barrier; a block-wide
-    // reduction of at most G <= 148 records cost two barriers and a serial
-    // cross-warp combine in every thread)
+    // global records: the G records are reduced by warp 0 alone (one
+    // barrier; a block-wide reduction of at most G <= 148 records cost two
+    // barriers and a serial cross-warp combine in every thread).  Cluster
+    // (G <= 16 records in shared memory): every warp reduces them itself —
+    // identical results, no barrier, no broadcast
     Cand cown = cand_none(), cpi = cand_none(), cpj = cand_none();
-    if (warp_u == 0) {
+    if (CL || warp_u == 0) {
       for (int k = lane; k < G; k += 32) {
         cand_take(cown, rec[k].own);
         cand_take(cpi, rec[k].pi);
@@ -241,16 +243,18 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       cown = warp_best(cown);
       cpi = warp_best(cpi);
       cpj = warp_best(cpj);
-      if (lane == 0) {
+      if (!CL && lane == 0) {
         s_part[0] = cown;
         s_part[1] = cpi;
         s_part[2] = cpj;
       }
     }
-    __syncthreads();
-    cown = s_part[0];
-    cpi = s_part[1];
-    cpj = s_part[2];
+    if (!CL) {
+      __syncthreads();
+      cown = s_part[0];
+      cpi = s_part[1];
+      cpj = s_part[2];
+    }
     // the new candidates of the last rotation's rows i, j (their owners keep them)
     if (pi_row >= r0 && pi_row < r1 && tid == 0) s_row[pi_row - r0] = cpi;
     if (pj_row >= r0 && pj_row < r1 && tid == 0) s_row[pj_row - r0] = cpj;
