@@ -98,11 +98,11 @@ __device__ __forceinline__ Cand warp_best(Cand c) {
   const int wl = warp_argmax(c);
   return (wl >= 0) ? shfl_cand_p(c, wl) : cand_none();
 }
-// three block-wide bests at once (every thread gets them; one barrier pair):
-// per-warp bests, then warp 0 reduces the kCoopWarps partials of each with
-// a warp argmax (instead of a serial cross-warp chain in every thread);
-// s_part: 3 * kCoopWarps + 3 entries
-__device__ __forceinline__ void block_best3(Cand& a, Cand& b, Cand& c, Cand* s_part) {
+// three block-wide bests at once for the publish step, where only warp 0
+// (the record writers) needs them: per-warp bests, then warp 0 reduces the
+// kCoopWarps partials of each with a warp argmax — one barrier, no broadcast;
+// s_part: 3 * kCoopWarps entries
+__device__ __forceinline__ void block_best3_w0(Cand& a, Cand& b, Cand& c, Cand* s_part) {
   const Cand wa = warp_best(a), wb = warp_best(b), wc = warp_best(c);
   const int w = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   if (lane == 0) {
@@ -115,19 +115,10 @@ __device__ __forceinline__ void block_best3(Cand& a, Cand& b, Cand& c, Cand* s_p
     Cand x = lane < kCoopWarps ? s_part[lane] : cand_none();
     Cand y = lane < kCoopWarps ? s_part[kCoopWarps + lane] : cand_none();
     Cand z = lane < kCoopWarps ? s_part[2 * kCoopWarps + lane] : cand_none();
-    x = warp_best(x);
-    y = warp_best(y);
-    z = warp_best(z);
-    if (lane == 0) {
-      s_part[3 * kCoopWarps] = x;
-      s_part[3 * kCoopWarps + 1] = y;
-      s_part[3 * kCoopWarps + 2] = z;
-    }
+    a = warp_best(x);
+    b = warp_best(y);
+    c = warp_best(z);
   }
-  __syncthreads();
-  a = s_part[3 * kCoopWarps];
-  b = s_part[3 * kCoopWarps + 1];
-  c = s_part[3 * kCoopWarps + 2];
 }
 // block-wide best (every thread gets it); s_part: kCoopWarps entries
 __device__ __forceinline__ Cand block_best_p(const Cand& c, Cand* s_part) {
@@ -370,8 +361,18 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
         }
       }
       if (!EK && bx >= 0) b = make_cand(bv, ((unsigned)bx << 16) | (unsigned)x, ek);
-      b = block_best_p(b, s_part);
-      if (tid == 0) s_row[x - r0] = b;
+      // block best; only thread 0 (the writer of the row state) folds the
+      // warp partials, in the same order as block_best_p
+      b = warp_best(b);
+      if (lane == 0) s_part[tid >> 5] = b;
+      __syncthreads();
+      if (tid == 0) {
+        Cand rb = s_part[0];
+#pragma unroll
+        for (int k = 1; k < kCoopWarps; ++k) cand_take(rb, s_part[k]);
+        s_row[x - r0] = rb;
+      }
+      __syncthreads();
     }
     tick(4);
     // best over own rows other than i, j (their state arrives with the next phase B)
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       const int x = r0 + k;
       if (x != i && x != j) cand_take(own, s_row[k]);
     }
-    block_best3(own, ppi, ppj, s_part);
+    block_best3_w0(own, ppi, ppj, s_part);  // valid in warp 0: the record writers
     tick(7);
     ++applied;
     if (CL) {
