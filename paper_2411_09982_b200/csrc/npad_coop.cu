@@ -224,34 +224,38 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     // barriers and a serial cross-warp combine in every thread).  Cluster
     // (G <= 16 records in shared memory): every warp reduces them itself —
     // identical results, no barrier, no broadcast
-    Cand cown = cand_none(), cpi = cand_none(), cpj = cand_none();
+    // The pivot is the best of ALL record entries (one warp argmax); the new
+    // states of the last rotation's rows i, j (the combined pi / pj partials)
+    // are reduced only by the CTAs that own those rows.
+    const bool own_pi = pi_row >= r0 && pi_row < r1, own_pj = pj_row >= r0 && pj_row < r1;  // CTA-uniform
+    Cand piv = cand_none(), cpi = cand_none(), cpj = cand_none();
     if (CL || warp_u == 0) {
       for (int k = lane; k < G; k += 32) {
-        cand_take(cown, rec[k].own);
-        cand_take(cpi, rec[k].pi);
-        cand_take(cpj, rec[k].pj);
+        const Cand ro = rec[k].own, rpi = rec[k].pi, rpj = rec[k].pj;
+        cand_take(piv, ro);
+        cand_take(piv, rpi);
+        cand_take(piv, rpj);
+        if (own_pi) cand_take(cpi, rpi);
+        if (own_pj) cand_take(cpj, rpj);
       }
-      cown = warp_best(cown);
-      cpi = warp_best(cpi);
-      cpj = warp_best(cpj);
+      piv = warp_best(piv);
+      if (own_pi) cpi = warp_best(cpi);
+      if (own_pj) cpj = warp_best(cpj);
       if (!CL && lane == 0) {
-        s_part[0] = cown;
+        s_part[0] = piv;
         s_part[1] = cpi;
         s_part[2] = cpj;
       }
     }
     if (!CL) {
       __syncthreads();
-      cown = s_part[0];
+      piv = s_part[0];
       cpi = s_part[1];
       cpj = s_part[2];
     }
     // the new candidates of the last rotation's rows i, j (their owners keep them)
-    if (pi_row >= r0 && pi_row < r1 && tid == 0) s_row[pi_row - r0] = cpi;
-    if (pj_row >= r0 && pj_row < r1 && tid == 0) s_row[pj_row - r0] = cpj;
-    Cand piv = cown;
-    cand_take(piv, cpi);
-    cand_take(piv, cpj);
+    if (own_pi && tid == 0) s_row[pi_row - r0] = cpi;
+    if (own_pj && tid == 0) s_row[pj_row - r0] = cpj;
     if (!(piv.q > 0.0) || [&] {
           if (ek) return piv.q < a.threshold;
           const double t2 = a.threshold * a.threshold;
