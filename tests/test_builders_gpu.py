@@ -65,3 +65,35 @@ def test_spin_chain_device_evolve_matches_host(E):
     a = E.evolve(E.spin_chain_hamiltonians_device(p), grid, 512, psi0, order=2).amplitudes
     b = E.evolve(E.spin_chain_hamiltonians(p), grid, 512, psi0, order=2).amplitudes
     assert rel_fro(a, b) <= 1e-13
+
+
+@pytest.mark.parametrize("length", [1, 2, 3])
+def test_spin_chain_c_abi_short_chains(E, length):
+    # the C-ABI accepts 1 <= L <= 30 (SpinChainParams needs L >= 3): the
+    # reference's numpy expressions (models.py:302-320) stated directly
+    import ctypes
+
+    import scipy.sparse as sps
+    import torch
+
+    from paper_2411_09982_b200 import _lib
+
+    w, jn, g2 = 0.7, 0.4, -0.25
+    n = 1 << length
+    idx = np.arange(n, dtype=np.int64)
+    z = 1 - 2 * ((idx[:, None] >> np.arange(length)) & 1)
+    diag = 0.5 * w * z.sum(axis=1) - jn * (z * np.roll(z, -1, axis=1)).sum(axis=1) \
+        - g2 * (z * np.roll(z, -2, axis=1)).sum(axis=1)
+    want = sps.diags(diag.astype(np.complex128), format="csr")
+    ip = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    ix = torch.empty(n, dtype=torch.int32, device="cuda")
+    dv = torch.empty(n, dtype=torch.complex128, device="cuda")
+    nnz = ctypes.c_int64(-1)
+    _lib.call("qch_build_spin_chain_drift_c128", length, w, jn, g2, _lib.dptr(ip), _lib.dptr(ix), _lib.dptr(dv),
+              ctypes.byref(nnz), _lib.stream_ptr())
+    k = nnz.value
+    got = sps.csr_matrix((dv[:k].cpu().numpy(), ix[:k].cpu().numpy(), ip.cpu().numpy()), shape=(n, n))
+    _same(got, want)
+    with pytest.raises(ValueError):
+        _lib.call("qch_build_spin_chain_drift_c128", 31, w, jn, g2, _lib.dptr(ip), _lib.dptr(ix), _lib.dptr(dv),
+                  ctypes.byref(nnz), _lib.stream_ptr())
