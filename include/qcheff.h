@@ -134,7 +134,8 @@ int qch_build_transmon_resonator_c128(void* d_h, int64_t batch, int64_t n_q, int
 /* spin_chain_hamiltonians (models.py:288-325), the drift built on the device
  * as a CSR: d_indptr (2^L + 1) int64, d_indices / d_data (capacity 2^L; the
  * diagonal's exact zeros are not stored, as scipy's diags -> csr drops them),
- * *nnz (host) = stored entries.  1 <= length <= 30.  Synchronous. */
+ * *nnz (host) = stored entries.  1 <= length <= 30 (one CTA compacts the
+ * diagonal: sized for the dense-propagation chains, L <= 20).  Synchronous. */
 int qch_build_spin_chain_drift_c128(int64_t length, double qubit_freq, double j_nn, double g_nnn,
                                     int64_t* d_indptr, int32_t* d_indices, void* d_data, int64_t* nnz,
                                     void* stream);
