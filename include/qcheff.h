@@ -97,10 +97,6 @@ int qch_npad_run_batch_c128(void* d_h, int64_t batch, int64_t n, const int32_t* 
                             int64_t n_target, const double* d_thresholds, int64_t max_iter,
                             int64_t* d_applied, int32_t* d_converged, void* stream);
 
-/* Device-side builder of the transmon (x) resonator Hamiltonians of the NPAD
- * configs (SURVEY.md Appendix A.1): for each b, params[4b..4b+3] =
- * {omega_q, alpha, omega_r, g}; H = wq n + a/2 n(n-1) (x) I + I (x) wr a^dag a
- * + g (b + b^dag) (x) (a + a^dag), index q*n_r + k.  d_h: (batch, nq*nr)^2. */
 /* _conjugate_sparse (npad.py:148-232) on a device CSR (indptr int64 (n+1),
  * sorted int32 column indices, complex128 values, no explicit zeros): the
  * NEW CSR of U H U^dag for the rotation (i < j; c = cos_half and
@@ -129,6 +125,10 @@ int qch_build_ladder_csr_c128(int64_t n, int64_t* d_indptr, int32_t* d_indices, 
 int qch_npad_sparse_entries_c128(const int64_t* d_indptr, const int32_t* d_indices, const void* d_data, int64_t n,
                                  int64_t i, int64_t j, void* d_out, void* stream);
 
+/* Device-side builder of the transmon (x) resonator Hamiltonians of the NPAD
+ * configs (SURVEY.md Appendix A.1): for each b, params[4b..4b+3] =
+ * {omega_q, alpha, omega_r, g}; H = wq n + a/2 n(n-1) (x) I + I (x) wr a^dag a
+ * + g (b + b^dag) (x) (a + a^dag), index q*n_r + k.  d_h: (batch, nq*nr)^2. */
 int qch_build_transmon_resonator_c128(void* d_h, int64_t batch, int64_t n_q, int64_t n_r,
                                       const double* d_params, void* stream);
 /* spin_chain_hamiltonians (models.py:288-325), the drift built on the device
