@@ -289,6 +289,10 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     if (tid == 0) s_nresc = 0;
     __syncthreads();
     Cand ppi = cand_none(), ppj = cand_none();
+    // best over own rows other than i, j (their state arrives with the next
+    // phase B), folded as each row's state is finalised: here, or by thread 0
+    // after a rescan
+    Cand own = cand_none();
     for (int k = tid; k < nr; k += kCoopThreads) {
       const int x = r0 + k;
       if (x == i || x == j) continue;
@@ -311,6 +315,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
         if (i < x) cand_take(st, make_cand(c2d(cconj(ni)), ((unsigned)i << 16) | (unsigned)x, ek));
         if (j < x) cand_take(st, make_cand(c2d(cconj(nj)), ((unsigned)j << 16) | (unsigned)x, ek));
         s_row[k] = st;
+        cand_take(own, st);
       }
     }
     // the 2x2 block entries, by the owners of columns i and j
@@ -375,16 +380,11 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
 #pragma unroll
         for (int k = 1; k < kCoopWarps; ++k) cand_take(rb, s_part[k]);
         s_row[x - r0] = rb;
+        cand_take(own, rb);
       }
       __syncthreads();
     }
     tick(4);
-    // best over own rows other than i, j (their state arrives with the next phase B)
-    Cand own = cand_none();
-    for (int k = tid; k < nr; k += kCoopThreads) {
-      const int x = r0 + k;
-      if (x != i && x != j) cand_take(own, s_row[k]);
-    }
     block_best3_w0(own, ppi, ppj, s_part);  // valid in warp 0: the record writers
     tick(7);
     ++applied;
