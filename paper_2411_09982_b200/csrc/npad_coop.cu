@@ -385,18 +385,38 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       __syncthreads();
     }
     tick(4);
-    block_best3_w0(own, ppi, ppj, s_part);  // valid in warp 0: the record writers
-    tick(7);
-    ++applied;
     if (CL) {
-      if (tid < G) {
-        CoopRec* r = cg::this_cluster().map_shared_rank(&s_rec[applied & 1][g], tid);
-        r->own = own;
-        r->pi = ppi;
-        r->pj = ppj;
+      // per-warp bests, then warps 0, 1, 2 reduce own / pi / pj in parallel
+      // and each writes its field of the record into every CTA
+      const Cand wa = warp_best(own), wb = warp_best(ppi), wc = warp_best(ppj);
+      if (lane == 0) {
+        s_part[warp_u] = wa;
+        s_part[kCoopWarps + warp_u] = wb;
+        s_part[2 * kCoopWarps + warp_u] = wc;
+      }
+      __syncthreads();
+      tick(7);
+      ++applied;
+      if (warp_u < 3) {
+        Cand x = lane < kCoopWarps ? s_part[warp_u * kCoopWarps + lane] : cand_none();
+        x = warp_best(x);
+        if (lane < G) {
+          CoopRec* r = cg::this_cluster().map_shared_rank(&s_rec[applied & 1][g], lane);
+          if (warp_u == 0)
+            r->own = x;
+          else if (warp_u == 1)
+            r->pi = x;
+          else
+            r->pj = x;
+        }
       }
       cg::this_cluster().sync();  // release/acquire: records and matrix writes
-    } else if (tid == 0) {
+    } else {
+      block_best3_w0(own, ppi, ppj, s_part);  // valid in warp 0: the record writer
+      tick(7);
+      ++applied;
+    }
+    if (!CL && tid == 0) {
       CoopRec* w = a.rec + (size_t)(applied & 1) * G + g;
       w->own = own;
       w->pi = ppi;
