@@ -229,33 +229,51 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     // are reduced only by the CTAs that own those rows.
     const bool own_pi = pi_row >= r0 && pi_row < r1, own_pj = pj_row >= r0 && pj_row < r1;  // CTA-uniform
     Cand piv = cand_none(), cpi = cand_none(), cpj = cand_none();
-    if (CL || warp_u == 0) {
+    if (CL) {
+      // every warp finds the pivot; the row-i / row-j states are reduced by
+      // warps 1 and 2 of their owner CTAs, in parallel with the others
+      const bool red_i = own_pi && warp_u == 1, red_j = own_pj && warp_u == 2;  // warp-uniform
       for (int k = lane; k < G; k += 32) {
         const Cand ro = rec[k].own, rpi = rec[k].pi, rpj = rec[k].pj;
         cand_take(piv, ro);
         cand_take(piv, rpi);
         cand_take(piv, rpj);
-        if (own_pi) cand_take(cpi, rpi);
-        if (own_pj) cand_take(cpj, rpj);
+        if (red_i) cand_take(cpi, rpi);
+        if (red_j) cand_take(cpj, rpj);
       }
       piv = warp_best(piv);
-      if (own_pi) cpi = warp_best(cpi);
-      if (own_pj) cpj = warp_best(cpj);
-      if (!CL && lane == 0) {
-        s_part[0] = piv;
-        s_part[1] = cpi;
-        s_part[2] = cpj;
+      if (red_i) {
+        cpi = warp_best(cpi);
+        if (lane == 0) s_row[pi_row - r0] = cpi;
       }
-    }
-    if (!CL) {
+      if (red_j) {
+        cpj = warp_best(cpj);
+        if (lane == 0) s_row[pj_row - r0] = cpj;
+      }
+    } else {
+      if (warp_u == 0) {
+        for (int k = lane; k < G; k += 32) {
+          const Cand ro = rec[k].own, rpi = rec[k].pi, rpj = rec[k].pj;
+          cand_take(piv, ro);
+          cand_take(piv, rpi);
+          cand_take(piv, rpj);
+          if (own_pi) cand_take(cpi, rpi);
+          if (own_pj) cand_take(cpj, rpj);
+        }
+        piv = warp_best(piv);
+        if (own_pi) cpi = warp_best(cpi);
+        if (own_pj) cpj = warp_best(cpj);
+        if (lane == 0) {
+          s_part[0] = piv;
+          if (own_pi) s_row[pi_row - r0] = cpi;
+          if (own_pj) s_row[pj_row - r0] = cpj;
+        }
+      }
       __syncthreads();
       piv = s_part[0];
-      cpi = s_part[1];
-      cpj = s_part[2];
     }
-    // the new candidates of the last rotation's rows i, j (their owners keep them)
-    if (own_pi && tid == 0) s_row[pi_row - r0] = cpi;
-    if (own_pj && tid == 0) s_row[pj_row - r0] = cpj;
+    // (the new states of the last rotation's rows i, j are visible to the
+    // rotation pass after the barrier below)
     if (!(piv.q > 0.0) || [&] {
           if (ek) return piv.q < a.threshold;
           const double t2 = a.threshold * a.threshold;
