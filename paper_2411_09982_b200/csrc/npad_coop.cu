@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
   double* s_dg = (double*)smem;                  // full diagonal copy
   Cand* s_row = (Cand*)(smem + (((size_t)8 * n + 15) & ~(size_t)15));  // best candidate of each own row
   Cand* s_part = s_row + a.rows_per;             // [kCoopWarps] reduction scratch
-  int* s_resc = (int*)(s_part + 3 * kCoopWarps + 3);  // own rows to rescan
+  Cand* s_rpart = s_part + 3 * kCoopWarps + 3;    // [2][kCoopWarps] rescan partials (double-buffered)
+  int* s_resc = (int*)(s_rpart + 2 * kCoopWarps);  // own rows to rescan
   __shared__ int s_nresc;
   double2* __restrict__ h = a.h;
 
@@ -388,19 +389,23 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
         }
       }
       if (!EK && bx >= 0) b = make_cand(bv, ((unsigned)bx << 16) | (unsigned)x, ek);
-      // block best; only thread 0 (the writer of the row state) folds the
-      // warp partials, in the same order as block_best_p
+      // block best: warp partials, then warp 0 alone (lane 0 writes the row
+      // state).  The partials alternate between two buffers, so the next
+      // row's partials never overwrite ones warp 0 may still be reading and
+      // no trailing barrier is needed (the row state is read only after the
+      // record exchange)
+      Cand* rp = s_rpart + (q & 1) * kCoopWarps;
       b = warp_best(b);
-      if (lane == 0) s_part[tid >> 5] = b;
+      if (lane == 0) rp[tid >> 5] = b;
       __syncthreads();
-      if (tid == 0) {
-        Cand rb = s_part[0];
-#pragma unroll
-        for (int k = 1; k < kCoopWarps; ++k) cand_take(rb, s_part[k]);
-        s_row[x - r0] = rb;
-        cand_take(own, rb);
+      if (warp_u == 0) {
+        Cand rb = lane < kCoopWarps ? rp[lane] : cand_none();
+        rb = warp_best(rb);
+        if (lane == 0) {
+          s_row[x - r0] = rb;
+          cand_take(own, rb);
+        }
       }
-      __syncthreads();
     }
     tick(4);
     if (CL) {
@@ -457,7 +462,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
 }  // namespace
 
 size_t npad_coop_smem(int n, int rows_per) {
-  return (((size_t)8 * n + 15) & ~(size_t)15) + sizeof(Cand) * (rows_per + 3 * kCoopWarps + 3) + (size_t)4 * rows_per +
+  return (((size_t)8 * n + 15) & ~(size_t)15) + sizeof(Cand) * (rows_per + 5 * kCoopWarps + 3) + (size_t)4 * rows_per +
          64;
 }
 
