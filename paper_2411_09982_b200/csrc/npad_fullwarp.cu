@@ -60,6 +60,28 @@ __device__ __forceinline__ Cand warp_best(Cand c) {
   return shfl_cand(c, wl);
 }
 
+// two independent warp argmaxes with their REDUX / ballot steps interleaved
+// (same winners as two warp_best calls); the rare near-tie path stays exact
+__device__ __forceinline__ void warp_best2(Cand& c1, Cand& c2) {
+  const unsigned long long b1 = (c1.q > 0.0) ? (unsigned long long)__double_as_longlong(c1.q) : 0ull;
+  const unsigned long long b2 = (c2.q > 0.0) ? (unsigned long long)__double_as_longlong(c2.q) : 0ull;
+  const unsigned h1 = (unsigned)(b1 >> 32), h2 = (unsigned)(b2 >> 32);
+  const unsigned hm1 = __reduce_max_sync(kFull, h1), hm2 = __reduce_max_sync(kFull, h2);
+  const unsigned lm1 = __reduce_max_sync(kFull, (h1 == hm1) ? (unsigned)b1 : 0u);
+  const unsigned lm2 = __reduce_max_sync(kFull, (h2 == hm2) ? (unsigned)b2 : 0u);
+  const double qs1 = __longlong_as_double((long long)(((unsigned long long)hm1 << 32) | lm1));
+  const double qs2 = __longlong_as_double((long long)(((unsigned long long)hm2 << 32) | lm2));
+  const bool nf1 = (c1.q > 0.0) && (c1.q >= qs1 * (1.0 - kRel));
+  const bool nf2 = (c2.q > 0.0) && (c2.q >= qs2 * (1.0 - kRel));
+  const unsigned n1 = __ballot_sync(kFull, nf1), n2 = __ballot_sync(kFull, nf2);
+  int w1 = -1, w2 = -1;
+  if (hm1 != 0u) w1 = (__popc(n1) == 1) ? __ffs(n1) - 1 : warp_argmax_exact(c1.v, c1.m, c1.cr, nf1);
+  if (hm2 != 0u) w2 = (__popc(n2) == 1) ? __ffs(n2) - 1 : warp_argmax_exact(c2.v, c2.m, c2.cr, nf2);
+  const Cand o1 = shfl_cand(c1, w1 >= 0 ? w1 : 0), o2 = shfl_cand(c2, w2 >= 0 ? w2 : 0);
+  c1 = w1 >= 0 ? o1 : cand_none();
+  c2 = w2 >= 0 ? o2 : cand_none();
+}
+
 __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict__ jobs, NpadCommon2 cm) {
   extern __shared__ __align__(16) double2 hs[];  // n rows x kPitch
   NpadJob2* job = jobs + blockIdx.x;
@@ -172,8 +194,8 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       cyc[2] += c3 - c2;
     }
     // rows i, j: reduced from the fresh values
-    const Cand bi = warp_best(pi);
-    const Cand bj = warp_best(pj);
+    Cand bi = pi, bj = pj;
+    warp_best2(bi, bj);
     if (lane == (i & 31)) {
       if (i >> 5) rb[1] = bi;
       else rb[0] = bi;
@@ -191,25 +213,35 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       cyc[3] += c4 - c3;
       nresc += __popc(m0) + __popc(m1);
     }
-    while (m0 | m1) {
-      int r;
+    // two rows per pass (independent argmaxes, interleaved)
+    auto next_row = [&]() {
+      int r = -1;
       if (m0) {
         r = __ffs(m0) - 1;
         m0 &= m0 - 1;
-      } else {
+      } else if (m1) {
         r = __ffs(m1) - 1 + 32;
         m1 &= m1 - 1;
       }
-      Cand b = cand_none();
+      return r;
+    };
+    while (m0 | m1) {
+      const int r = next_row(), r2 = next_row();  // r2 = -1: one row left
+      Cand b = cand_none(), b2 = cand_none();
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int x = lane + 32 * q;
         if (x < r) cand_take(b, make_cand(hs[r * kPitch + x], ((unsigned)x << 16) | (unsigned)r, ek));
+        if (x < r2) cand_take(b2, make_cand(hs[r2 * kPitch + x], ((unsigned)x << 16) | (unsigned)r2, ek));
       }
-      const Cand br = warp_best(b);
+      warp_best2(b, b2);
       if (lane == (r & 31)) {
-        if (r >> 5) rb[1] = br;
-        else rb[0] = br;
+        if (r >> 5) rb[1] = b;
+        else rb[0] = b;
+      }
+      if (r2 >= 0 && lane == (r2 & 31)) {
+        if (r2 >> 5) rb[1] = b2;
+        else rb[0] = b2;
       }
     }
     ++applied;
