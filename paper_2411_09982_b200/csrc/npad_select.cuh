@@ -72,11 +72,12 @@ static __device__ __noinline__ bool cand_better_exact_v(double2 av, double am, u
 }
 
 // a strictly before b in the reference order (mag desc, c asc, r asc)
+// (none = q 0: 'a.q > b.q (1 + kRel)' already orders none below any
+// candidate and two nones as equal; one branch, taken only inside the band)
 __device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
-  if (!(a.q > 0.0)) return false;
-  if (!(b.q > 0.0)) return true;
-  if (a.q > b.q * (1.0 + kRel)) return true;
-  if (b.q > a.q * (1.0 + kRel)) return false;
+  const bool gt = a.q > b.q * (1.0 + kRel);
+  const bool lt = b.q > a.q * (1.0 + kRel);
+  if (gt || lt || !(a.q > 0.0) || !(b.q > 0.0)) return gt;
   return cand_better_exact_v(a.v, a.m, a.cr, b.v, b.m, b.cr);
 }
 
