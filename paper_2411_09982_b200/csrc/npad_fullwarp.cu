@@ -82,11 +82,13 @@ __device__ __forceinline__ void warp_best2(Cand& c1, Cand& c2) {
   c2 = w2 >= 0 ? o2 : cand_none();
 }
 
+// EK: exact-magnitude keys (compile-time, so make_cand carries no branch)
+template <bool EK>
 __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict__ jobs, NpadCommon2 cm) {
   extern __shared__ __align__(16) double2 hs[];  // n rows x kPitch
   NpadJob2* job = jobs + blockIdx.x;
   const int n = cm.n, lane = threadIdx.x;
-  const bool ek = cm.ek != 0;
+  constexpr bool ek = EK;
   double2* hg = job->h;
   double2* ug = job->u;
   for (int r = 0; r < n; ++r)
@@ -288,12 +290,17 @@ int npad_launch_full_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cuda
   const size_t smem = sizeof(double2) * (size_t)cm.n * kPitch;
   static bool attr = false;
   if (!attr) {
-    QCH_CUDA(cudaFuncSetAttribute(npad_full_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    QCH_CUDA(cudaFuncSetAttribute(npad_full_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double2) * kMaxN * kPitch)));
+    QCH_CUDA(cudaFuncSetAttribute(npad_full_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(double2) * kMaxN * kPitch)));
     attr = true;
   }
   void* pr = prof_begin("npad_run_kernel", st);
-  npad_full_warp_kernel<<<njobs, 32, smem, st>>>(jobs, cm);
+  if (cm.ek)
+    npad_full_warp_kernel<true><<<njobs, 32, smem, st>>>(jobs, cm);
+  else
+    npad_full_warp_kernel<false><<<njobs, 32, smem, st>>>(jobs, cm);
   prof_end(pr, st);
   QCH_LAUNCH_CHECK("npad_full_warp_kernel");
   note_launch(1);
