@@ -134,6 +134,15 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
     }
     const int i = (int)(piv.cr >> 16), j = (int)(piv.cr & 0xffffu);  // i < j
     const cplx v = d2c(piv.v);
+    // rows i, j of this lane's columns, loaded before the scalars' long
+    // sqrt / rsqrt chain so the loads overlap it
+    double2 ri2[2], rj2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int x = lane + 32 * q;
+      ri2[q] = x < n ? hs[i * kPitch + x] : make_double2(0.0, 0.0);
+      rj2[q] = x < n ? hs[j * kPitch + x] : make_double2(0.0, 0.0);
+    }
     const double hii = hs[i * kPitch + i].x, hjj = hs[j * kPitch + j].x;
     double c;
     cplx s;
@@ -155,7 +164,7 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       const int x = lane + 32 * q;
       if (x >= n || x == i || x == j) continue;
       cplx ni, nj;
-      rotate_rows(c, s, d2c(hs[i * kPitch + x]), d2c(hs[j * kPitch + x]), &ni, &nj);
+      rotate_rows(c, s, d2c(ri2[q]), d2c(rj2[q]), &ni, &nj);
       const cplx cxi = cconj(ni), cxj = cconj(nj);
       hs[i * kPitch + x] = c2d(ni);
       hs[j * kPitch + x] = c2d(nj);
