@@ -295,6 +295,13 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       a.pivots[2 * applied] = i;
       a.pivots[2 * applied + 1] = j;
     }
+    // this thread's first own column of rows i, j: issued before the scalars'
+    // sqrt / rsqrt chain so the global loads overlap it
+    double2 pre_i = make_double2(0.0, 0.0), pre_j = make_double2(0.0, 0.0);
+    if (tid < nr) {
+      pre_i = h[(size_t)i * n + r0 + tid];
+      pre_j = h[(size_t)j * n + r0 + tid];
+    }
     // rotation scalars and the 2x2 block: every thread, same values
     const cplx v = d2c(piv.v);
     const double hii = s_dg[i], hjj = s_dg[j];
@@ -315,7 +322,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     for (int k = tid; k < nr; k += kCoopThreads) {
       const int x = r0 + k;
       if (x == i || x == j) continue;
-      const cplx ri = d2c(h[(size_t)i * n + x]), rj = d2c(h[(size_t)j * n + x]);
+      const cplx ri = d2c(k == tid ? pre_i : h[(size_t)i * n + x]), rj = d2c(k == tid ? pre_j : h[(size_t)j * n + x]);
       cplx ni, nj;
       rotate_rows(c, s, ri, rj, &ni, &nj);
       h[(size_t)i * n + x] = c2d(ni);
