@@ -167,7 +167,8 @@ int qch_magnus_assemble_c128(const void* d_h0, const void* d_hk, const void* d_c
                              int order, void* d_hbar, void* stream);
 
 /* _expm_minus_i (expm.py:56-71) for a batch: U_b = exp(-i H_b), scaling and
- * squaring Taylor (degree <= 18, Paterson-Stockmeyer).  d_work: scratch of 4*batch*n*n complex128.
+ * squaring Taylor (degree <= 18; Hermitian batches as cos - i sin by
+ * Paterson-Stockmeyer on half (Hermitian) GEMMs).  d_work: scratch of 8*batch*n*n complex128.
  * Checks finiteness (expm.py:81-82, 97-99): QCH_ERR_NONFINITE, first bad
  * item index in *bad_index (host, nullable). */
 int qch_expm_minus_i_batch_c128(const void* d_h, int64_t batch, int64_t n, void* d_u, void* d_work,
@@ -249,6 +250,14 @@ int qch_rk4_evolve_c128(const int64_t* d_indptr, const int* d_indices, const voi
  * alias A or B. */
 int qch_zgemm_batched(const void* d_a, const void* d_b, void* d_c, int64_t m, int64_t n, int64_t k,
                       int64_t batch, int64_t stride_a, int64_t stride_b, int64_t stride_c, void* stream);
+
+/* C_b = A_b @ B_b for n x n factors whose product is Hermitian (commuting
+ * Hermitian factors, e.g. two polynomials of one Hermitian matrix — every
+ * product of the Hermitian exp(-iH) of expm.py:56-71): only the tiles meeting
+ * the lower triangle are computed, the upper triangle is written as the
+ * conjugate mirror (C is exactly Hermitian off the diagonal).  Contiguous
+ * batch (stride n*n). */
+int qch_zgemm_herm_batched(const void* d_a, const void* d_b, void* d_c, int64_t n, int64_t batch, void* stream);
 
 /* ------------------------------------------------ multi-GPU Magnus ------- */
 

@@ -110,6 +110,7 @@ PROTOTYPES = {
         c_int,
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p],
     ),
+    "qch_zgemm_herm_batched": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
 }
 
 QCH_OK = 0

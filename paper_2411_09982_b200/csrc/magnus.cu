@@ -23,15 +23,10 @@
 #include "qch_internal.h"
 #include "qch_math.cuh"
 #include "magnus_small.cuh"
+#include "zgemm.h"
 
 namespace qch {
 
-int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, int64_t batch, int64_t sa, int64_t sb,
-          int64_t sc, cudaStream_t st);
-int zgemm_taylor(const double2* a, const double2* b, double2* t, double2* o, int n, int64_t batch, double inv_k,
-                 cudaStream_t st);
-int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st);
-int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st);
 int fused_evolve_device(const SmallArgs& base, int64_t N, int64_t M, const double2* d_psi0, double2* d_traj,
                         int64_t* bad_index, unsigned long long* d_flags_out, cudaStream_t st, void* d_work);
 size_t fused_ws_bytes(int64_t N, int64_t M, int nlaunch);
@@ -467,6 +462,53 @@ struct DevBuf {
   }
 };
 
+
+// H bitwise Hermitian?  flag[b] |= 1 for any H[r][c] != conj(H[c][r]) (r > c)
+__global__ void herm_check_kernel(const double2* __restrict__ h, int n, int64_t batch, unsigned* __restrict__ flag) {
+  const int64_t nn = (int64_t)n * n;
+  const int64_t total = nn * batch;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = k / nn, e = k - b * nn;
+    const int r = (int)(e / n), c = (int)(e - (int64_t)r * n);
+    if (r <= c) continue;
+    const double2 x = h[k], y = h[b * nn + (int64_t)c * n + r];
+    if (!(x.x == y.x && x.y == -y.y)) flag[b] = 1u;
+  }
+}
+
+// hs = H * 2^-s_b
+__global__ void herm_scale_kernel(const double2* __restrict__ h, int64_t nn, int64_t batch,
+                                  const int* __restrict__ sarr, double2* __restrict__ hs) {
+  const int64_t total = nn * batch;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const double scl = ldexp(1.0, -sarr[k / nn]);
+    const double2 v = h[k];
+    hs[k] = make_double2(v.x * scl, v.y * scl);
+  }
+}
+
+// out = c0 I + sum_{i<np} c_{i+1} P_i  (elementwise)
+struct CombArgs {
+  const double2* p[4];
+  double c[5];
+  int np;
+};
+__global__ void comb_kernel(CombArgs a, int64_t nn, int n, int64_t batch, double2* __restrict__ out) {
+  const int64_t total = nn * batch;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = k % nn;
+    double xr = (e / n == e % n) ? a.c[0] : 0.0, xi = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < a.np) {
+        const double2 v = a.p[i][k];
+        xr = fma(a.c[i + 1], v.x, xr);
+        xi = fma(a.c[i + 1], v.y, xi);
+      }
+    out[k] = make_double2(xr, xi);
+  }
+}
+
 // exp(-i H) for a batch of n x n (n > 4) with the DMMA GEMM; d_u receives U.
 // work: 3*batch*n*n complex.  sarr: int[batch] (device).
 // exp(-i H) for a batch of n x n (n > 4) on the DMMA GEMM.  Same scaling as
@@ -478,32 +520,17 @@ struct DevBuf {
 //     X <- Q_j + a^3 X  (one GEMM with an accumulate epilogue per step)
 // i.e. 2 + m/3 GEMMs (6 at m = 12) instead of the reference's 17.
 // work: 4 * batch * n * n complex.  sarr: int[batch] (device).
-static int expm_generic(const double2* h, int64_t batch, int n, double2* u, double2* work, int* sarr,
-                        unsigned long long* norm, cudaStream_t st) {
+static int expm_ps(const double2* h, int64_t batch, int n, double2* u, double2* work, int* sarr,
+                   unsigned long long* norm, int m, int smax, cudaStream_t st) {
   const int64_t nn = (int64_t)n * n;
   double2* p1 = work;
   double2* p2 = work + batch * nn;
   double2* p3 = work + 2 * batch * nn;
   double2* xb = work + 3 * batch * nn;
-  QCH_CUDA(cudaMemsetAsync(norm, 0, sizeof(unsigned long long) * batch, st));
-  rownorm_kernel<<<(int)((n * batch + 127) / 128), 128, 0, st>>>(h, n, batch, norm);
+  (void)norm;
   taylor_init_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, n, batch, norm, p1, p2, u, sarr);
   QCH_LAUNCH_CHECK("taylor_init_kernel");
-  note_launch(2);
-  // degree from the scaled norms (one small D2H)
-  std::vector<unsigned long long> hn(batch);
-  std::vector<int> hs(batch);
-  QCH_CUDA(cudaMemcpyAsync(hn.data(), norm, sizeof(unsigned long long) * batch, cudaMemcpyDeviceToHost, st));
-  QCH_CUDA(cudaMemcpyAsync(hs.data(), sarr, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
-  QCH_CUDA(cudaStreamSynchronize(st));
-  int m = 1, smax = 0;
-  for (int64_t b = 0; b < batch; ++b) {
-    double nu;
-    memcpy(&nu, &hn[b], sizeof nu);
-    nu = ldexp(nu, -hs[b]);
-    m = std::max(m, taylor_degree(nu));
-    smax = std::max(smax, hs[b]);
-  }
+  note_launch(1);
   // powers a, a^2, a^3 (p1 holds a; taylor_init also left a in p2)
   if (m >= 2) {
     if (int rc = zgemm(p1, p1, p2, n, n, n, batch, nn, nn, nn, st)) return rc;
@@ -536,6 +563,145 @@ static int expm_generic(const double2* h, int64_t batch, int n, double2* u, doub
     note_launch(1);
   }
   return QCH_OK;
+}
+
+
+// exp(-i H) for a batch of Hermitian n x n (n > 4): with Hs = H / 2^s (the
+// reference's scaling, expm.py:58-63) and B = Hs^2,
+//     sum_{k<=m} (-i Hs)^k / k! = C(B) - i Hs T(B),
+//     C = sum_j (-1)^j B^j / (2j)!,   T = sum_j (-1)^j B^j / (2j+1)!,
+// the same truncated Taylor series as expm.py:64-68 (cut at the degree m whose
+// remainder is < 2^-56, kTheta), regrouped.  Every matrix product is of two
+// commuting Hermitian polynomials of Hs, so every product is Hermitian and
+// the GEMM computes only its lower-triangular tiles (zgemm_tma HERM): C and T
+// by Paterson-Stockmeyer in B with blocks B^q (q chosen to minimise GEMMs;
+// q = 3 and 6 half-GEMMs at the config-5 degree m = 12), the last GEMM's
+// epilogue forming U = C - i (Hs T) directly.  Then s squarings (full GEMMs).
+// work: 8 * batch * n * n complex.
+static int herm_gemm_count(int q, int dc, int dt) {
+  auto g = [q](int d) { return d < q ? 0 : (d % q == 0 ? d / q - 1 : d / q); };
+  return q + g(dc) + g(dt) + 1;
+}
+
+static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2* work, int* sarr, int m, int smax,
+                     cudaStream_t st) {
+  const int64_t nn = (int64_t)n * n;
+  double2* W[8];
+  for (int i = 0; i < 8; ++i) W[i] = work + i * batch * nn;
+  double2* hs = W[0];
+  double2* P[5] = {nullptr, W[1], W[2], W[3], W[4]};  // P[j] = B^j
+  herm_scale_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, nn, batch, sarr, hs);
+  QCH_LAUNCH_CHECK("herm_scale_kernel");
+  note_launch(1);
+  const int dc = m / 2, dt = (m - 1) / 2;
+  int q = 0;
+  if (std::max(dc, dt) >= 1) {
+    int best = 1 << 30;
+    for (int qq = 1; qq <= 4; ++qq) {
+      const int cst = herm_gemm_count(qq, dc, dt);
+      if (cst < best) best = cst, q = qq;
+    }
+    if (int rc = zgemm_herm(hs, hs, P[1], n, batch, st)) return rc;
+    for (int j = 2; j <= q; ++j)
+      if (int rc = zgemm_herm(P[j - 1], P[1], P[j], n, batch, st)) return rc;
+  }
+  double fac[20];
+  fac[0] = 1.0;
+  for (int k = 1; k < 20; ++k) fac[k] = fac[k - 1] * k;
+  auto comb = [&](double2* out, const double* coef, int deg) -> int {  // sum_{i<=deg} coef_i P_i
+    CombArgs a{};
+    a.c[0] = coef[0];
+    a.np = deg;
+    for (int i = 1; i <= deg; ++i) {
+      a.p[i - 1] = P[i];
+      a.c[i] = coef[i];
+    }
+    comb_kernel<<<grid_for(nn * batch), 256, 0, st>>>(a, nn, n, batch, out);
+    QCH_LAUNCH_CHECK("comb_kernel");
+    note_launch(1);
+    return QCH_OK;
+  };
+  // p(B) = sum_{i<=d} coef_i B^i by Paterson-Stockmeyer into one of bufs[0..1]
+  auto poly = [&](const double* coef, int d, double2* b0, double2* b1, double2** res) -> int {
+    double2* bufs[2] = {b0, b1};
+    int cur = 0;
+    if (d < q || q == 0) {
+      if (int rc = comb(bufs[0], coef, d)) return rc;
+      *res = bufs[0];
+      return QCH_OK;
+    }
+    const int r = d / q, rem = d - r * q;
+    int j;
+    if (rem == 0) {  // X = Q_{r-1} + coef_d B^q (elementwise)
+      double c5[5] = {0, 0, 0, 0, 0};
+      for (int i = 0; i < q; ++i) c5[i] = coef[(r - 1) * q + i];
+      c5[q] = coef[d];
+      if (int rc = comb(bufs[0], c5, q)) return rc;
+      j = r - 2;
+    } else {
+      if (int rc = comb(bufs[0], coef + r * q, rem)) return rc;
+      j = r - 1;
+    }
+    for (; j >= 0; --j) {  // X <- Q_j + B^q X
+      const double2* pp[4] = {P[1], P[2], P[3], P[4]};
+      double qc[5] = {0, 0, 0, 0, 0};
+      for (int i = 0; i < q; ++i) qc[i] = coef[j * q + i];
+      if (int rc = zgemm_qacc(true, P[q], bufs[cur], bufs[cur ^ 1], pp, qc, q - 1, n, batch, st)) return rc;
+      cur ^= 1;
+    }
+    *res = bufs[cur];
+    return QCH_OK;
+  };
+  double cc[20], tc[20];
+  for (int j = 0; j <= dc; ++j) cc[j] = ((j & 1) ? -1.0 : 1.0) / fac[2 * j];
+  for (int j = 0; j <= dt; ++j) tc[j] = ((j & 1) ? -1.0 : 1.0) / fac[2 * j + 1];
+  double2* C = nullptr;
+  double2* T = nullptr;
+  if (int rc = poly(cc, dc, W[5], W[6], &C)) return rc;
+  if (int rc = poly(tc, dt, W[7], C == W[5] ? W[6] : W[5], &T)) return rc;
+  if (int rc = zgemm_ufin(hs, T, C, u, n, batch, st)) return rc;
+  for (int step = 0; step < smax; ++step) {  // squarings (U is not Hermitian)
+    if (int rc = zgemm(u, u, W[1], n, n, n, batch, nn, nn, nn, st)) return rc;
+    select_square_kernel<<<grid_for(nn * batch), 256, 0, st>>>(u, W[1], nn, batch, sarr, step);
+    QCH_LAUNCH_CHECK("select_square_kernel");
+    note_launch(1);
+  }
+  return QCH_OK;
+}
+
+// Dispatcher: norms, scaling and degree as the reference (one small D2H);
+// bitwise-Hermitian batches take expm_herm, anything else expm_ps.
+// work: 8 * batch * n * n complex.  sarr: int[batch]; norm: u64[2 * batch].
+static int expm_generic(const double2* h, int64_t batch, int n, double2* u, double2* work, int* sarr,
+                        unsigned long long* norm, cudaStream_t st) {
+  const int64_t nn = (int64_t)n * n;
+  unsigned* hflag = (unsigned*)(norm + batch);
+  QCH_CUDA(cudaMemsetAsync(norm, 0, sizeof(unsigned long long) * 2 * batch, st));
+  rownorm_kernel<<<(int)((n * batch + 127) / 128), 128, 0, st>>>(h, n, batch, norm);
+  herm_check_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, n, batch, hflag);
+  QCH_LAUNCH_CHECK("herm_check_kernel");
+  note_launch(2);
+  std::vector<unsigned long long> hn(2 * batch);
+  QCH_CUDA(cudaMemcpyAsync(hn.data(), norm, sizeof(unsigned long long) * 2 * batch, cudaMemcpyDeviceToHost, st));
+  QCH_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> hs(batch);
+  int m = 1, smax = 0;
+  bool herm = true;
+  const unsigned* hf = (const unsigned*)(hn.data() + batch);
+  for (int64_t b = 0; b < batch; ++b) {
+    double nu;
+    memcpy(&nu, &hn[b], sizeof nu);
+    int s = 0;
+    if (nu > kScaleTarget) s = (int)ceil(log2(nu / kScaleTarget));
+    hs[b] = s;
+    m = std::max(m, taylor_degree(ldexp(nu, -s)));
+    smax = std::max(smax, s);
+    if (hf[b]) herm = false;
+  }
+  QCH_CUDA(cudaMemcpyAsync(sarr, hs.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, st));
+  static const bool force_ps = getenv("QCH_EXPM") && strcmp(getenv("QCH_EXPM"), "ps") == 0;
+  if (herm && !force_ps) return expm_herm(h, batch, n, u, work, sarr, m, smax, st);
+  return expm_ps(h, batch, n, u, work, sarr, norm, m, smax, st);
 }
 
 static int validate_generic(const double2* u, int64_t batch, int n, double2* scratch, double* dbuf,
@@ -628,7 +794,7 @@ extern "C" int qch_expm_minus_i_batch_c128(const void* d_h, int64_t batch, int64
   if (batch <= 0) return QCH_OK;
   cudaStream_t st = (cudaStream_t)stream;
   DevBuf flags(st);
-  QCH_CUDA(flags.alloc(sizeof(unsigned long long) * (1 + batch) + sizeof(int) * batch));
+  QCH_CUDA(flags.alloc(sizeof(unsigned long long) * (1 + 2 * batch) + sizeof(int) * batch));
   unsigned long long* bad = flags.as<unsigned long long>();
   QCH_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
   const int64_t nn = n * n;
@@ -644,7 +810,7 @@ extern "C" int qch_expm_minus_i_batch_c128(const void* d_h, int64_t batch, int64
     case 3: expm_small_kernel<3><<<blocks, 128, 0, st>>>(h, batch, u); break;
     case 4: expm_small_kernel<4><<<blocks, 128, 0, st>>>(h, batch, u); break;
     default: {
-      int* sarr = (int*)(bad + 1 + batch);
+      int* sarr = (int*)(bad + 1 + 2 * batch);
       return expm_generic(h, batch, (int)n, u, (double2*)d_work, sarr, bad + 1, st);
     }
   }
@@ -749,20 +915,20 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
     if (K > 0) {
       if (int rc = qch_magnus_coefficients(d_sig, K, S, M, dt, order, c1, c2, stream)) return rc;
     }
-    // chunk so that 6 matrices per interval (Hbar, U, 4 of expm work) stay within ~12 GiB
+    // chunk so that 10 matrices per interval (Hbar, U, 8 of expm work) stay within ~20 GiB
     const size_t per = sizeof(double2) * (size_t)nn;
-    int64_t mb = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)((12ull << 30) / (6 * per))));
+    int64_t mb = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)((20ull << 30) / (10 * per))));
     mb = std::min<int64_t>(mb, 4096);
     DevBuf buf(st);
-    QCH_CUDA(buf.alloc(per * mb * 6 + sizeof(double2) * N + sizeof(int) * mb + sizeof(unsigned long long) * mb +
+    QCH_CUDA(buf.alloc(per * mb * 10 + sizeof(double2) * N + sizeof(int) * mb + sizeof(unsigned long long) * 2 * mb +
                        sizeof(double) * 2 * mb + 64));
     double2* hbar = buf.as<double2>();
     double2* ubuf = hbar + nn * mb;
-    double2* work = ubuf + nn * mb;  // 4 * mb
-    double2* psi = work + 4 * nn * mb;
+    double2* work = ubuf + nn * mb;  // 8 * mb
+    double2* psi = work + 8 * nn * mb;
     int* sarr = (int*)(psi + N);
     unsigned long long* norms = (unsigned long long*)(sarr + mb + (mb & 1));
-    double* vbuf = (double*)(norms + mb);
+    double* vbuf = (double*)(norms + 2 * mb);
     QCH_CUDA(cudaMemcpyAsync(psi, d_psi0, sizeof(double2) * N, cudaMemcpyDeviceToDevice, st));
     QCH_CUDA(cudaMemcpyAsync(d_traj, d_psi0, sizeof(double2) * N, cudaMemcpyDeviceToDevice, st));
     DevBuf chainw(st);  // chain barrier counter (16 B) + 3 norm slots

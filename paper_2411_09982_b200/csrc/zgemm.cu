@@ -18,7 +18,8 @@
 //   DEFECT  sum |(A B^H) - I|^2 into a per-batch accumulator (unitarity audit,
 //           npad.py:257, expm.py:35-38)
 //   ACCUM   C += A B   (Paterson-Stockmeyer Horner steps of exp(-iH))
-#include "qch_internal.h"
+#include "zgemm.h"
+#include <cstring>
 #include "qch_math.cuh"
 
 namespace qch {
@@ -246,8 +247,18 @@ static int zgemm_launch(const ZgemmArgs& g, int64_t batch, cudaStream_t st) {
   return QCH_OK;
 }
 
+// The TMA-fed kernel (zgemm_tma.cu) is the default; QCH_ZGEMM=cpasync selects
+// this file's cp.async kernel (A/B comparisons).
+static bool use_cpasync() {
+  static const int v = [] {
+    const char* e = getenv("QCH_ZGEMM");
+    return (e && strcmp(e, "cpasync") == 0) ? 1 : 0;
+  }();
+  return v != 0;
+}
+
 // C = A @ B (square/rect, batched, contiguous)
-int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, int64_t batch, int64_t sa, int64_t sb,
+static int zgemm_cpasync(const double2* a, const double2* b, double2* c, int m, int n, int k, int64_t batch, int64_t sa, int64_t sb,
           int64_t sc, cudaStream_t st) {
   ZgemmArgs g{};
   g.a = a;
@@ -266,7 +277,7 @@ int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, i
 }
 
 // C += A @ B   (square n x n, batched contiguous; C must not alias A or B)
-int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st) {
+static int zgemm_accum_cpasync(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st) {
   ZgemmArgs g{};
   g.a = a;
   g.b = b;
@@ -277,23 +288,8 @@ int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t b
   return zgemm_launch<ZG_ACCUM, false>(g, batch, st);
 }
 
-// T = (A @ B) * inv_k ; O += T   (square n x n, batched contiguous)
-int zgemm_taylor(const double2* a, const double2* b, double2* t, double2* o, int n, int64_t batch, double inv_k,
-                 cudaStream_t st) {
-  ZgemmArgs g{};
-  g.a = a;
-  g.b = b;
-  g.c = t;
-  g.o = o;
-  g.m = g.n = g.k = n;
-  g.sa = g.sb = g.sc = (int64_t)n * n;
-  g.lda = g.ldb = g.ldc = n;
-  g.inv_k = inv_k;
-  return zgemm_launch<ZG_TAYLOR, false>(g, batch, st);
-}
-
 // acc[b] += || U_b U_b^H - I ||_F^2
-int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st) {
+static int zgemm_defect_cpasync(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st) {
   ZgemmArgs g{};
   g.a = u;
   g.b = u;
@@ -304,6 +300,64 @@ int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream
   g.lda = g.ldb = n;
   g.ldc = n;
   return zgemm_launch<ZG_DEFECT, true>(g, batch, st);
+}
+
+// ---- dispatch: TMA kernel (default) or the cp.async kernel above
+int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, int64_t batch, int64_t sa, int64_t sb,
+          int64_t sc, cudaStream_t st) {
+  if (use_cpasync()) return zgemm_cpasync(a, b, c, m, n, k, batch, sa, sb, sc, st);
+  ZtArgs g{};
+  g.c = c;
+  g.sc = sc;
+  return zt_gemm(ZT_STORE, false, false, a, b, m, n, k, batch, sa, sb, g, st);
+}
+
+int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st) {
+  if (use_cpasync()) return zgemm_accum_cpasync(a, b, c, n, batch, st);
+  ZtArgs g{};
+  g.c = c;
+  const int64_t nn = (int64_t)n * n;
+  return zt_gemm(ZT_ACCUM, false, false, a, b, n, n, n, batch, nn, nn, g, st);
+}
+
+// acc[b] += || U_b U_b^H - I ||_F^2 ; U U^H is Hermitian: lower tiles only
+int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st) {
+  if (use_cpasync()) return zgemm_defect_cpasync(u, acc, n, batch, st);
+  ZtArgs g{};
+  g.acc = acc;
+  const int64_t nn = (int64_t)n * n;
+  return zt_gemm(ZT_DEFECT, true, true, u, u, n, n, n, batch, nn, nn, g, st);
+}
+
+int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st) {
+  ZtArgs g{};
+  g.c = c;
+  const int64_t nn = (int64_t)n * n;
+  return zt_gemm(ZT_STORE, true, false, a, b, n, n, n, batch, nn, nn, g, st);
+}
+
+int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const double2* const* p, const double* q,
+               int nq, int n, int64_t batch, cudaStream_t st) {
+  if (nq > 4) return fail(QCH_ERR_UNSUPPORTED, "zgemm_qacc: at most 4 power terms");
+  ZtArgs g{};
+  g.c = c;
+  g.nq = nq;
+  g.q[0] = q[0];
+  for (int i = 0; i < nq; ++i) {
+    g.p[i] = p[i];
+    g.q[i + 1] = q[i + 1];
+  }
+  const int64_t nn = (int64_t)n * n;
+  return zt_gemm(ZT_QACC, herm, false, a, b, n, n, n, batch, nn, nn, g, st);
+}
+
+int zgemm_ufin(const double2* a, const double2* b, const double2* cpart, double2* u, int n, int64_t batch,
+               cudaStream_t st) {
+  ZtArgs g{};
+  g.c = u;
+  g.p[0] = cpart;
+  const int64_t nn = (int64_t)n * n;
+  return zt_gemm(ZT_UFIN, true, false, a, b, n, n, n, batch, nn, nn, g, st);
 }
 
 __global__ void sqrt_kernel(double* x, int64_t n) {
@@ -321,6 +375,13 @@ extern "C" int qch_zgemm_batched(const void* d_a, const void* d_b, void* d_c, in
   if (m > INT32_MAX / 2 || n > INT32_MAX / 2 || k > INT32_MAX / 2) return fail(QCH_ERR_UNSUPPORTED, "zgemm: too large");
   return zgemm((const double2*)d_a, (const double2*)d_b, (double2*)d_c, (int)m, (int)n, (int)k, batch, stride_a,
                stride_b, stride_c, (cudaStream_t)stream);
+}
+
+extern "C" int qch_zgemm_herm_batched(const void* d_a, const void* d_b, void* d_c, int64_t n, int64_t batch,
+                                      void* stream) {
+  if (n <= 0 || batch <= 0) return QCH_OK;
+  if (n > INT32_MAX / 2) return fail(QCH_ERR_UNSUPPORTED, "zgemm: too large");
+  return zgemm_herm((const double2*)d_a, (const double2*)d_b, (double2*)d_c, (int)n, batch, (cudaStream_t)stream);
 }
 
 extern "C" int qch_unitarity_defect_c128(const void* d_u, int64_t batch, int64_t n, double* d_defect, void* stream) {

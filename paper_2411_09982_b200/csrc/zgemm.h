@@ -1,0 +1,46 @@
+// zgemm.h — complex128 GEMMs on the FP64 tensor pipe (DMMA), shared between
+// the translation units of libqcheff (not part of the public C-ABI).
+#pragma once
+#include "qch_internal.h"
+
+namespace qch {
+
+enum { ZT_STORE = 0, ZT_ACCUM = 1, ZT_QACC = 2, ZT_UFIN = 3, ZT_DEFECT = 4 };
+
+struct ZtArgs {
+  double2* c;           // output (STORE/ACCUM/QACC/UFIN)
+  const double2* p[4];  // QACC: P_1..P_nq ; UFIN: p[0] = C (cos part)
+  double q[5];          // QACC: q_0..q_nq
+  int nq;
+  double* acc;  // DEFECT: per-batch sum of squares
+  int m, n, k;
+  int64_t sc;  // batch stride of C / P (elements; 0 = m n)
+  int ldc;     // 0 = n
+  // set by the launcher:
+  int tn, tm;   // tiles along n, m
+  int tiles;    // tiles per matrix
+  int nbatch;   // batch items of this launch
+  int64_t b0;   // first batch item of this launch
+};
+
+// TMA-fed DMMA GEMM (zgemm_tma.cu).  herm: the product is Hermitian (m == n),
+// only lower tiles are computed and mirrored.  bh: B is given as Bm (n x k)
+// and used as conj(Bm)^T.
+int zt_gemm(int mode, bool herm, bool bh, const double2* a, const double2* b, int m, int n, int k, int64_t batch,
+            int64_t sa, int64_t sb, ZtArgs g, cudaStream_t st);
+
+// square / rectangular conveniences (zgemm.cu)
+int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, int64_t batch, int64_t sa, int64_t sb,
+          int64_t sc, cudaStream_t st);
+int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st);
+int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st);
+// Hermitian products of commuting Hermitian n x n factors (batched)
+int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st);
+// C = q0 I + sum_i q_i P_i + A B  (nq <= 4), Hermitian when herm
+int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const double2* const* p, const double* q,
+               int nq, int n, int64_t batch, cudaStream_t st);
+// U = C - i (A B), A B Hermitian
+int zgemm_ufin(const double2* a, const double2* b, const double2* cpart, double2* u, int n, int64_t batch,
+               cudaStream_t st);
+
+}  // namespace qch

@@ -66,7 +66,7 @@ def expm_device(d_h):
     t = _lib.require_cuda()
     b, n = int(d_h.shape[0]), int(d_h.shape[1])
     d_u = t.empty_like(d_h)
-    work = t.empty((4 * b, n, n), dtype=t.complex128, device="cuda") if n > 4 else None
+    work = t.empty((8 * b, n, n), dtype=t.complex128, device="cuda") if n > 4 else None
     bad = ctypes.c_int64(-1)
     st = _lib.load().qch_expm_minus_i_batch_c128(
         _lib.dptr(d_h), b, n, _lib.dptr(d_u), _lib.dptr(work), ctypes.byref(bad), _lib.stream_ptr()

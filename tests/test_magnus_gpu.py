@@ -158,7 +158,8 @@ def test_zgemm_dmma_vs_numpy(E):
     from paper_2411_09982_b200 import _lib
 
     rng = np.random.default_rng(3)
-    for m, n, k, b in [(64, 64, 64, 1), (100, 37, 129, 3), (1, 1, 1, 2), (257, 130, 65, 1)]:
+    for m, n, k, b in [(64, 64, 64, 1), (100, 37, 129, 3), (1, 1, 1, 2), (257, 130, 65, 1), (128, 64, 8, 2),
+                       (300, 200, 77, 2), (513, 511, 1030, 1)]:
         a = rng.standard_normal((b, m, k)) + 1j * rng.standard_normal((b, m, k))
         bb = rng.standard_normal((b, k, n)) + 1j * rng.standard_normal((b, k, n))
         da, db = _lib.to_device(a), _lib.to_device(bb)
@@ -206,3 +207,86 @@ def test_config5_first_intervals_vs_reference_itself(E):
     psi0[0] = 1.0
     got = E.evolve(ch, grid, 2, psi0, order=1, check=True)
     assert rel_fro(got.amplitudes, g["traj"]) <= 1e-10
+
+
+def _herm(rng, n, scale=1.0):
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    return (a + a.conj().T) * (0.5 * scale)
+
+
+@pytest.mark.parametrize("n,b", [(64, 1), (100, 3), (129, 2), (300, 1), (5, 4)])
+def test_zgemm_herm_vs_numpy(E, n, b):
+    # product of two commuting Hermitian factors (H^2 and H^3 = H^2 H): only
+    # the lower tiles are computed, the upper triangle is the exact mirror
+    import torch
+    from paper_2411_09982_b200 import _lib
+
+    rng = np.random.default_rng(n + b)
+    h = np.stack([_herm(rng, n) for _ in range(b)])
+    h2 = h @ h
+    dh, dh2 = _lib.to_device(h), _lib.to_device(h2)
+    out = torch.empty((b, n, n), dtype=torch.complex128, device="cuda")
+    _lib.call("qch_zgemm_herm_batched", _lib.dptr(dh2), _lib.dptr(dh), _lib.dptr(out), n, b, _lib.stream_ptr())
+    got = out.cpu().numpy()
+    assert rel_fro(got, h2 @ h) <= 1e-14
+    iu = np.triu_indices(n, 1)
+    for q in range(b):
+        np.testing.assert_array_equal(got[q][iu], got[q].T[iu].conj())
+
+
+@pytest.mark.parametrize("n", [100, 300])
+def test_unitarity_defect_vs_numpy(E, n):
+    import torch
+    from paper_2411_09982_b200 import _lib
+
+    rng = np.random.default_rng(n)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    u = q * (1.0 + 1e-6 * rng.standard_normal(n))
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    _lib.call("qch_unitarity_defect_c128", _lib.dptr(_lib.to_device(u)), 1, n, _lib.dptr(out), _lib.stream_ptr())
+    want = np.linalg.norm(u @ u.conj().T - np.eye(n))
+    assert abs(float(out.item()) - want) <= 1e-9 * want
+
+
+@pytest.mark.parametrize("n,scale", [(17, 0.3), (64, 0.05), (130, 1.0), (256, 8.0)])
+def test_expm_hermitian_and_general_paths_vs_oracle(E, n, scale):
+    # bitwise-Hermitian input -> cos/sin form on Hermitian half-GEMMs; the
+    # same matrix with a 1e-9 non-Hermitian part -> the general
+    # Paterson-Stockmeyer path; both against the reference's 18-term Taylor
+    rng = np.random.default_rng(7 * n)
+    h = _herm(rng, n, scale)
+    assert np.array_equal(h, h.conj().T)
+    assert rel_fro(E.expm_unitary(h).entries, expm_oracle.expm_minus_i(h)) <= 1e-12
+    g = h + 1e-9 * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    assert rel_fro(E.expm_unitary(g, check=False).entries, expm_oracle.expm_minus_i(g)) <= 1e-12
+    hs = [_herm(rng, n, scale) for _ in range(3)]
+    for h_, p in zip(hs, E.expm_batch(hs)):
+        assert rel_fro(p.entries, expm_oracle.expm_minus_i(h_)) <= 1e-12
+
+
+def test_config5_order2_vs_oracle(E):
+    # BASELINE config 5 at ORDER 2 (the configured order; the reference has
+    # no second order): the first 3 of its 4096 intervals against the oracle
+    # (magnus_oracle.evolve, 18-term Taylor as expm.py:56-71; made by
+    # oracle/gen_golden_long.py), through the device path with check=True
+    from pathlib import Path
+
+    g = np.load(Path(__file__).parent / "golden" / "magnus_config5_order2_oracle.npz")
+    ch = E.heisenberg_chain_hamiltonians(12)
+    grid = E.ControlGrid(0.0, float(g["t_end"]), g["signals"])
+    psi0 = np.zeros(4096, dtype=complex)
+    psi0[0] = 1.0
+    got = E.evolve(ch, grid, 3, psi0, order=2, check=True)
+    assert rel_fro(got.amplitudes, g["traj"]) <= 1e-10
+    # mid-pulse intervals (2048, 2049), where the second-order term is large
+    # (the pulse starts near zero)
+    gm = np.load(Path(__file__).parent / "golden" / "magnus_config5_mid_order2_oracle.npz")
+    t0, t1 = (float(x) for x in gm["t"])
+    gridm = E.ControlGrid(t0, t1, gm["signals"])
+    psim = gm["traj"][0]
+    got2 = E.evolve(ch, gridm, 2, psim, order=2, check=True)
+    assert rel_fro(got2.amplitudes, gm["traj"]) <= 1e-10
+    got1 = E.evolve(ch, gridm, 2, psim, order=1, check=False)
+    # the second-order term is small at this grid spacing (dt = 25/4096) but
+    # well above the tolerance: order 1 misses the golden by ~4e-9
+    assert rel_fro(got1.amplitudes, gm["traj"]) > 10 * 1e-10

@@ -66,3 +66,20 @@ def test_config3_first_rotations(E, G):
     fin = st.current.data
     assert rel_fro(np.real(np.diag(fin)), G["c3_diag"]) <= TOL
     assert rel_fro(fin[G["c3_rows_idx"]], G["c3_rows"]) <= TOL
+
+
+def test_config3_full_length_vs_oracle(E, G):
+    # BASELINE config 3 to convergence: all 292,068 greedy picks bit-equal to
+    # the oracle (npad_oracle.run_incremental, itself bit-identical to the
+    # reference on the first 60 picks above and on every case the reference
+    # can finish; oracle/gen_golden_long.py), final diagonal and rows <= 1e-10
+    L = np.load(Path(__file__).parent / "golden" / "npad_config3_full_oracle.npz")
+    want = L["pivots"].astype(np.int64)
+    h = E.transmon_resonator_hamiltonian(4, 1024).data
+    st, piv = E.npad_run_logged(E.HermitianOperator(h), tol=1e-12, pivot_cap=len(want) + 16)
+    assert st.applied == int(L["applied"]) == len(want) and st.converged == bool(L["converged"])
+    bad = np.flatnonzero((piv != want).any(axis=1)) if piv.shape == want.shape else [-1]
+    assert len(bad) == 0, f"first differing pick at rotation {bad[0]} of {len(want)}"
+    fin = st.current.data
+    assert rel_fro(np.real(np.diag(fin)), L["diag"]) <= TOL
+    assert rel_fro(fin[L["rows_idx"]], L["rows"]) <= TOL

@@ -3,7 +3,11 @@ itself (oracle/gen_golden.py).  Bit-exact: same numpy operations, same host."""
 import numpy as np
 import pytest
 
+from pathlib import Path
+
 from oracle import expm_oracle, magnus_oracle, npad_oracle
+
+GOLD = Path(__file__).resolve().parent / "golden"
 
 
 @pytest.mark.parametrize("runner", [npad_oracle.run_full_scan, npad_oracle.run_incremental])
@@ -105,3 +109,12 @@ def test_npad_oracle_at_baseline_sizes(golden):
     ref = npad_oracle.run_incremental(h, tol=1e-12, max_iter=int(g["c3_applied"]))
     np.testing.assert_array_equal(ref["pivots"], g["c3_pivots"])
     np.testing.assert_array_equal(ref["h"][g["c3_rows_idx"]], g["c3_rows"])
+
+
+def test_long_config3_golden_starts_with_reference_picks():
+    # the oracle-made full-length config-3 golden agrees with the reference's
+    # own first 60 picks (the part the reference can produce here)
+    g = np.load(GOLD / "npad_large_ref.npz")
+    L = np.load(GOLD / "npad_config3_full_oracle.npz")
+    np.testing.assert_array_equal(L["pivots"][: len(g["c3_pivots"])].astype(np.int64), g["c3_pivots"])
+    assert int(L["applied"]) == 292068 and bool(L["converged"])
