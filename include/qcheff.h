@@ -55,6 +55,9 @@ int64_t qch_launch_count(void);
 /* HermitianOperator.max_abs (operators.py:92-99): max_ij |H_ij| with numpy's
  * |z| rounding, written to the device double *d_out. */
 int qch_max_abs_c128(const void* d_h, int64_t n_elems, double* d_out, void* stream);
+/* The same for a contiguous batch of items of n_elems each (one launch):
+ * d_out[b] = max_abs of item b. */
+int qch_max_abs_batch_c128(const void* d_h, int64_t batch, int64_t n_elems, double* d_out, void* stream);
 
 /* *d_nonherm = 0 iff H[x,y] == conj(H[y,x]) for all x, y (exact compare), else 1.
  * Selects the mirrored-column fast path of the rotation kernels. */
@@ -260,6 +263,22 @@ int qch_zgemm_batched(const void* d_a, const void* d_b, void* d_c, int64_t m, in
 int qch_zgemm_herm_batched(const void* d_a, const void* d_b, void* d_c, int64_t n, int64_t batch, void* stream);
 
 /* ------------------------------------------------ multi-GPU Magnus ------- */
+
+/* The N > 4 pipeline in two halves (multi-GPU relay, sharding.RelayEvolvePlan):
+ * qch_magnus_propagators_c128: U_m = exp(-i Hbar_m) (expm.py:56-71, the
+ * batched propagators of evolve's dense path, magnus.py:247-248) for the M
+ * intervals of a local signal window d_sig (K, S), S - 1 = M * sub; dt the
+ * grid spacing, dt_int the interval length; d_comm: basis commutators (order
+ * 2); d_u (M, N, N); check -> validate each (QCH_ERR_NONFINITE, local index).
+ * qch_magnus_chain_c128: the sequential product psi <- U_m psi
+ * (magnus.py:249-252) from d_psi_in, every state into d_rows (M, N), with the
+ * NormDrift check (QCH_ERR_NORM_DRIFT, local index).  Both synchronous. */
+int qch_magnus_propagators_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K, int64_t N,
+                                const double* d_sig, int64_t S, double dt, double dt_int, int64_t M, int order,
+                                int check, void* d_u, int64_t* bad_index, void* stream);
+int qch_magnus_chain_c128(const void* d_u, int64_t N, int64_t M, const void* d_psi_in, void* d_rows,
+                          int64_t* bad_index, void* stream);
+
 
 /* Interval sharding, N <= 4.  Workspace bytes for M local
  * intervals. */

@@ -34,6 +34,7 @@ PROTOTYPES = {
     "qch_last_error": (ctypes.c_size_t, [ctypes.c_char_p, ctypes.c_size_t]),
     "qch_launch_count": (c_int64, []),
     "qch_max_abs_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "qch_max_abs_batch_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "qch_hermitian_exact_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
     "qch_givens_params_c128": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "qch_npad_apply_rotations_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
@@ -110,6 +111,12 @@ PROTOTYPES = {
         c_int,
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_void_p],
     ),
+    "qch_magnus_propagators_c128": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_double, c_double, c_int64, c_int,
+         c_int, c_void_p, P_int64, c_void_p],
+    ),
+    "qch_magnus_chain_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, P_int64, c_void_p]),
     "qch_zgemm_herm_batched": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
 }
 

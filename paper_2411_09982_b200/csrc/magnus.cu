@@ -864,6 +864,53 @@ static int small_report(unsigned long long* d_bad, int check, int64_t* bad_index
   return QCH_OK;
 }
 
+// The ordered product psi <- U_m psi over cm propagators (magnus.py:249-252),
+// rows into traj_rows (cm, N), NormDrift index (m0 + m) into bad_norm.
+// chainw: 64 B device scratch.
+static int chain_run(const double2* u, int64_t N, int64_t cm, const double2* psi, double2* traj_rows, int64_t m0,
+                     void* chainw, unsigned long long* bad_norm, cudaStream_t st) {
+  if (N <= 64) {
+    void* pr = prof_begin("chain_cta64_kernel", st);
+    const size_t ring = sizeof(double2) * kChainStages * (size_t)N * N;
+    static bool attr64 = false;
+    if (!attr64) {
+      QCH_CUDA(cudaFuncSetAttribute(chain_cta64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(double2) * kChainStages * 64 * 64)));
+      attr64 = true;
+    }
+    chain_cta64_kernel<<<1, 256, ring, st>>>(u, (int)N, cm, psi, traj_rows, m0, bad_norm);
+    prof_end(pr, st);
+    QCH_LAUNCH_CHECK("chain_cta64_kernel");
+    note_launch(1);
+  } else {
+    // rows per CTA: one CTA for small N, up to one per SM for large N
+    static const int64_t gdiv = getenv("QCH_CHAIN_DIV") ? atoll(getenv("QCH_CHAIN_DIV")) : 1024;
+    const int G = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), N * N / gdiv));
+    QCH_CUDA(cudaMemsetAsync(chainw, 0, 64, st));
+    const double2* pin = psi;
+    int nI = (int)N;
+    int64_t cmv = cm, m0v = m0;
+    unsigned* barp = (unsigned*)chainw;
+    double* nrm3 = (double*)((unsigned char*)chainw + 16);
+    void* args[] = {(void*)&u, (void*)&nI, (void*)&cmv, (void*)&pin, (void*)&traj_rows, (void*)&m0v,
+                    (void*)&barp, (void*)&nrm3, (void*)&bad_norm};
+    // rows in flight per warp: as many as the CTA's rows allow
+    const int R = (int)((N + G - 1) / G), per_warp = R / (kChainThreads / 32);
+    auto kern = per_warp >= 8 ? chain_grid_kernel<8>
+              : per_warp >= 4 ? chain_grid_kernel<4>
+              : per_warp >= 2 ? chain_grid_kernel<2> : chain_grid_kernel<1>;
+    void* pr = prof_begin("chain_grid_kernel", st);
+    if (G > 1)
+      QCH_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kChainThreads), args, 0, st));
+    else
+      kern<<<1, kChainThreads, 0, st>>>(u, nI, cmv, pin, traj_rows, m0v, barp, nrm3, bad_norm);
+    prof_end(pr, st);
+    QCH_LAUNCH_CHECK("chain_grid_kernel");
+    note_launch(1);
+  }
+  return QCH_OK;
+}
+
 static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_comm_in, int64_t K, int64_t N,
                               const double* d_sig, int64_t S, double t_start, double t_end, int64_t M, int order,
                               const void* d_psi0, void* d_traj, void* d_props, int check, int64_t* bad_index,
@@ -951,47 +998,8 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
         }
       }
       double2* traj_rows = (double2*)d_traj + (m0 + 1) * N;
-      if (N <= 64) {
-        void* pr = prof_begin("chain_cta64_kernel", st);
-        const size_t ring = sizeof(double2) * kChainStages * (size_t)N * N;
-        static bool attr64 = false;
-        if (!attr64) {
-          QCH_CUDA(cudaFuncSetAttribute(chain_cta64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)(sizeof(double2) * kChainStages * 64 * 64)));
-          attr64 = true;
-        }
-        chain_cta64_kernel<<<1, 256, ring, st>>>(u, (int)N, cm, psi, traj_rows, m0, bad_norm);
-        prof_end(pr, st);
-        QCH_LAUNCH_CHECK("chain_cta64_kernel");
-        note_launch(1);
-        QCH_CUDA(cudaMemcpyAsync(psi, traj_rows + (cm - 1) * N, sizeof(double2) * N, cudaMemcpyDeviceToDevice, st));
-      } else {
-        // rows per CTA: one CTA for small N, up to one per SM for large N
-        static const int64_t gdiv = getenv("QCH_CHAIN_DIV") ? atoll(getenv("QCH_CHAIN_DIV")) : 1024;
-        const int G = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), N * N / gdiv));
-        QCH_CUDA(cudaMemsetAsync(chainw.p, 0, 64, st));
-        const double2* pin = psi;
-        int nI = (int)N;
-        int64_t cmv = cm, m0v = m0;
-        unsigned* barp = chainw.as<unsigned>();
-        double* nrm3 = (double*)(chainw.as<unsigned char>() + 16);
-        void* args[] = {(void*)&u, (void*)&nI, (void*)&cmv, (void*)&pin, (void*)&traj_rows, (void*)&m0v,
-                        (void*)&barp, (void*)&nrm3, (void*)&bad_norm};
-        // rows in flight per warp: as many as the CTA's rows allow
-        const int R = (int)((N + G - 1) / G), per_warp = R / (kChainThreads / 32);
-        auto kern = per_warp >= 8 ? chain_grid_kernel<8>
-                  : per_warp >= 4 ? chain_grid_kernel<4>
-                  : per_warp >= 2 ? chain_grid_kernel<2> : chain_grid_kernel<1>;
-        void* pr = prof_begin("chain_grid_kernel", st);
-        if (G > 1)
-          QCH_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kChainThreads), args, 0, st));
-        else
-          kern<<<1, kChainThreads, 0, st>>>(u, nI, cmv, pin, traj_rows, m0v, barp, nrm3, bad_norm);
-        prof_end(pr, st);
-        QCH_LAUNCH_CHECK("chain_grid_kernel");
-        note_launch(1);
-        QCH_CUDA(cudaMemcpyAsync(psi, traj_rows + (cm - 1) * N, sizeof(double2) * N, cudaMemcpyDeviceToDevice, st));
-      }
+      if (int rc = chain_run(u, N, cm, psi, traj_rows, m0, chainw.p, bad_norm, st)) return rc;
+      QCH_CUDA(cudaMemcpyAsync(psi, traj_rows + (cm - 1) * N, sizeof(double2) * N, cudaMemcpyDeviceToDevice, st));
     }
   }
   if (check) {
@@ -1016,6 +1024,80 @@ extern "C" int qch_magnus_evolve_async_c128(const void* d_h0, const void* d_hk, 
     return fail(QCH_ERR_UNSUPPORTED, "asynchronous evolve: N <= 4 and at most 8 controls (fused pipeline)");
   return magnus_evolve_impl(d_h0, d_hk, d_comm, K, N, d_sig, S, t_start, t_end, M, order, d_psi0, d_traj, d_props,
                             check, nullptr, (unsigned long long*)d_flags, stream);
+}
+
+// ---------------------------------------------------------------------------
+// The two halves of the N > 4 pipeline as separate calls, for the multi-GPU
+// relay (sharding.RelayEvolvePlan): propagators of a run of intervals, and
+// the ordered product over them from a given state.
+
+// U_m = exp(-i Hbar_m) for the M intervals of a local signal window d_sig
+// (K, S), S - 1 = M * sub, grid spacing dt, interval length dt_int; d_u
+// (M, N, N).  check: UnitaryPropagator.validate for each (expm.py:40-47).
+extern "C" int qch_magnus_propagators_c128(const void* d_h0, const void* d_hk, const void* d_comm, int64_t K,
+                                           int64_t N, const double* d_sig, int64_t S, double dt, double dt_int,
+                                           int64_t M, int order, int check, void* d_u, int64_t* bad_index,
+                                           void* stream) {
+  if (M < 1 || (S - 1) % M) return fail(QCH_ERR_GRID, "interval count does not divide the local sample steps");
+  if (order != 1 && order != 2) return fail(QCH_ERR_VALUE, "order must be 1 or 2");
+  if (N <= 4) return fail(QCH_ERR_UNSUPPORTED, "propagator runs: N > 4 (N <= 4 uses the fused pipeline)");
+  if (order >= 2 && K > 0 && d_comm == nullptr) return fail(QCH_ERR_VALUE, "order 2 needs the basis commutators");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nn = N * N;
+  const int ncomm = (int)(K + K * (K - 1) / 2);
+  DevBuf coef(st);
+  QCH_CUDA(coef.alloc(sizeof(double) * M * (K + ncomm + 1)));
+  double* c1 = coef.as<double>();
+  double* c2 = c1 + M * K;
+  if (K > 0) {
+    if (int rc = qch_magnus_coefficients(d_sig, K, S, M, dt, order, c1, c2, stream)) return rc;
+  }
+  const size_t per = sizeof(double2) * (size_t)nn;
+  int64_t mb = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)((18ull << 30) / (9 * per))));
+  DevBuf buf(st);
+  QCH_CUDA(buf.alloc(per * mb * 9 + sizeof(int) * mb + sizeof(unsigned long long) * (2 * mb + 1) +
+                     sizeof(double) * 2 * mb + 64));
+  double2* hbar = buf.as<double2>();
+  double2* work = hbar + nn * mb;  // 8 * mb
+  int* sarr = (int*)(work + 8 * nn * mb);
+  unsigned long long* norms = (unsigned long long*)(sarr + mb + (mb & 1));
+  unsigned long long* bad_u = norms + 2 * mb;
+  double* vbuf = (double*)(bad_u + 1);
+  QCH_CUDA(cudaMemsetAsync(bad_u, 0xff, sizeof(unsigned long long), st));
+  for (int64_t m0 = 0; m0 < M; m0 += mb) {
+    const int64_t cm = std::min<int64_t>(mb, M - m0);
+    if (int rc = qch_magnus_assemble_c128(d_h0, d_hk, d_comm, K, N, c1, c2, m0, cm, dt_int, order, hbar, stream))
+      return rc;
+    double2* u = (double2*)d_u + m0 * nn;
+    if (int rc = expm_generic(hbar, cm, (int)N, u, work, sarr, norms, st)) return rc;
+    if (check) {
+      if (int rc = validate_generic(u, cm, (int)N, work, vbuf, bad_u, st)) return rc;
+      unsigned long long b = 0;
+      QCH_CUDA(cudaMemcpyAsync(&b, bad_u, sizeof b, cudaMemcpyDeviceToHost, st));
+      QCH_CUDA(cudaStreamSynchronize(st));
+      if (b != ~0ull) {
+        if (bad_index) *bad_index = (int64_t)b + m0;
+        return fail(QCH_ERR_NONFINITE, "propagator not unitary (interval " + std::to_string(b + m0) + ")");
+      }
+    }
+  }
+  return QCH_OK;
+}
+
+// psi <- U_m psi for m = 0 .. M-1 (magnus.py:249-252) from d_psi_in; d_rows
+// (M, N) receives every state.  NormDrift (magnus.py:270-273) ->
+// QCH_ERR_NORM_DRIFT with the local interval in *bad_index.  Synchronous.
+extern "C" int qch_magnus_chain_c128(const void* d_u, int64_t N, int64_t M, const void* d_psi_in, void* d_rows,
+                                     int64_t* bad_index, void* stream) {
+  if (M < 1) return QCH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf w(st);
+  QCH_CUDA(w.alloc(64 + sizeof(unsigned long long)));
+  unsigned long long* bad_norm = (unsigned long long*)((unsigned char*)w.p + 64);
+  QCH_CUDA(cudaMemsetAsync(bad_norm, 0xff, sizeof(unsigned long long), st));
+  if (int rc = chain_run((const double2*)d_u, N, M, (const double2*)d_psi_in, (double2*)d_rows, 0, w.p, bad_norm, st))
+    return rc;
+  return report_bad(bad_norm, bad_index, QCH_ERR_NORM_DRIFT, "state norm drifted", st);
 }
 
 // Plan (replayed) evolve: a self-cleaning workspace owned by the caller, so a

@@ -48,6 +48,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "magnus_small.cuh"
@@ -735,7 +736,15 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
   const auto tl0 = std::chrono::steady_clock::now();
   void* pr = prof_begin("magnus_fused_kernel", st);
   const auto tl1 = std::chrono::steady_clock::now();
-  magnus_fused_kernel<N><<<grid, kFusedThreads, smem, st>>>(g);
+  // Cooperative launch: the tile schedule (static round-robin, or dynamic
+  // with group waits) needs every block of the grid resident at once; a
+  // cooperative launch guarantees that (or fails cleanly) even when other
+  // kernels share the GPU.
+  {
+    void* kargs[] = {(void*)&g};
+    QCH_CUDA(cudaLaunchCooperativeKernel((const void*)magnus_fused_kernel<N>, dim3(grid), dim3(kFusedThreads), kargs,
+                                         smem, st));
+  }
   const auto tl2 = std::chrono::steady_clock::now();
   prof_end(pr, st);
   if (trace)
@@ -867,6 +876,7 @@ struct FBuf {
 
 // page-locked status words of the host-buffer call (one pair per device)
 struct Pipe {
+  std::mutex mu;  // one host-buffer call at a time per device (shared workspace + status words)
   unsigned long long* h_flags = nullptr;
   cudaStream_t in = nullptr;  // copy stream of the host-buffer call
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -881,6 +891,8 @@ Pipe& pipe_for_device() {
   int dev = 0;
   cudaGetDevice(&dev);
   Pipe& p = pipes[dev & 63];
+  static std::mutex init_mu;
+  std::lock_guard<std::mutex> lk(init_mu);
   if (p.h_flags == nullptr) {
     cudaHostAlloc(&p.h_flags, 2 * sizeof(unsigned long long), cudaHostAllocMapped);
     cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking);
@@ -1218,8 +1230,9 @@ extern "C" int qch_magnus_evolve_host_c128(const void* h_h0, const void* h_hk, i
   }
   if (traj == nullptr) traj = d_traj;
   Pipe& pp = pipe_for_device();
-  // the device's self-cleaning workspace (grown on demand; the call is not
-  // re-entrant on one device, see qcheff.h)
+  // the device's self-cleaning workspace (grown on demand) and status words:
+  // concurrent callers on one device (ctypes releases the GIL) take turns
+  std::lock_guard<std::mutex> call_lock(pp.mu);
   const size_t b_ws = fused_ws_bytes(N, M, 1);
   if (pp.ws_bytes < b_ws || pp.ws_dirty || pp.ws_n != N || pp.ws_m != M) {  // the layout depends on (N, M)
     if (pp.ws != nullptr && pp.ws_bytes < b_ws) {

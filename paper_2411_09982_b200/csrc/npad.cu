@@ -63,6 +63,8 @@ __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldcg(p); }
 // ----------------------------------------------------------------------------
 // max_abs (operators.py:92-99)
 __global__ void max_abs_kernel(const double2* __restrict__ h, int64_t n, unsigned long long* out) {
+  h += blockIdx.y * n;  // batched: grid.y = item, n elements each
+  out += blockIdx.y;
   double m = 0.0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     double2 v = h[k];
@@ -267,6 +269,23 @@ extern "C" int qch_max_abs_c128(const void* d_h, int64_t n_elems, double* d_out,
   max_abs_kernel<<<blocks, 256, 0, st>>>((const double2*)d_h, n_elems, (unsigned long long*)d_out);
   QCH_LAUNCH_CHECK("max_abs_kernel");
   note_launch(1);
+  return QCH_OK;
+}
+
+extern "C" int qch_max_abs_batch_c128(const void* d_h, int64_t batch, int64_t n_elems, double* d_out,
+                                      void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (batch <= 0) return QCH_OK;
+  QCH_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double) * batch, st));
+  if (n_elems <= 0) return QCH_OK;
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = std::min<int64_t>(batch - b0, 65535);
+    const int per = (int)std::max<int64_t>(1, std::min<int64_t>((n_elems + 255) / 256, (int64_t)sm_count() * 8 / nb));
+    max_abs_kernel<<<dim3(per, (unsigned)nb), 256, 0, st>>>((const double2*)d_h + b0 * n_elems, n_elems,
+                                                            (unsigned long long*)d_out + b0);
+    QCH_LAUNCH_CHECK("max_abs_kernel");
+    note_launch(1);
+  }
   return QCH_OK;
 }
 

@@ -402,18 +402,44 @@ def npad_run_logged(op, target=None, *, tol, max_iter=None, track_unitary=False,
 
 @dataclass
 class BatchResult:
-    """Result of a batched npad_run: device-resident final operators
-    (batch, n, n), rotation counts and convergence flags."""
+    """Result of a batched npad_run: device-resident final operators, rotation
+    counts and convergence flags.  ``parts`` holds (first item, (b, n, n)
+    CUDA tensor) per device (one part unless ``devices`` spread the batch)."""
 
-    matrices: object  # CUDA tensor (batch, n, n) complex128
+    parts: list
     applied: np.ndarray
     converged: np.ndarray
 
+    @property
+    def matrices(self):
+        """(batch, n, n) CUDA tensor of the final operators (single-device
+        results; multi-device results are in ``parts``)."""
+        if len(self.parts) != 1:
+            raise ValueError("result spans several devices: use .parts or .operator(b)")
+        return self.parts[0][1]
+
+    def _locate(self, b: int):
+        for start, mats in reversed(self.parts):
+            if b >= start:
+                return mats, b - start
+        raise IndexError(b)
+
     def operator(self, b: int) -> HermitianOperator:
-        return HermitianOperator._from_device(self.matrices[b])
+        mats, k = self._locate(b)
+        return HermitianOperator._from_device(mats[k])
 
     def diagonals(self) -> np.ndarray:
-        return _lib.to_host(self.matrices.diagonal(dim1=1, dim2=2).real.contiguous())
+        return np.concatenate([_lib.to_host(m.diagonal(dim1=1, dim2=2).real.contiguous()) for _, m in self.parts])
+
+
+def max_abs_batch(mats):
+    """Per-item max |H| of a (b, n, n) device batch, ONE launch
+    (qch_max_abs_batch_c128, numpy |z| as operators.py:92-99)."""
+    t = _lib.require_cuda()
+    b = int(mats.shape[0])
+    out = t.empty(b, dtype=t.float64, device=mats.device)
+    _lib.call("qch_max_abs_batch_c128", _lib.dptr(mats), b, int(mats[0].numel()), _lib.dptr(out), _lib.stream_ptr())
+    return out
 
 
 def _run_batch_inplace(mats, target, tol, max_iter, max_abs_dev=None, sync=True):
@@ -425,12 +451,10 @@ def _run_batch_inplace(mats, target, tol, max_iter, max_abs_dev=None, sync=True)
         max_iter = 20 * n * n
     d_target, n_target = _target_tensor(target, n)
     if max_abs_dev is None:
-        max_abs_dev = t.empty(b, dtype=t.float64, device="cuda")
-        for k in range(b):
-            _lib.call("qch_max_abs_c128", _lib.dptr(mats[k]), n * n, _lib.dptr(max_abs_dev[k:k + 1]), _lib.stream_ptr())
+        max_abs_dev = max_abs_batch(mats)
     thr = max_abs_dev * float(tol)
-    applied = t.empty(b, dtype=t.int64, device="cuda")
-    conv = t.empty(b, dtype=t.int32, device="cuda")
+    applied = t.empty(b, dtype=t.int64, device=mats.device)
+    conv = t.empty(b, dtype=t.int32, device=mats.device)
     _lib.call(
         "qch_npad_run_batch_c128", _lib.dptr(mats), b, n, _lib.dptr(d_target), n_target, _lib.dptr(thr),
         int(max_iter), _lib.dptr(applied), _lib.dptr(conv), _lib.stream_ptr(),
@@ -438,24 +462,84 @@ def _run_batch_inplace(mats, target, tol, max_iter, max_abs_dev=None, sync=True)
     return applied, conv
 
 
+def _batch_on_current_device(ops, target, tol, max_iter):
+    """One device: bitwise-Hermitian operators go through the batched
+    many-chain driver; any others (Hermitian only to rounding, which the
+    batched lazy-column driver cannot take) through npad_run one by one —
+    the same per-operator results either way."""
+    t = _lib.require_cuda()
+    mats = t.stack([op.device_tensor().to(t.cuda.current_device()) for op in ops]).contiguous()
+    b = len(ops)
+    herm = [not _nonherm(mats[k]) for k in range(b)]
+    applied = np.zeros(b, dtype=np.int64)
+    conv = np.zeros(b, dtype=bool)
+    idx = [k for k in range(b) if herm[k]]
+    if idx:
+        sub = mats[idx].contiguous() if len(idx) < b else mats
+        max_abs = t.tensor([ops[k].max_abs() for k in idx], dtype=t.float64, device=mats.device)
+        ap, cv = _run_batch_inplace(sub, target, tol, max_iter, max_abs)
+        applied[idx] = _lib.to_host(ap)
+        conv[idx] = _lib.to_host(cv).astype(bool)
+        if len(idx) < b:
+            mats[idx] = sub
+    for k in range(b):
+        if not herm[k]:
+            st = npad_run(HermitianOperator._from_device(mats[k].clone()), target, tol=tol, max_iter=max_iter)
+            mats[k].copy_(st.current.device_tensor())
+            applied[k], conv[k] = st.applied, st.converged
+    return mats, applied, conv
+
+
 def npad_run_batch(ops: Sequence[HermitianOperator], target=None, *, tol: float, max_iter: int | None = None,
                    devices: Sequence[int] | None = None) -> BatchResult:
-    """``npad_run`` over independent operators of one dimension, one
-    persistent block per operator (new API; per-point results equal
-    ``npad_run`` on each operator).  Operators must be exactly Hermitian
-    (H[x,y] == conj(H[y,x]) bitwise), as the builders produce."""
-    t = _lib.require_cuda()
+    """``npad_run`` over independent operators of one dimension (new API;
+    per-point results equal ``npad_run`` on each operator): one warp-resident
+    chain per operator.  ``devices``: CUDA device ordinals to spread the batch
+    over (contiguous blocks, one host thread per device, no communication);
+    default the current device."""
+    _lib.require_cuda()
     ops = list(ops)
     if not ops:
         raise ValueError("need at least one operator")
-    n = ops[0].dim
-    mats = t.stack([op.device_tensor() for op in ops]).contiguous()
-    nonherm = any(_nonherm(mats[k]) for k in range(len(ops)))
-    if nonherm:
-        raise ValueError("npad_run_batch needs exactly Hermitian operators; use npad_run per operator")
-    max_abs = t.tensor([op.max_abs() for op in ops], dtype=t.float64, device="cuda")
-    applied, conv = _run_batch_inplace(mats, target, tol, max_iter, max_abs)
-    return BatchResult(mats, _lib.to_host(applied), _lib.to_host(conv).astype(bool))
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    devs = list(devices) if devices else [None]
+    if len(devs) == 1:
+        if devs[0] is None:
+            mats, ap, cv = _batch_on_current_device(ops, target, tol, max_iter)
+        else:
+            with _lib.torch().cuda.device(int(devs[0])):
+                mats, ap, cv = _batch_on_current_device(ops, target, tol, max_iter)
+        return BatchResult([(0, mats)], ap, cv)
+    import threading
+
+    from .sharding import shard_bounds
+
+    t = _lib.torch()
+    res, errs = {}, []
+
+    def work(r, dev):
+        try:
+            a, b = shard_bounds(len(ops), len(devs), r)
+            if a == b:
+                return
+            with t.cuda.device(int(dev)):
+                mats, ap, cv = _batch_on_current_device(ops[a:b], target, tol, max_iter)
+                t.cuda.current_stream().synchronize()
+            res[r] = (a, mats, ap, cv)
+        except BaseException as e:  # re-raised on the calling thread
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(r, d)) for r, d in enumerate(devs)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    if errs:
+        raise errs[0]
+    parts = [res[r] for r in sorted(res)]
+    return BatchResult([(a, m) for a, m, _, _ in parts], np.concatenate([p[2] for p in parts]),
+                       np.concatenate([p[3] for p in parts]))
 
 
 def build_transmon_resonator_batch(params: np.ndarray, n_q: int, n_r: int):
@@ -478,9 +562,5 @@ def npad_sweep_transmon(params: np.ndarray, n_q: int, n_r: int, target=None, *, 
     point on the device and run the batched greedy NPAD (new API)."""
     t = _lib.require_cuda()
     mats = build_transmon_resonator_batch(params, n_q, n_r)
-    n = n_q * n_r
-    max_abs = t.empty(mats.shape[0], dtype=t.float64, device="cuda")
-    for k in range(mats.shape[0]):
-        _lib.call("qch_max_abs_c128", _lib.dptr(mats[k]), n * n, _lib.dptr(max_abs[k:k + 1]), _lib.stream_ptr())
-    applied, conv = _run_batch_inplace(mats, target, tol, max_iter, max_abs)
-    return BatchResult(mats, _lib.to_host(applied), _lib.to_host(conv).astype(bool))
+    applied, conv = _run_batch_inplace(mats, target, tol, max_iter, max_abs_batch(mats))
+    return BatchResult([(0, mats)], _lib.to_host(applied), _lib.to_host(conv).astype(bool))
