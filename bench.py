@@ -140,6 +140,16 @@ def time_steps(torch, fn, steps, flush, world):
     return out
 
 
+def sum_over_ranks(torch, value, world):
+    if world == 1:
+        return value
+    import torch.distributed as dist
+
+    t = torch.tensor([float(value)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def max_over_ranks(torch, value, world):
     if world == 1:
         return value
@@ -310,6 +320,18 @@ def run_headline(torch, eff, lib, args, world, rank, local):
     torch.cuda.synchronize()
     e2e_ms = time_steps(torch, e2e_step, max(3, args.steps), flush, world)
     e2e_per = max_over_ranks(torch, sum(e2e_ms), world) / len(e2e_ms)
+    # the same with the plain (pageable) numpy signals a reference caller passes
+    gp = eff.ControlGrid(grid.t_start, grid.t_end, np.array(grid.signals, copy=True))
+
+    def e2e_pageable_step():
+        if world == 1:
+            return eff.evolve(chh, gp, m, psi0, order=2, check=False).amplitudes
+        return sharding.evolve_sharded(chh, gp, m, psi0, order=2, check=False).trajectory.cpu().numpy()
+
+    e2e_pageable_step()
+    torch.cuda.synchronize()
+    pg_ms = time_steps(torch, e2e_pageable_step, max(3, args.steps), flush, world)
+    pg_per = max_over_ranks(torch, sum(pg_ms), world) / len(pg_ms)
     h2d = grid.signals.nbytes // world + sum(o.nbytes for o in ops) + psi0.nbytes
     d2h = (M_PER_GPU + 1) * 3 * 16
 
@@ -322,10 +344,30 @@ def run_headline(torch, eff, lib, args, world, rank, local):
                 "executed_flops_per_launch": magnus_executed_flops_per_interval() * M_PER_GPU,
                 "kernel_share_of_step": k1_ms / per_step}
     return dict(value=value, per_step=per_step, ms=ms, launches=launches // args.steps, clocks=clk.summary(),
-                e2e=(M_PER_GPU * world / (e2e_per * 1e-3), h2d, d2h), roof=roof, m=m)
+                e2e=(M_PER_GPU * world / (e2e_per * 1e-3), h2d, d2h), e2e_pageable=M_PER_GPU * world / (pg_per * 1e-3),
+                roof=roof, m=m)
 
 
 # -------------------------------------------------------------- secondaries --
+
+def _e2e_npad(torch, eff, h, reps, target=None, flush=lambda: None):
+    """NPAD end to end through the public API: host numpy H -> HermitianOperator
+    -> npad_run -> host diagonal (the reference contract, npad.py:320-354 +
+    operators.py:120-131), H2D and D2H inside the timed region."""
+    res = {}
+
+    def step():
+        st = eff.npad_run(eff.HermitianOperator(h), target, tol=1e-12)
+        res["diag"] = st.current.diagonal()
+        res["applied"] = st.applied
+
+    step()
+    ms = time_steps(torch, step, reps, flush, 1)
+    per = sum(ms) / len(ms)
+    return {"value": res["applied"] / (per * 1e-3), "unit": "rotations/s", "ms_per_solve": per,
+            "h2d_bytes_per_step": int(h.nbytes), "d2h_bytes_per_step": int(res["diag"].nbytes),
+            "path": "npad_run(HermitianOperator(host H)).current.diagonal() (pageable host H)"}
+
 
 def sec_npad60(torch, eff, lib, args, peaks):
     from oracle import npad_oracle
@@ -349,12 +391,14 @@ def sec_npad60(torch, eff, lib, args, peaks):
     rot = res["st"].applied
     per = sum(ms) / len(ms)
     kms = prof["npad_run_kernel"][0] / prof["npad_run_kernel"][1]
+    e2e = _e2e_npad(torch, eff, h, 10)
     t0 = time.perf_counter()
     ref = npad_oracle.run_full_scan(h, tol=1e-12)
     cpu = ref["applied"] / (time.perf_counter() - t0)
     return {"workload": "config 1: NPAD transmon3 x resonator20 (dim 60), full diagonal, tol 1e-12",
             "metric": "NPAD rotations/s", "unit": "rotations/s", "value": rot / (per * 1e-3),
             "rotations": rot, "ms_per_solve": per, "us_per_rotation_kernel": kms * 1e3 / rot,
+            "e2e": e2e,
             "roofline": {"bound": "latency", "note": "serial greedy chain; matrix resident in shared memory",
                          "achieved": 96 * 60 * rot / (kms * 1e-3) / 1e9, "peak": peaks[0], "unit": "GB/s",
                          "frac": 96 * 60 * rot / (kms * 1e-3) / 1e9 / peaks[0]},
@@ -387,6 +431,7 @@ def sec_npad4096(torch, eff, lib, args, peaks, rotations=None):
     kms = prof["npad_run_kernel"][0] / prof["npad_run_kernel"][1]
     n = n_q * n_r
     ach = 96 * n * st.applied / (kms * 1e-3) / 1e9
+    e2e = _e2e_npad(torch, eff, h, 1, flush=L2Flusher(torch)) if not mi else None
     t0 = time.perf_counter()
     ref = npad_oracle.run_full_scan(h, tol=1e-12, max_iter=3)
     cpu = 3 / (time.perf_counter() - t0)
@@ -395,6 +440,7 @@ def sec_npad4096(torch, eff, lib, args, peaks, rotations=None):
             "metric": "NPAD rotations/s", "unit": "rotations/s", "value": st.applied / (per * 1e-3),
             "rotations": st.applied, "converged": st.converged, "ms_per_solve": per,
             "us_per_rotation_kernel": kms * 1e3 / st.applied,
+            "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks[0], "unit": "GB/s", "frac": ach / peaks[0],
                          "bytes_per_rotation": 96 * n, "note": "single greedy chain: latency-bound (see DESIGN.md)",
                          "traffic": (traffic_from_profiles("npad_coop_kernel@npad4096") or 0) / 2000 * st.applied
@@ -405,24 +451,27 @@ def sec_npad4096(torch, eff, lib, args, peaks, rotations=None):
                              "sample": "3 rotations of the same operator, oracle run_full_scan"}}
 
 
-def sec_sweep(torch, eff, lib, args, peaks, n_points=1024):
+def sec_sweep(torch, eff, lib, args, peaks, world=1, rank=0, n_points=1024):
+    """Config 4: 1024 (g, Delta) points of a dim-1024 transmon x resonator,
+    subspace NPAD to convergence.  N > 1: the points are split in contiguous
+    blocks over the ranks (sharding.sweep_sharded; strong scaling, no
+    collective on the data path)."""
     from oracle import npad_oracle
+    from paper_2411_09982_b200 import npad as npd
+    from paper_2411_09982_b200 import sharding
 
     n_q, n_r = 4, 256
     n = n_q * n_r
     side = int(round(n_points ** 0.5))
     pts = eff.sweep_points(side, n_points // side)
     tgt = eff.sweep_target(n_r)
-    from paper_2411_09982_b200 import npad as npd
-
+    a, b = sharding.shard_bounds(pts.shape[0], world, rank)
+    mine = pts[a:b]
     state = {}
 
-    def rebuild():
-        state["mats"] = npd.build_transmon_resonator_batch(pts, n_q, n_r)
-        mx = torch.empty(pts.shape[0], dtype=torch.float64, device="cuda")
-        for k in range(pts.shape[0]):
-            lib.call("qch_max_abs_c128", lib.dptr(state["mats"][k]), n * n, lib.dptr(mx[k:k + 1]), lib.stream_ptr())
-        state["mx"] = mx
+    def rebuild():  # fresh operators on the device (writes 16 GiB / world: L2 flushed)
+        state["mats"] = npd.build_transmon_resonator_batch(mine, n_q, n_r)
+        state["mx"] = npd.max_abs_batch(state["mats"])
 
     def step():
         state["out"] = npd._run_batch_inplace(state["mats"], tgt, 1e-12, None, state["mx"])
@@ -433,81 +482,179 @@ def sec_sweep(torch, eff, lib, args, peaks, n_points=1024):
     lib.profile_read(reset=True)
     lib.profile_enable(True)
     for _ in range(2):
-        rebuild()  # fresh operators; writes 16 GiB => L2 flushed
-        tot += time_steps(torch, step, 1, lambda: None, 1)
+        rebuild()
+        tot += time_steps(torch, step, 1, lambda: None, world)
     lib.profile_enable(False)
     prof = lib.profile_read(reset=True)
     applied = state["out"][0].cpu().numpy()
     conv = state["out"][1].cpu().numpy()
-    rot = int(applied.sum())
-    per = sum(tot) / len(tot)
-    kms = prof["npad_run_kernel"][0] / prof["npad_run_kernel"][1]
-    ach = 96 * n * rot / (kms * 1e-3) / 1e9
-    # CPU: reference algorithm on 2 sweep points
-    t0 = time.perf_counter()
-    crot = 0
-    for row in pts[:2]:
-        h = eff.transmon_resonator_hamiltonian(n_q, n_r, omega_q=row[0], alpha=row[1], omega_r=row[2], g=row[3]).data
-        crot += npad_oracle.run_full_scan(h, tgt, tol=1e-12, max_iter=60)["applied"]
-    cpu = crot / (time.perf_counter() - t0)
+    rot_local = int(applied.sum())
+    rot = int(round(sum_over_ranks(torch, rot_local, world)))
+    all_conv = sum_over_ranks(torch, float(conv.all()), world) == world
+    per = max_over_ranks(torch, sum(tot) / len(tot), world)
+    kms = max_over_ranks(torch, prof["npad_run_kernel"][0] / prof["npad_run_kernel"][1], world)
+    ach = 96 * n * rot / world / (kms * 1e-3) / 1e9  # per GPU
+    # e2e: host (omega_q, alpha, omega_r, g) rows in -> per-point applied,
+    # converged and final diagonal on the host (rank 0 gathers), through the
+    # public API (npad_sweep_transmon on 1 GPU, sharding.sweep_sharded on N)
+    del state["mats"]
+
+    def e2e_step():
+        if world == 1:
+            r = eff.npad_sweep_transmon(pts, n_q, n_r, tgt, tol=1e-12)
+            state["e2e"] = (r.applied, r.converged, r.diagonals())
+            del r
+        else:
+            r = sharding.sweep_sharded(pts, n_q, n_r, tgt, tol=1e-12)
+            state["e2e"] = r.gather()
+            del r
+
+    e2e_ms = time_steps(torch, e2e_step, 1, lambda: None, world)
+    e2e_per = max_over_ranks(torch, sum(e2e_ms) / len(e2e_ms), world)
+    assert int(state["e2e"][0].sum()) == rot
+    cpu = None
+    if rank == 0:  # CPU: reference algorithm on 2 sweep points, first 60 rotations each
+        t0 = time.perf_counter()
+        crot = 0
+        for row in pts[:2]:
+            h = eff.transmon_resonator_hamiltonian(n_q, n_r, omega_q=row[0], alpha=row[1], omega_r=row[2],
+                                                   g=row[3]).data
+            crot += npad_oracle.run_full_scan(h, tgt, tol=1e-12, max_iter=60)["applied"]
+        cpu = crot / (time.perf_counter() - t0)
     return {"workload": f"config 4: NPAD sweep {pts.shape[0]} (g, Delta) points, transmon4 x resonator256 (dim 1024),"
-                        f" subspace target 10 levels, tol 1e-12, one GPU",
+                        f" subspace target 10 levels, tol 1e-12, "
+                        + ("one GPU" if world == 1 else f"points split over {world} GPUs"),
             "metric": "NPAD rotations/s", "unit": "rotations/s", "value": rot / (per * 1e-3), "rotations": rot,
-            "all_converged": bool(conv.all()), "ms_per_sweep": per,
+            "n_gpus": world, "scaling": "strong", "all_converged": bool(all_conv), "ms_per_sweep": per,
+            "e2e": {"value": rot / (e2e_per * 1e-3), "unit": "rotations/s", "ms_per_sweep": e2e_per,
+                    "h2d_bytes_per_step": int(pts.nbytes),
+                    "d2h_bytes_per_step": int(pts.shape[0] * (n * 8 + 8 + 1)),
+                    "path": "npad_sweep_transmon(host points) / sharding.sweep_sharded(...).gather(): per-point "
+                            "applied, converged, final diagonal to the host"},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks[0], "unit": "GB/s", "frac": ach / peaks[0],
-                         "bytes_per_rotation": 96 * n, "traffic": traffic_from_profiles("npad_trows_warp_kernel@sweep")},
+                         "per": "GPU", "bytes_per_rotation": 96 * n,
+                         "traffic": traffic_from_profiles("npad_trows_warp_kernel@sweep")},
             "cpu_baseline": {"value": cpu, "unit": "rotations/s", "cores": 1, "kind": "port",
                              "sample": "first 60 rotations of 2 sweep points, oracle run_full_scan"}}
 
 
-def sec_magnus4096(torch, eff, lib, args, fp64, n_int=2):
-    from paper_2411_09982_b200 import magnus as mg
-
+def _magnus5_problem(eff, n_int=4096):
     L = 12
     ch = eff.heisenberg_chain_hamiltonians(L)
     full = eff.synthetic_transfer_pulse(25.0, 4096 * 8 + 1, seed=7)
     grid = eff.ControlGrid(0.0, 25.0 * n_int / 4096, full.signals[:, :n_int * 8 + 1])
     psi0 = np.zeros(1 << L, dtype=complex)
     psi0[0] = 1
-    d_psi = lib.to_device(psi0)
+    return ch, grid, psi0
+
+
+def _herm_fraction(n, bm=128, bn=64):
+    """Share of the 8 N^3 of a complex GEMM the Hermitian kernel computes (the
+    128 x 64 tiles meeting the lower triangle)."""
+    tm, tn = -(-n // bm), -(-n // bn)
+    return sum(min(2 * r + 2, tn) for r in range(tm)) / (tm * tn)
+
+
+def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
+    """Config 5 at its stated size: Magnus order 2 on the 12-spin Heisenberg
+    chain (dim 4096), ALL 4096 intervals.  One GPU: the public evolve()
+    (host psi0 + signals in, host trajectory out), its device phase timed
+    with CUDA events (value) and the whole call (e2e).  N GPUs: the relay
+    (sharding.evolve_relay, chunks round-robin, psi passed rank to rank) +
+    the trajectory gather to the host."""
+    from oracle import expm_oracle
+    from paper_2411_09982_b200 import magnus as mg
+    from paper_2411_09982_b200 import sharding
+
+    ch, grid, psi0 = _magnus5_problem(eff, n_int)
+    n = ch.dim
     ch.device_operators()
-
-    def step():
-        mg.evolve_device(ch, grid, n_int, d_psi, check=False, order=2)
-
-    step()
+    # warm-up: 2 intervals (allocations, attributes, commutators)
+    g2 = eff.ControlGrid(0.0, 25.0 * 2 / 4096, grid.signals[:, :17])
+    if world == 1:
+        eff.evolve(ch, g2, 2, psi0, order=2, check=False)
+    else:
+        sharding.evolve_relay(ch, eff.ControlGrid(0.0, 25.0 * world / 4096, grid.signals[:, :8 * world + 1]), world,
+                              psi0, order=2, check=False, chunk=1)
+    torch.cuda.synchronize()
     lib.profile_read(reset=True)
     lib.profile_enable(True)
-    ms = time_steps(torch, step, 1, lambda: None, 1)
+    if world == 1:
+        mg.PHASE_TIMING = True
+        ms = time_steps(torch, lambda: eff.evolve(ch, grid, n_int, psi0, order=2, check=False), 1, lambda: None, 1)
+        mg.PHASE_TIMING = False
+        ph = dict(mg.LAST_PHASES)
+        dev_ms, e2e_ms = ph["device_ms"], ms[0]
+        d2h = (n_int + 1) * n * 16
+    else:
+        res = {}
+
+        def relay():
+            res["r"] = sharding.evolve_relay(ch, grid, n_int, psi0, order=2, check=False)
+
+        def gather():
+            tr = res["r"].gather()
+            if rank == 0:
+                res["host"] = lib.to_host(tr)
+
+        dev_ms = max_over_ranks(torch, time_steps(torch, relay, 1, lambda: None, world)[0], world)
+        g_ms = max_over_ranks(torch, time_steps(torch, gather, 1, lambda: None, world)[0], world)
+        e2e_ms = dev_ms + g_ms
+        d2h = (n_int + 1) * n * 16
     lib.profile_enable(False)
     prof = lib.profile_read(reset=True)
-    per = sum(ms) / len(ms)
-    n = 1 << L
-    # every GEMM of the step is one batched launch over the n_int intervals:
-    # powers a^2, a^3 + the Paterson-Stockmeyer Horner steps (zgemm_accum)
-    g_ms = sum(prof[k][0] for k in ("zgemm", "zgemm_accum", "zgemm_taylor") if k in prof)
-    g_cnt = sum(prof[k][1] for k in ("zgemm", "zgemm_accum", "zgemm_taylor") if k in prof)
-    fl_exec = g_cnt * n_int * 8 * n**3
-    ach = fl_exec / (g_ms * 1e-3) / 1e12 if g_ms else None
-    fl_ref = 17 * 8 * n**3  # the reference's 17 GEMMs per interval (s = 0)
-    return {"workload": f"config 5: Magnus 12-spin Heisenberg chain (dim 4096), order 2, sample of {n_int} of 4096 "
-                        f"intervals, one GPU",
-            "metric": "Magnus intervals/s", "unit": "intervals/s", "value": n_int / (per * 1e-3),
-            "ms_per_interval": per / n_int,
-            "gemms_per_interval": g_cnt,
-            "roofline": {"bound": "tensor", "kernel": "zgemm_kernel (DMMA)", "achieved": ach, "peak": fp64.get("dmma"),
-                         "unit": "TFLOP/s", "frac": (ach / fp64["dmma"]) if ach and fp64.get("dmma") else None,
+    gk = {k: v for k, v in prof.items() if k.startswith("zgemm")}
+    g_ms = max_over_ranks(torch, sum(v[0] for v in gk.values()), world)
+    frac_h = _herm_fraction(n)
+    rp = int(lib.load().qch_zgemm_real_products())  # real DMMA products per complex product (3M: 3)
+    # executed DMMA flops: one GEMM launch = one product for every interval
+    # of a chunk (one chain launch per chunk); the Hermitian kernels compute
+    # frac_h of the 8 N^3 of a complex product
+    chunks = max(1, prof.get("chain_grid_kernel", (0, 1))[1])
+    gemm_per_interval = {k: c / chunks for k, (_t, c) in gk.items()}
+    fl_exec = sum((frac_h if "herm" in k else 1.0) * 2.0 * rp * n**3 * c for k, c in gemm_per_interval.items()) * n_int
+    ach = fl_exec / world / (g_ms * 1e-3) / 1e12 if g_ms else None
+    fl_ref = 17 * 8 * n**3
+    cpu = None
+    if rank == 0:  # the reference's _expm_minus_i (18-term Taylor, expm.py:56-71) on ONE interval, host cores
+        from paper_2411_09982_b200 import models
+
+        try:
+            from threadpoolctl import threadpool_info
+
+            blas = [(i.get("internal_api"), i.get("num_threads")) for i in threadpool_info()]
+        except Exception:  # pragma: no cover
+            blas = None
+        hb = ch.drift.to_dense() * (25.0 / 4096)
+        t0 = time.perf_counter()
+        expm_oracle.expm_minus_i(hb)
+        cpu_s = time.perf_counter() - t0
+        cpu = {"value": 1.0 / cpu_s, "unit": "intervals/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"one interval's propagator at N = 4096 (oracle expm_minus_i = the reference's 18-term "
+                         f"Taylor, 17 complex GEMMs on numpy/OpenBLAS), {cpu_s:.1f} s; BLAS threads {blas}"}
+    return {"workload": f"config 5: Magnus 12-spin Heisenberg chain (dim 4096), order 2, ALL {n_int} intervals, "
+                        + ("one GPU" if world == 1 else f"relay over {world} GPUs"),
+            "metric": "Magnus intervals/s", "unit": "intervals/s", "value": n_int / (dev_ms * 1e-3),
+            "intervals": n_int, "n_gpus": world, "scaling": "strong", "ms_per_evolve": dev_ms,
+            "e2e": {"value": n_int / (e2e_ms * 1e-3), "unit": "intervals/s", "ms": e2e_ms,
+                    "h2d_bytes_per_step": int(grid.signals.nbytes + psi0.nbytes), "d2h_bytes_per_step": int(d2h),
+                    "path": "evolve(host psi0, host grid) -> host trajectory" if world == 1
+                            else "sharding.evolve_relay + gather -> host trajectory on rank 0"},
+            "gemms_per_interval": gemm_per_interval,
+            "roofline": {"bound": "tensor", "kernel": "zgemm_tma_kernel (DMMA, TMA-fed)", "achieved": ach,
+                         "peak": fp64.get("dmma"), "unit": "TFLOP/s",
+                         "frac": (ach / fp64["dmma"]) if ach and fp64.get("dmma") else None,
                          "peak_kind": "FP64 DMMA (mma.sync f64) measured live; cuBLAS zgemm "
-                                      f"{fp64.get('cublas_zgemm', 0):.1f} TFLOP/s for reference",
-                         "flops_basis": "executed GEMM flops (8N^3 per complex GEMM); the Taylor series is cut at "
-                                        "the 2^-56 degree and evaluated by Paterson-Stockmeyer (2 + m/3 GEMMs)",
-                         "reference_equivalent_tflops": (fl_ref * n_int / (per * 1e-3) / 1e12),
-                         "flops_per_interval_executed": fl_exec / n_int if n_int else None,
+                                      f"{fp64.get('cublas_zgemm', 0):.1f} TFLOP/s on the same box",
+                         "flops_basis": f"executed DMMA flops: {2 * rp} N^3 per full complex GEMM ({rp} real "
+                                        "products per complex product), the computed share "
+                                        f"({frac_h:.3f}) of it for the Hermitian half-GEMMs",
+                         "gemm_ms": g_ms,
+                         "reference_equivalent_tflops": fl_ref * n_int / (dev_ms * 1e-3) / 1e12,
+                         "flops_per_interval_executed": fl_exec / n_int,
                          "flops_per_interval_reference": fl_ref,
-                         "traffic": traffic_from_profiles("zgemm_kernel@zgemm4096")},
-            "cpu_baseline": {"value": 1.0 / 36.7, "unit": "intervals/s", "cores": 8, "kind": "port",
-                             "sample": "SURVEY.md §8(d) measurement (one _expm_minus_i at N=4096 = 36.7 s, 8-core "
-                                       "OpenBLAS); not re-timed here (42 h full run)"}}
+                         "traffic": traffic_from_profiles("zgemm_tma_kernel@c5")},
+            "cpu_baseline": cpu}
 
 
 def sec_midsize(torch, eff, lib, args, fp64, L=8, n_int=2048):
@@ -536,8 +683,12 @@ def sec_midsize(torch, eff, lib, args, fp64, L=8, n_int=2048):
     prof = lib.profile_read(reset=True)
     per = sum(ms) / len(ms)
     g_ms = sum(v[0] for k, v in prof.items() if k.startswith("zgemm")) / 3
-    g_cnt = sum(v[1] for k, v in prof.items() if k.startswith("zgemm")) / 3
-    fl = g_cnt * n_int * 8 * n**3
+    rp = int(lib.load().qch_zgemm_real_products())
+    frac_h = _herm_fraction(n)
+    chunks = max(1, prof.get("chain_cta64_kernel", prof.get("chain_grid_kernel", (0, 1)))[1] / 3)
+    # executed DMMA flops: every GEMM launch covers one chunk of intervals
+    fl = sum((frac_h if "herm" in k else 1.0) * 2 * rp * n**3 * v[1] / 3 for k, v in prof.items()
+             if k.startswith("zgemm")) * n_int / chunks
     ach = fl / (g_ms * 1e-3) / 1e12 if g_ms else None
     chain_ms = prof.get("chain_grid_kernel", (0.0, 1))[0] / 3
     # CPU: the oracle (numpy restatement of evolve, 18-term Taylor, order 2) on 8 intervals
@@ -552,9 +703,10 @@ def sec_midsize(torch, eff, lib, args, fp64, L=8, n_int=2048):
                         f"order 2, check=True",
             "metric": "Magnus intervals/s", "unit": "intervals/s", "value": n_int / (per * 1e-3),
             "ms_per_step": per, "gemm_ms": g_ms, "chain_ms": chain_ms,
-            "roofline": {"bound": "tensor", "kernel": "zgemm_kernel (DMMA)", "achieved": ach, "peak": fp64.get("dmma"),
+            "roofline": {"bound": "tensor", "kernel": "zgemm_tma_kernel (DMMA, TMA-fed)", "achieved": ach, "peak": fp64.get("dmma"),
                          "unit": "TFLOP/s", "frac": (ach / fp64["dmma"]) if ach and fp64.get("dmma") else None,
-                         "flops_basis": "executed GEMM flops (8N^3 per complex GEMM)"},
+                         "flops_basis": f"executed DMMA flops ({2 * rp} N^3 per complex GEMM, the computed "
+                                        f"share {frac_h:.3f} for Hermitian half-GEMMs)"},
             "cpu_baseline": {"value": cpu, "unit": "intervals/s", "cores": os.cpu_count(), "kind": "port",
                              "sample": f"{k_cpu} intervals, oracle/magnus_oracle.evolve (numpy/OpenBLAS)"}}
 
@@ -694,21 +846,22 @@ def main():
     head = run_headline(torch, eff, lib, args, world, rank, local)
 
     secondary = []
-    if rank == 0 and world == 1 and args.secondary != "none":
+    if args.secondary != "none":
         want = {"npad60", "npad4096", "sweep", "magnus4096", "givens", "midsize"} if args.secondary == "all" else set(
             args.secondary.split(","))
         peaks = (hbm_peak, hbm_src)
-        if "npad60" in want:
+        single = rank == 0 and world == 1  # replicas-only paths: one GPU
+        if single and "npad60" in want:
             secondary.append(sec_npad60(torch, eff, lib, args, peaks))
-        if "npad4096" in want:
+        if single and "npad4096" in want:
             secondary.append(sec_npad4096(torch, eff, lib, args, peaks, args.npad4096_rotations or None))
-        if "sweep" in want:
-            secondary.append(sec_sweep(torch, eff, lib, args, peaks))
-        if "magnus4096" in want:
-            secondary.append(sec_magnus4096(torch, eff, lib, args, fp64))
-        if "givens" in want:
+        if "sweep" in want:  # sharded over the ranks when N > 1
+            secondary.append(sec_sweep(torch, eff, lib, args, peaks, world, rank))
+        if "magnus4096" in want:  # relay over the ranks when N > 1
+            secondary.append(sec_magnus4096(torch, eff, lib, args, fp64, world, rank))
+        if single and "givens" in want:
             secondary.append(sec_givens(torch, eff, lib, args, peaks))
-        if "midsize" in want:
+        if single and "midsize" in want:
             secondary.append(sec_midsize(torch, eff, lib, args, fp64))
 
     if rank == 0:
@@ -734,7 +887,9 @@ def main():
                        "parallelism": f"interval-sharded x{world}" if world > 1 else "single GPU",
                        "l2": "flushed between timed steps (256 MiB write, outside the events)"},
             "e2e": {"value": head["e2e"][0], "unit": "intervals/s", "h2d_bytes_per_step": head["e2e"][1],
-                    "d2h_bytes_per_step": head["e2e"][2]},
+                    "d2h_bytes_per_step": head["e2e"][2], "signals": "page-locked host array",
+                    "pageable_value": head["e2e_pageable"],
+                    "pageable_note": "same call with the plain pageable numpy signals a reference caller passes"},
             "gpu_launches": head["launches"],
             "clocks": head["clocks"],
             "roofline": {"bound": "fp64", "kernel": "magnus_fused_kernel", "achieved": achieved,

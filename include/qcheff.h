@@ -62,6 +62,10 @@ int qch_max_abs_batch_c128(const void* d_h, int64_t batch, int64_t n_elems, doub
 /* *d_nonherm = 0 iff H[x,y] == conj(H[y,x]) for all x, y (exact compare), else 1.
  * Selects the mirrored-column fast path of the rotation kernels. */
 int qch_hermitian_exact_c128(const void* d_h, int64_t n, int* d_nonherm, void* stream);
+/* HermitianOperator validation (operators.py:104-116) on the device:
+ * *d_defect = max |H - H^dag| with numpy's |z| (the caller compares it with
+ * 1e-12 * max_abs, as the reference). */
+int qch_hermitian_defect_c128(const void* d_h, int64_t n, double* d_defect, void* stream);
 
 /* givens_rotation_matrix (npad.py:101-123) for n_pairs (i, j) index pairs of
  * one operator.  d_pairs: int64[2*n_pairs].  d_params: double[8*n_pairs] =
@@ -77,7 +81,8 @@ int qch_givens_params_c128(const void* d_h, int64_t n, const int64_t* d_pairs, i
  * reference's sequential order, in one launch.  d_params as produced by
  * qch_givens_params_c128.  herm_exact selects mirrored column writes (valid
  * when qch_hermitian_exact_c128 reported 0).  d_u (nullable): accumulated
- * unitary, rows i, j updated like _apply_left (npad.py:244-251). */
+ * unitary, rows i, j updated like _apply_left (npad.py:244-251).  d_h may be
+ * NULL: only d_u is updated (sparse operators keep their CSR path). */
 int qch_npad_apply_rotations_c128(void* d_h, int64_t n, const int64_t* d_pairs, const double* d_params,
                                   int64_t n_pairs, int herm_exact, void* d_u, void* stream);
 
@@ -261,6 +266,10 @@ int qch_zgemm_batched(const void* d_a, const void* d_b, void* d_c, int64_t m, in
  * conjugate mirror (C is exactly Hermitian off the diagonal).  Contiguous
  * batch (stride n*n). */
 int qch_zgemm_herm_batched(const void* d_a, const void* d_b, void* d_c, int64_t n, int64_t batch, void* stream);
+/* Real DMMA products per complex product of the GEMMs above: 3 (Gauss / 3M,
+ * the default: 6 N^3 tensor flops per complex GEMM) or 4 (QCH_ZGEMM_3M=0:
+ * 8 N^3).  For roofline accounting. */
+int qch_zgemm_real_products(void);
 
 /* ------------------------------------------------ multi-GPU Magnus ------- */
 

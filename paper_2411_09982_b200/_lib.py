@@ -36,6 +36,7 @@ PROTOTYPES = {
     "qch_max_abs_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
     "qch_max_abs_batch_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "qch_hermitian_exact_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "qch_hermitian_defect_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
     "qch_givens_params_c128": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "qch_npad_apply_rotations_c128": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     "qch_npad_run_dense_c128": (
@@ -118,6 +119,7 @@ PROTOTYPES = {
     ),
     "qch_magnus_chain_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, P_int64, c_void_p]),
     "qch_zgemm_herm_batched": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
+    "qch_zgemm_real_products": (c_int, []),
 }
 
 QCH_OK = 0
@@ -226,6 +228,16 @@ def require_cuda():
     load()
     _cuda_ok = True
     return t
+
+
+def cuda_available() -> bool:
+    """True when a CUDA device and the library are usable (validation
+    helpers move large scans to the device; the hot paths require it)."""
+    try:
+        require_cuda()
+        return True
+    except RuntimeError:
+        return False
 
 
 def stream_ptr():

@@ -86,17 +86,41 @@ __global__ void max_abs_kernel(const double2* __restrict__ h, int64_t n, unsigne
   }
 }
 
-__global__ void hermitian_exact_kernel(const double2* __restrict__ h, int64_t n, int* flag) {
-  // sets *flag = 1 when some H[x,y] != conj(H[y,x])
-  int64_t total = n * n;
-  int bad = 0;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-    int64_t x = k / n, y = k - x * n;
-    if (y > x) continue;
-    double2 a = h[x * n + y], b = h[y * n + x];
-    if (!(a.x == b.x && a.y == -b.y)) bad = 1;
+// Hermiticity of a dense matrix, 32x32 tile pairs (R >= C) through shared
+// memory so both the tile and its mirror are read coalesced: *flag |= 1 when
+// some H[x,y] != conj(H[y,x]) (exact), and *defect (u64 bits of a
+// non-negative double, atomicMax) = max |H[x,y] - conj(H[y,x])| with numpy's
+// |z| (operators.py:104-116: max(abs(H - H^dag))).
+__global__ void __launch_bounds__(256) hermitian_tiles_kernel(const double2* __restrict__ h, int64_t n, int* flag,
+                                                              unsigned long long* defect) {
+  __shared__ double2 ta[32][33], tb[32][33];
+  // tile pair from the linear block index: row R, col C <= R
+  const int t = blockIdx.x;
+  int R = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((R + 1) * (R + 2) / 2 <= t) ++R;
+  while (R * (R + 1) / 2 > t) --R;
+  const int C = t - R * (R + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int64_t r = (int64_t)R * 32 + yy, c = (int64_t)C * 32 + tx;
+    ta[yy][tx] = (r < n && c < n) ? h[r * n + c] : make_double2(0.0, 0.0);
+    const int64_t r2 = (int64_t)C * 32 + yy, c2 = (int64_t)R * 32 + tx;
+    tb[yy][tx] = (r2 < n && c2 < n) ? h[r2 * n + c2] : make_double2(0.0, 0.0);
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+  __syncthreads();
+  int bad = 0;
+  double worst = 0.0;
+  for (int yy = ty; yy < 32; yy += 8) {
+    const double2 a = ta[yy][tx], b = tb[tx][yy];  // H[r, c] and H[c, r]
+    if (!(a.x == b.x && a.y == -b.y)) bad = 1;
+    worst = fmax(worst, np_cabs(a.x - b.x, a.y + b.y));
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && flag) atomicOr(flag, 1);
+  if (defect) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, off));
+    if ((threadIdx.x & 31) == 0 && worst > 0.0) atomicMax(defect, (unsigned long long)__double_as_longlong(worst));
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -139,7 +163,8 @@ __global__ void apply_rotations_kernel(double2* __restrict__ h, int64_t n, const
   const int64_t i = pairs[2 * p], j = pairs[2 * p + 1];
   const double c = params[8 * p];
   const cplx s = mkc(params[8 * p + 4], params[8 * p + 5]);
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h != nullptr && x < n;
+       x += (int64_t)gridDim.x * blockDim.x) {
     int q = pair_of[x];
     if (q < 0) {
       cplx ri = d2c(h[i * n + x]), rj = d2c(h[j * n + x]);
@@ -289,15 +314,28 @@ extern "C" int qch_max_abs_batch_c128(const void* d_h, int64_t batch, int64_t n_
   return QCH_OK;
 }
 
+static int hermitian_tiles(const void* d_h, int64_t n, int* d_flag, double* d_defect, cudaStream_t st) {
+  if (n <= 0) return QCH_OK;
+  const int64_t T = (n + 31) / 32;
+  const int64_t pairs = T * (T + 1) / 2;
+  if (pairs > INT32_MAX) return fail(QCH_ERR_UNSUPPORTED, "hermiticity check: matrix too large");
+  hermitian_tiles_kernel<<<(unsigned)pairs, 256, 0, st>>>((const double2*)d_h, n, d_flag,
+                                                          (unsigned long long*)d_defect);
+  QCH_LAUNCH_CHECK("hermitian_tiles_kernel");
+  note_launch(1);
+  return QCH_OK;
+}
+
 extern "C" int qch_hermitian_exact_c128(const void* d_h, int64_t n, int* d_nonherm, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   QCH_CUDA(cudaMemsetAsync(d_nonherm, 0, sizeof(int), st));
-  if (n <= 0) return QCH_OK;
-  int blocks = (int)std::min<int64_t>((n * n + 255) / 256, (int64_t)sm_count() * 8);
-  hermitian_exact_kernel<<<blocks, 256, 0, st>>>((const double2*)d_h, n, d_nonherm);
-  QCH_LAUNCH_CHECK("hermitian_exact_kernel");
-  note_launch(1);
-  return QCH_OK;
+  return hermitian_tiles(d_h, n, d_nonherm, nullptr, st);
+}
+
+extern "C" int qch_hermitian_defect_c128(const void* d_h, int64_t n, double* d_defect, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  QCH_CUDA(cudaMemsetAsync(d_defect, 0, sizeof(double), st));
+  return hermitian_tiles(d_h, n, nullptr, d_defect, st);
 }
 
 extern "C" int qch_givens_params_c128(const void* d_h, int64_t n, const int64_t* d_pairs, int64_t n_pairs,
@@ -445,21 +483,55 @@ extern "C" int qch_npad_run_dense_c128(void* d_h, int64_t n, const int32_t* d_ta
   }
   if (int rc = npad_state_init((const double2*)d_h, 1, cm, trows, rb.q, rb.c, rb.v, st)) return rc;
 
-  // one large full-diagonal chain: the whole GPU (cooperative, npad_coop.cu)
+  const int64_t audit_every = 100;  // UNITARY_CHECK_EVERY, npad.py:216
+  // one large full-diagonal chain: the whole GPU (cooperative, npad_coop.cu).
+  // With U tracking the chain pauses at every multiple of 100 rotations for
+  // the audit (npad.py:254-259) and resumes from a fresh row state.
   {
     const char* e = getenv("QCH_NPAD_COOP");
     const bool coop = e ? atoi(e) != 0 : n >= 1024;
-    if (coop && !trows && herm && d_u == nullptr && d_target == nullptr) {
-      long long ap = 0;
+    if (coop && !trows && herm && d_target == nullptr) {
+      Workspace wsd(st);
+      double* d_def = nullptr;
+      if (d_u) {
+        QCH_CUDA(wsd.alloc(sizeof(double)));
+        d_def = (double*)wsd.p;
+      }
+      long long total = 0;
       int stt = 0;
-      const int rc = npad_run_coop((double2*)d_h, ni, threshold, max_iter, cm.ek, rb.q, rb.c, rb.v, d_pivots,
-                                   d_pivots ? pivot_cap : 0, &ap, &stt, st);
-      if (rc == QCH_OK) {
-        *applied = ap;
+      bool ran = false;
+      while (true) {
+        long long limit = max_iter - total;
+        if (d_u) limit = std::min<long long>(limit, ((total / audit_every) + 1) * audit_every - total);
+        if (total > 0)
+          if (int rc = npad_state_init((const double2*)d_h, 1, cm, trows, rb.q, rb.c, rb.v, st)) return rc;
+        long long ap = 0;
+        const int rc = npad_run_coop((double2*)d_h, ni, threshold, limit, cm.ek, rb.q, rb.c, rb.v,
+                                     d_pivots ? d_pivots + 2 * std::min<long long>(total, pivot_cap) : nullptr,
+                                     d_pivots ? std::max<long long>(0, pivot_cap - total) : 0, &ap, &stt, st,
+                                     (double2*)d_u);
+        if (rc == QCH_ERR_UNSUPPORTED && !ran) break;  // the single-CTA driver below
+        if (rc != QCH_OK) return rc;
+        ran = true;
+        total += ap;
+        if (d_u && ap > 0 && total % audit_every == 0) {
+          if (int rc2 = qch_unitarity_defect_c128(d_u, 1, n, d_def, stream)) return rc2;
+          double defect = 0.0;
+          QCH_CUDA(cudaMemcpyAsync(&defect, d_def, sizeof(double), cudaMemcpyDeviceToHost, st));
+          QCH_CUDA(cudaStreamSynchronize(st));
+          if (!(defect <= 1e-10 * (double)n)) {
+            char buf[160];
+            snprintf(buf, sizeof buf, "accumulated unitary drift %.3e after %lld rotations", defect, total);
+            return fail(QCH_ERR_UNITARITY_DRIFT, buf);
+          }
+        }
+        if (stt == 0 || total >= max_iter) break;
+      }
+      if (ran) {
+        *applied = total;
         *converged = stt == 0 ? 1 : 0;
         return QCH_OK;
       }
-      if (rc != QCH_ERR_UNSUPPORTED) return rc;
     }
   }
 
@@ -475,7 +547,6 @@ extern "C" int qch_npad_run_dense_c128(void* d_h, int64_t n, const int32_t* d_ta
   job.applied = 0;
   job.status = 0;
   job.stats[0] = job.stats[1] = job.stats[2] = job.stats[3] = 0;
-  const int64_t audit_every = 100;  // UNITARY_CHECK_EVERY, npad.py:216
   Workspace ws2(st);
   double* d_defect = nullptr;
   if (d_u) {

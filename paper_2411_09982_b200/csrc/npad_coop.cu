@@ -59,6 +59,7 @@ struct CoopRec {
 
 struct CoopArgs {
   double2* h;
+  double2* u;          // nullable: accumulated unitary, rows i, j updated (npad.py:244-251)
   int n;
   int rows_per;        // rows (and columns) per CTA
   int ek;
@@ -344,6 +345,17 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
         cand_take(own, st);
       }
     }
+    // accumulated unitary: rows i, j of U on the own columns (_apply_left,
+    // npad.py:244-251; the same arithmetic as the single-CTA driver)
+    if (a.u != nullptr) {
+      double2* __restrict__ u = a.u;
+      for (int x = r0 + tid; x < r1; x += kCoopThreads) {
+        cplx ni, nj;
+        rotate_rows(c, s, d2c(u[(size_t)i * n + x]), d2c(u[(size_t)j * n + x]), &ni, &nj);
+        u[(size_t)i * n + x] = c2d(ni);
+        u[(size_t)j * n + x] = c2d(nj);
+      }
+    }
     // the 2x2 block entries, by the owners of columns i and j
     if (tid == 0) {
       if (i >= r0 && i < r1) {
@@ -479,7 +491,7 @@ size_t npad_coop_smem(int n, int rows_per) {
 // one CTA per SM is not possible.
 int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int ek, const double* q, const int* c,
                   const double2* v, int* pivots, long long pivot_cap, long long* applied, int* status,
-                  cudaStream_t st) {
+                  cudaStream_t st, double2* u) {
   int dev = 0, coop = 0;
   QCH_CUDA(cudaGetDevice(&dev));
   QCH_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
@@ -542,6 +554,7 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   QCH_CUDA(cudaMallocAsync(&ws, bytes, st));
   CoopArgs a;
   a.h = h;
+  a.u = u;
   a.n = n;
   a.rows_per = rows_per;
   a.ek = ek;

@@ -38,7 +38,7 @@ int npad_launch_trows_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cud
 int npad_launch_trows_cta(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st);
 int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int ek, const double* q, const int* c,
                   const double2* v, int* pivots, long long pivot_cap, long long* applied, int* status,
-                  cudaStream_t st);
+                  cudaStream_t st, double2* u = nullptr);
 bool npad_full_warp_ok(const NpadCommon2& cm, bool herm, bool trows);
 int npad_launch_full_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st);
 int npad_launch2(NpadJob2* jobs, int njobs, const NpadCommon2& cm, bool herm, bool trows, int pref_threads,

@@ -29,6 +29,9 @@ struct ZtArgs {
 int zt_gemm(int mode, bool herm, bool bh, const double2* a, const double2* b, int m, int n, int k, int64_t batch,
             int64_t sa, int64_t sb, ZtArgs g, cudaStream_t st);
 
+// true: 3 real DMMA products per complex product (default), false: 4
+bool zgemm_use_3m();
+
 // square / rectangular conveniences (zgemm.cu)
 int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, int64_t batch, int64_t sa, int64_t sb,
           int64_t sc, cudaStream_t st);

@@ -22,7 +22,13 @@
 // makes every 8-lane phase of a fragment LDS.128 hit 8 distinct 16-byte bank
 // groups (conflict free, no padding), for A, B and BH alike.
 //
-// Complex product = four real DMMAs: Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br.
+// Complex product: by default THREE real DMMA products (Gauss / 3M):
+//     P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi);  Re = P1 - P2,
+//     Im = P3 - P1 - P2
+// (6 N^3 DMMA flops per complex GEMM instead of 8 N^3; the error bound
+// grows from eps |A||B| componentwise to eps (|Ar|+|Ai|)(|Br|+|Bi|), ~1e-14
+// relative here — the parity bar is 1e-10).  QCH_ZGEMM_3M=0: four products,
+// Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br.
 //
 // Epilogues (fused):
 //   STORE   C = A B
@@ -94,7 +100,7 @@ __device__ __forceinline__ void zt_tile(int t, const ZtArgs& g, bool herm, int& 
   }
 }
 
-template <int MODE, bool HERM, bool BH>
+template <int MODE, bool HERM, bool BH, bool M3>
 __global__ void __launch_bounds__(ZT_THREADS, 1)
     zgemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, ZtArgs g) {
   extern __shared__ unsigned char zt_raw[];
@@ -117,7 +123,7 @@ __global__ void __launch_bounds__(ZT_THREADS, 1)
   __syncthreads();
 
   if (warp >= ZT_CONSUMERS) {  // ===== producer warpgroup: one TMA lane, runs ahead across tiles
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
     if (warp == ZT_CONSUMERS && lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(ZT_THREADS, 1)
   }
 
   // ===== consumers: warp (wm, wn) owns rows wm*32.., cols wn*32.. of the tile
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 240;" ::: "memory");
   const int wm = warp & 3, wn = warp >> 2;
   const int fr = lane >> 2, fk = lane & 3;
   int it = 0;
@@ -158,13 +164,17 @@ __global__ void __launch_bounds__(ZT_THREADS, 1)
     int ti, tj;
     zt_tile((int)(w % g.tiles), g, HERM, ti, tj);
     const int m0 = ti * ZT_BM, n0 = tj * ZT_BN;
-    double cr[4][4][2], ci[4][4][2];
+    // 4M: cr = Re, ci = Im.  M3 (Gauss): cr = Ar Br, p2 = Ai Bi,
+    // ci = (Ar + Ai)(Br + Bi) -> Re = cr - p2, Im = ci - cr - p2 (3 DMMAs
+    // per complex product instead of 4)
+    double cr[4][4][2], ci[4][4][2], p2[M3 ? 4 : 1][4][2];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 4; ++y) {
         cr[x][y][0] = cr[x][y][1] = 0.0;
         ci[x][y][0] = ci[x][y][1] = 0.0;
+        if (M3) p2[M3 ? x : 0][y][0] = p2[M3 ? x : 0][y][1] = 0.0;
       }
     for (int kt = 0; kt < KT; ++kt, ++it) {
       const int s = it % ZT_ST;
@@ -176,7 +186,7 @@ __global__ void __launch_bounds__(ZT_THREADS, 1)
         const int kl = 2 * fk + kk;  // complex column of this lane's k slot
         // B fragments of the 4 column tiles stay live; A fragments are loaded
         // one row tile at a time
-        double br[4], bi[4];
+        double br[4], bi[4], bs[4];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
           double2 v;
@@ -189,18 +199,30 @@ __global__ void __launch_bounds__(ZT_THREADS, 1)
           }
           br[nt] = v.x;
           bi[nt] = v.y;
+          if (M3) bs[nt] = v.x + v.y;
         }
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
           const int row = wm * 32 + mt * 8 + fr;
           const double2 v = *(const double2*)(As + row * 128 + ((kl ^ fr) << 4));
-          const double ar = v.x, ai = v.y, nai = -v.y;
+          const double ar = v.x, ai = v.y;
+          if (M3) {
+            const double as = v.x + v.y;
 #pragma unroll
-          for (int nt = 0; nt < 4; ++nt) {
-            zt_dmma(cr[mt][nt][0], cr[mt][nt][1], ar, br[nt]);
-            zt_dmma(ci[mt][nt][0], ci[mt][nt][1], ar, bi[nt]);
-            zt_dmma(cr[mt][nt][0], cr[mt][nt][1], nai, bi[nt]);
-            zt_dmma(ci[mt][nt][0], ci[mt][nt][1], ai, br[nt]);
+            for (int nt = 0; nt < 4; ++nt) {
+              zt_dmma(cr[mt][nt][0], cr[mt][nt][1], ar, br[nt]);
+              zt_dmma(p2[M3 ? mt : 0][nt][0], p2[M3 ? mt : 0][nt][1], ai, bi[nt]);
+              zt_dmma(ci[mt][nt][0], ci[mt][nt][1], as, bs[nt]);
+            }
+          } else {
+            const double nai = -v.y;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              zt_dmma(cr[mt][nt][0], cr[mt][nt][1], ar, br[nt]);
+              zt_dmma(ci[mt][nt][0], ci[mt][nt][1], ar, bi[nt]);
+              zt_dmma(cr[mt][nt][0], cr[mt][nt][1], nai, bi[nt]);
+              zt_dmma(ci[mt][nt][0], ci[mt][nt][1], ai, br[nt]);
+            }
           }
         }
       }
@@ -223,7 +245,12 @@ __global__ void __launch_bounds__(ZT_THREADS, 1)
           if (r >= g.m || c >= g.n) continue;
           if (HERM && r < c) continue;
           const bool mirror = HERM && r > c;
-          const double re = cr[mt][nt][e], im = ci[mt][nt][e];
+          double re = cr[mt][nt][e], im = ci[mt][nt][e];
+          if (M3) {
+            const double q2 = p2[M3 ? mt : 0][nt][e];
+            im = (im - re) - q2;
+            re = re - q2;
+          }
           const int64_t off = cb + (int64_t)r * g.ldc + c;
           const int64_t moff = cb + (int64_t)c * g.ldc + r;
           if (MODE == ZT_DEFECT) {
@@ -307,13 +334,13 @@ static const char* zt_name(int mode, bool herm) {
   }
 }
 
-template <int MODE, bool HERM, bool BH>
+template <int MODE, bool HERM, bool BH, bool M3>
 static int zt_launch(const CUtensorMap& ma, const CUtensorMap& mb, ZtArgs g, int64_t batch, cudaStream_t st) {
   const int smem = ZT_ST * ZT_STAGE + 2 * ZT_ST * 8 + 1024;
   static bool attr = false;
   if (!attr) {
-    QCH_CUDA(cudaFuncSetAttribute(zgemm_tma_kernel<MODE, HERM, BH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  smem));
+    QCH_CUDA(cudaFuncSetAttribute(zgemm_tma_kernel<MODE, HERM, BH, M3>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   g.tm = (g.m + ZT_BM - 1) / ZT_BM;
@@ -331,12 +358,22 @@ static int zt_launch(const CUtensorMap& ma, const CUtensorMap& mb, ZtArgs g, int
     g.nbatch = (int)std::min<int64_t>(batch - done, per);
     const int64_t work = (int64_t)g.tiles * g.nbatch;
     const int grid = (int)std::min<int64_t>(work, sm_count());  // persistent: one CTA per SM
-    zgemm_tma_kernel<MODE, HERM, BH><<<grid, ZT_THREADS, smem, st>>>(ma, mb, g);
+    zgemm_tma_kernel<MODE, HERM, BH, M3><<<grid, ZT_THREADS, smem, st>>>(ma, mb, g);
     QCH_LAUNCH_CHECK("zgemm_tma_kernel");
     note_launch(1);
   }
   prof_end(pr, st);
   return QCH_OK;
+}
+
+// 3 real DMMA products per complex product (Gauss / 3M) by default;
+// QCH_ZGEMM_3M=0 selects the 4-product form.
+bool zgemm_use_3m() {
+  static const bool v = [] {
+    const char* e = getenv("QCH_ZGEMM_3M");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  return v;
 }
 
 // Generic entry: C (m x n) = op(A (m x k) B (k x n)) for a contiguous batch.
@@ -358,8 +395,10 @@ int zt_gemm(int mode, bool herm, bool bh, const double2* a, const double2* b, in
   g.k = k;
   if (g.ldc == 0) g.ldc = n;
   if (g.sc == 0) g.sc = (int64_t)m * n;
-#define ZT_CASE(MD, H, B) \
-  if (mode == MD && herm == H && bh == B) return zt_launch<MD, H, B>(ma, mb, g, batch, st);
+  const bool m3 = zgemm_use_3m();
+#define ZT_CASE(MD, H, B)                                                                          \
+  if (mode == MD && herm == H && bh == B)                                                          \
+    return m3 ? zt_launch<MD, H, B, true>(ma, mb, g, batch, st) : zt_launch<MD, H, B, false>(ma, mb, g, batch, st);
   ZT_CASE(ZT_STORE, false, false)
   ZT_CASE(ZT_STORE, true, false)
   ZT_CASE(ZT_ACCUM, false, false)

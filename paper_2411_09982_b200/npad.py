@@ -260,26 +260,42 @@ def eliminate_couplings(state: NPADState, pairs: Sequence[tuple[int, int]]) -> N
     op = state.current
     for i, j in pairs:
         _check_pair(op, i, j)
-    if _is_sparse(op) and state.accumulated_unitary is None:
+    u_host = state.accumulated_unitary
+    # the reference audits U after every rotation that brings the count to a
+    # multiple of UNITARY_CHECK_EVERY (npad.py:290-296): apply the pairs in
+    # segments ending at those points, auditing after each
+    cuts = [k + 1 for k in range(len(pairs)) if (state.applied + k + 1) % UNITARY_CHECK_EVERY == 0]
+    bounds = sorted(set([0] + (cuts if u_host is not None else []) + [len(pairs)]))
+    if _is_sparse(op):
         # the reference's sparse branch: every rotation built from the input
-        # operator, applied in list order (npad.py:287-296)
+        # operator, applied in list order (npad.py:287-296); U (if tracked)
+        # is a dense device matrix updated by rows, the operator stays a CSR
         rots = [_sparse_rotation(op, i, j) for i, j in pairs]
+        d_u = _lib.to_device(u_host) if u_host is not None else None
         cur = op
-        for rot in rots:
-            cur = _sparse_transform(cur, rot)
-        return replace(state, current=cur, applied=state.applied + len(pairs))
+        for a, b in zip(bounds, bounds[1:]):
+            for rot in rots[a:b]:
+                cur = _sparse_transform(cur, rot)
+            if d_u is not None:
+                d_pairs = _lib.to_device(np.array([[r.i, r.j] for r in rots[a:b]], dtype=np.int64))
+                d_params = _lib.to_device(_params_from_rotations(rots[a:b]))
+                _lib.call("qch_npad_apply_rotations_c128", None, op.dim, _lib.dptr(d_pairs), _lib.dptr(d_params),
+                          b - a, 0, _lib.dptr(d_u), _lib.stream_ptr())
+                if (state.applied + b) % UNITARY_CHECK_EVERY == 0:
+                    _audit(d_u, state.applied + b, op.dim)
+        return replace(state, current=cur, applied=state.applied + len(pairs),
+                       accumulated_unitary=_lib.to_host(d_u) if d_u is not None else None)
     d_pairs, d_params, _, status = _device_params(op, pairs)
     bad = np.flatnonzero(status)
     if bad.size:
         i, j = pairs[int(bad[0])]
         raise ZeroCoupling(f"entry ({j}, {i}) is zero; nothing to eliminate")
-    new_op, new_u, d_u = _apply(op, d_pairs, d_params, len(pairs), state.accumulated_unitary)
-    applied = state.applied + len(pairs)
-    if d_u is not None:
-        # audit whenever a multiple of UNITARY_CHECK_EVERY was reached
-        if applied // UNITARY_CHECK_EVERY > state.applied // UNITARY_CHECK_EVERY:
-            _audit(d_u, applied, op.dim)
-    return replace(state, current=new_op, applied=applied, accumulated_unitary=new_u)
+    cur = op
+    for a, b in zip(bounds, bounds[1:]):
+        cur, u_host, d_u = _apply(cur, d_pairs[a:b].contiguous(), d_params[a:b].contiguous(), b - a, u_host)
+        if d_u is not None and (state.applied + b) % UNITARY_CHECK_EVERY == 0:
+            _audit(d_u, state.applied + b, op.dim)
+    return replace(state, current=cur, applied=state.applied + len(pairs), accumulated_unitary=u_host)
 
 
 def _target_tensor(target, dim: int):
