@@ -740,10 +740,17 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
   // with group waits) needs every block of the grid resident at once; a
   // cooperative launch guarantees that (or fails cleanly) even when other
   // kernels share the GPU.
-  {
+  // QCH_FUSED_COOP: 1 always, 0 never, 2 (default) for the static schedule
+  // only — there every block owns fixed tiles, so a non-resident block would
+  // stall the scan; the dynamic schedule hands tiles only to running blocks
+  // and keeps every group within half the grid
+  static const int coop_mode = getenv("QCH_FUSED_COOP") ? atoi(getenv("QCH_FUSED_COOP")) : 2;
+  if (coop_mode == 1 || (coop_mode == 2 && g.sched_static)) {
     void* kargs[] = {(void*)&g};
     QCH_CUDA(cudaLaunchCooperativeKernel((const void*)magnus_fused_kernel<N>, dim3(grid), dim3(kFusedThreads), kargs,
                                          smem, st));
+  } else {
+    magnus_fused_kernel<N><<<grid, kFusedThreads, smem, st>>>(g);
   }
   const auto tl2 = std::chrono::steady_clock::now();
   prof_end(pr, st);
@@ -837,7 +844,7 @@ void fused_carve(void* ws, int64_t N, int64_t M, int nlaunch, FusedArgs* g, int*
   *ctr = g->flag + nt;
   g->gflag = *ctr + nlaunch;
   g->gcount = g->gflag + nt;
-  g->sched_static = 0;
+  g->sched_static = 1;  // static round-robin tiles, cooperative launch (measured faster than dynamic grabbing)
   g->tstamp = nullptr;
   g->done_ctr = nullptr;  // set by the self-cleaning callers
   g->flags_out = nullptr;
