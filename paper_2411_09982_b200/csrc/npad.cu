@@ -545,7 +545,7 @@ extern "C" int qch_npad_run_dense_c128(void* d_h, int64_t n, const int32_t* d_ta
   job.pivot_cap = d_pivots ? pivot_cap : 0;
   job.threshold = threshold;
   job.applied = 0;
-  job.status = 0;
+  job.status = 3;  // not started
   job.stats[0] = job.stats[1] = job.stats[2] = job.stats[3] = 0;
   Workspace ws2(st);
   double* d_defect = nullptr;
@@ -590,7 +590,7 @@ __global__ void batch_jobs_kernel(NpadJob2* jobs, double2* h, int64_t n, const d
   j.pivot_cap = 0;
   j.threshold = thr[b];
   j.applied = 0;
-  j.status = 0;
+  j.status = 3;  // not started
   j.stats[0] = j.stats[1] = j.stats[2] = j.stats[3] = 0;
   jobs[b] = j;
 }
@@ -630,7 +630,34 @@ extern "C" int qch_npad_run_batch_c128(void* d_h, int64_t batch, int64_t n, cons
   batch_jobs_kernel<<<(int)((batch + 127) / 128), 128, 0, st>>>(rb.jobs, (double2*)d_h, n, d_thresholds, rb.q, rb.c,
                                                                    rb.v, per, batch);
   note_launch(1);
-  if (int rc = npad_launch2(rb.jobs, (int)batch, cm, true, trows, 256, false, st)) return rc;
+  // Sweeps: the chains run concurrently on the many-chain driver (one warp
+  // each) until at most one per SM is left; the survivors — the long chains
+  // that set the makespan — finish on the shared-memory T-rows driver (one
+  // CTA per chain, one global round trip per rotation).  A batch that fits
+  // one CTA per SM starts there.  QCH_NPAD_DRIVER forces one driver;
+  // QCH_NPAD_HANDOVER=k sets the hand-over point (0: never).
+  const char* drv = getenv("QCH_NPAD_DRIVER");
+  const size_t tsb = trows ? npad_tsmem_bytes(cm) : 0;
+  int handover = sm_count();
+  if (const char* e = getenv("QCH_NPAD_HANDOVER")) handover = atoi(e);
+  if (drv != nullptr && strcmp(drv, "tsmem") == 0) {
+    if (int rc = npad_launch_tsmem(rb.jobs, (int)batch, cm, st)) return rc;
+  } else if (drv == nullptr && tsb > 0 && handover > 0 && batch <= handover) {
+    if (int rc = npad_launch_tsmem(rb.jobs, (int)batch, cm, st)) return rc;
+  } else if (drv == nullptr && tsb > 0 && handover > 0) {
+    Workspace live(st);
+    QCH_CUDA(live.alloc(sizeof(int)));
+    const int nb = (int)batch;
+    QCH_CUDA(cudaMemcpyAsync(live.p, &nb, sizeof(int), cudaMemcpyHostToDevice, st));
+    NpadCommon2 c1 = cm;
+    c1.live = (int*)live.p;
+    c1.handover = handover;
+    if (int rc = npad_launch_trows_warp(rb.jobs, (int)batch, c1, st)) return rc;
+    if (int rc = npad_launch_tsmem(rb.jobs, (int)batch, cm, st)) return rc;
+    QCH_CUDA(cudaStreamSynchronize(st));  // (the counter's memory is released at scope exit)
+  } else {
+    if (int rc = npad_launch2(rb.jobs, (int)batch, cm, true, trows, 256, false, st)) return rc;
+  }
   batch_out_kernel<<<(int)((batch + 127) / 128), 128, 0, st>>>(rb.jobs, batch, d_applied, d_converged);
   QCH_LAUNCH_CHECK("batch_out_kernel");
   note_launch(1);

@@ -775,14 +775,15 @@ int npad_launch2(NpadJob2* jobs, int njobs, const NpadCommon2& cm, bool herm, bo
   int cpt, threads;
   shape_for(cm.n, pref_threads, &cpt, &threads);
   // many independent chains (the sweep): one warp per chain with lazy
-  // columns (npad_warp.cu); QCH_NPAD_DRIVER=warp|cta|block overrides (cta:
-  // npad_cta.cu, lower per-rotation latency when few chains run)
+  // columns (npad_warp.cu); QCH_NPAD_DRIVER=warp|cta|tsmem|block overrides
+  // (cta: npad_cta.cu; tsmem: npad_tsmem.cu, T-rows in shared memory)
   if (trows) {
     const char* d = getenv("QCH_NPAD_DRIVER");
     const char* wenv = getenv("QCH_NPAD_WARP");  // legacy switch: 1 = many-chain driver for any batch
     const bool many = wenv ? atoi(wenv) != 0 : njobs > 1;
     if (d != nullptr && strcmp(d, "warp") == 0) return npad_launch_trows_warp(jobs, njobs, cm, st);
     if (d != nullptr && strcmp(d, "cta") == 0) return npad_launch_trows_cta(jobs, njobs, cm, st);
+    if (d != nullptr && strcmp(d, "tsmem") == 0 && npad_tsmem_bytes(cm) > 0) return npad_launch_tsmem(jobs, njobs, cm, st);
     if ((d == nullptr || strcmp(d, "block") != 0) && many) return npad_launch_trows_warp(jobs, njobs, cm, st);
   }
   if (npad_full_warp_ok(cm, herm, trows)) return npad_launch_full_warp(jobs, njobs, cm, st);

@@ -29,6 +29,8 @@ struct NpadCommon2 {
   long long max_iter;
   long long stop_at;
   int stats;                 // 1: accumulate job->stats and printf them at exit
+  int* live = nullptr;       // many-chain drivers: chains not yet finished (device counter) ...
+  int handover = 0;          // ... pause (status 2) once it is <= handover (the low-latency driver takes over)
 };
 
 bool npad_use_trows(const NpadCommon2& cm, bool herm);
@@ -36,6 +38,8 @@ int npad_state_init(const double2* h, int64_t batch, const NpadCommon2& cm, bool
                     double2* v, cudaStream_t st);
 int npad_launch_trows_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st);
 int npad_launch_trows_cta(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st);
+size_t npad_tsmem_bytes(const NpadCommon2& cm);
+int npad_launch_tsmem(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st);
 int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int ek, const double* q, const int* c,
                   const double2* v, int* pivots, long long pivot_cap, long long* applied, int* status,
                   cudaStream_t st, double2* u = nullptr);

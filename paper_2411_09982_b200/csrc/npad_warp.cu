@@ -312,6 +312,11 @@ __global__ void __launch_bounds__(256, 1) npad_trows_warp_kernel(NpadJob2* __res
       status = 1;
       break;
     }
+    // hand the chain over to the low-latency driver once few chains are left
+    if (cm.live != nullptr && (applied & 15) == 0 && *(volatile int*)cm.live <= cm.handover) {
+      status = 2;
+      break;
+    }
     const int i = (int)(piv.cr >> 16), j = (int)(piv.cr & 0xffffu);
     const int t = s_kof[i] >= 0 ? i : j;
     const int kt = s_kof[t];
@@ -527,6 +532,7 @@ __global__ void __launch_bounds__(256, 1) npad_trows_warp_kernel(NpadJob2* __res
   if (lane == 0) {
     job->applied = applied;
     job->status = status;
+    if (cm.live != nullptr && status != 2) atomicSub(cm.live, 1);
     if (cm.stats) {
       job->stats[0] += rescans;
       job->stats[1] += cyc_sel;

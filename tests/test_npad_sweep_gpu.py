@@ -20,9 +20,10 @@ def E():
     return eff
 
 
-@pytest.fixture(params=["cta", "warp"])
+@pytest.fixture(params=["cta", "warp", "tsmem"])
 def warp_mode(request):
-    """Force a many-chain driver (npad_cta.cu / npad_warp.cu) even for one chain."""
+    """Force a many-chain driver (npad_cta.cu / npad_warp.cu / npad_tsmem.cu)
+    even for one chain."""
     old = os.environ.get("QCH_NPAD_DRIVER")
     os.environ["QCH_NPAD_DRIVER"] = request.param
     yield request.param
@@ -118,3 +119,32 @@ def test_config4_sweep_full_size(E):
         for b in range(0, 1024, 97):
             m = mats[b]
             assert bool(torch.equal(m, m.conj().T))
+
+
+@pytest.mark.parametrize("handover", ["40", "0", "1000"])
+def test_sweep_handover_to_shared_memory_driver(E, handover):
+    # 200 sweep points (dim 256): the warp driver runs every chain until
+    # <= handover are left, the T-rows-in-shared-memory driver finishes them
+    # (0: warp driver only; 1000: shared-memory driver from the start) — the
+    # same per-point results as npad_run on each operator, matrices bit for bit
+    old = os.environ.get("QCH_NPAD_HANDOVER")
+    os.environ["QCH_NPAD_HANDOVER"] = handover
+    try:
+        nq, nr = 4, 64
+        pts = E.sweep_points(20, 10)
+        tgt = E.sweep_target(nr)
+        res = E.npad_sweep_transmon(pts, nq, nr, tgt, tol=1e-12)
+    finally:
+        if old is None:
+            del os.environ["QCH_NPAD_HANDOVER"]
+        else:
+            os.environ["QCH_NPAD_HANDOVER"] = old
+    assert res.converged.all()
+    for k in (0, 57, 133, 199):
+        wq, al, wr, g = pts[k]
+        h = E.transmon_resonator_hamiltonian(nq, nr, omega_q=wq, alpha=al, omega_r=wr, g=g).data
+        ref = npad_oracle.run_incremental(h, tgt, tol=1e-12)
+        assert int(res.applied[k]) == ref["applied"]
+        assert rel_fro(res.operator(k).data, ref["h"]) <= TOL_F
+        single = E.npad_run(E.HermitianOperator(h), tgt, tol=1e-12)
+        np.testing.assert_array_equal(res.operator(k).data, single.current.data)
