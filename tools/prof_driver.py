@@ -1,6 +1,6 @@
 """Run ONE instance of a hot-path workload (after a warm-up) so ncu can
 capture its kernels:  python tools/prof_driver.py <case> [arg]
-cases: npad60 | npad4096 [max_iter] | sweep [points] | magnus2 [intervals] | magnus4096
+cases: npad60 | npad4096 [max_iter] | sweep [points] | magnus2 [intervals] | magnus4096 | zgemm4096 | herm4096
 """
 import sys
 from pathlib import Path
@@ -84,6 +84,20 @@ def main():
         tr = mg.evolve_device(ch, grid, 1, torch.from_numpy(psi0).cuda(), check=False, order=2)
         torch.cuda.synchronize()
         print("traj", tr.shape)
+    elif case in ("zgemm4096", "herm4096"):
+        from paper_2411_09982_b200 import _lib as lib
+
+        n = 4096
+        a = torch.randn(n, n, dtype=torch.complex128, device="cuda")
+        h = (a + a.mH) * 0.5
+        c = torch.empty_like(a)
+        for _ in range(2):
+            if case == "zgemm4096":
+                lib.call("qch_zgemm_batched", lib.dptr(h), lib.dptr(a), lib.dptr(c), n, n, n, 1, n * n, n * n, n * n,
+                         lib.stream_ptr())
+            else:
+                lib.call("qch_zgemm_herm_batched", lib.dptr(h), lib.dptr(h), lib.dptr(c), n, 1, lib.stream_ptr())
+        print(case, "done")
     torch.cuda.synchronize()
 
 

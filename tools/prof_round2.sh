@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round-2 profiling pass (run under gpurun, one GPU): launch list of the
+# headline bench + ncu --set full captures of each hot kernel -> gpurun_out/.
+O=gpurun_out
+mkdir -p $O
+NCU="ncu --clock-control none"
+$NCU --metrics gpu__time_duration.sum --csv --log-file $O/launches_bench.csv \
+    python bench.py --steps 3 --warmup 3 --secondary none > $O/launches_bench.out 2>&1
+$NCU --set full --import-source on -k regex:'magnus_fused' -s 1 -c 1 -o $O/magnus2 -f \
+    python tools/prof_driver.py magnus2 > $O/magnus2.out 2>&1
+$NCU --set full --import-source on -k regex:'zgemm_tma' -s 1 -c 1 -o $O/zgemm4096 -f \
+    python tools/prof_driver.py zgemm4096 > $O/zgemm4096.out 2>&1
+$NCU --set full --import-source on -k regex:'zgemm_tma' -s 1 -c 1 -o $O/herm4096 -f \
+    python tools/prof_driver.py herm4096 > $O/herm4096.out 2>&1
+$NCU --set full --import-source on -k regex:'zgemm_tma' -s 0 -c 6 -o $O/c5 -f \
+    python tools/prof_driver.py magnus4096 > $O/c5.out 2>&1
+$NCU --set full --import-source on -k regex:npad_tsmem -s 1 -c 1 -o $O/sweep128 -f \
+    python tools/prof_driver.py sweep 128 > $O/sweep128.out 2>&1
+$NCU --set full --import-source on -k regex:npad_trows_warp -s 1 -c 1 -o $O/sweep -f \
+    python tools/prof_driver.py sweep 1024 > $O/sweep.out 2>&1
+$NCU --set full --import-source on -k regex:npad_coop -s 1 -c 1 -o $O/npad4096 -f \
+    python tools/prof_driver.py npad4096 2000 > $O/npad4096.out 2>&1
+ls -la $O
