@@ -12,7 +12,7 @@ $NCU --set full --import-source on -k regex:'zgemm_tma' -s 1 -c 1 -o $O/zgemm409
     python tools/prof_driver.py zgemm4096 > $O/zgemm4096.out 2>&1
 $NCU --set full --import-source on -k regex:'zgemm_tma' -s 1 -c 1 -o $O/herm4096 -f \
     python tools/prof_driver.py herm4096 > $O/herm4096.out 2>&1
-$NCU --set full --import-source on -k regex:'zgemm_tma' -s 0 -c 6 -o $O/c5 -f \
+$NCU --set full --import-source on -k regex:'zgemm_tma' -s 3 -c 3 -o $O/c5 -f \
     python tools/prof_driver.py magnus4096 > $O/c5.out 2>&1
 $NCU --set full --import-source on -k regex:npad_tsmem -s 1 -c 1 -o $O/sweep128 -f \
     python tools/prof_driver.py sweep 128 > $O/sweep128.out 2>&1
@@ -20,4 +20,11 @@ $NCU --set full --import-source on -k regex:npad_trows_warp -s 1 -c 1 -o $O/swee
     python tools/prof_driver.py sweep 1024 > $O/sweep.out 2>&1
 $NCU --set full --import-source on -k regex:npad_coop -s 1 -c 1 -o $O/npad4096 -f \
     python tools/prof_driver.py npad4096 2000 > $O/npad4096.out 2>&1
+# summaries on the box (reports are large): markdown + per-kernel DRAM bytes
+python tools/ncu_summary.py $O/ncu_full_r02.md $O/magnus2.ncu-rep $O/zgemm4096.ncu-rep $O/herm4096.ncu-rep \
+    $O/c5.ncu-rep $O/sweep128.ncu-rep $O/sweep.ncu-rep $O/npad4096.ncu-rep > $O/summary.log 2>&1
+python tools/ncu_summary.py --launches $O/launches_bench_r02.md $O/launches_bench.csv >> $O/summary.log 2>&1
+cp profiles/ncu_traffic.json $O/ncu_traffic.json
+python tools/shard_probe.py > $O/shard_probe.txt 2>&1
+find $O -name '*.ncu-rep' -size +6M -delete
 ls -la $O
