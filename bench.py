@@ -492,7 +492,9 @@ def sec_sweep(torch, eff, lib, args, peaks, world=1, rank=0, n_points=1024):
     rot = int(round(sum_over_ranks(torch, rot_local, world)))
     all_conv = sum_over_ranks(torch, float(conv.all()), world) == world
     per = max_over_ranks(torch, sum(tot) / len(tot), world)
-    kms = max_over_ranks(torch, prof["npad_run_kernel"][0] / prof["npad_run_kernel"][1], world)
+    # kernel time per sweep (the warp driver, then the shared-memory driver
+    # for the tail: both record as npad_run_kernel)
+    kms = max_over_ranks(torch, prof["npad_run_kernel"][0] / len(tot), world)
     ach = 96 * n * rot / world / (kms * 1e-3) / 1e9  # per GPU
     # e2e: host (omega_q, alpha, omega_r, g) rows in -> per-point applied,
     # converged and final diagonal on the host (rank 0 gathers), through the
@@ -579,6 +581,7 @@ def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
     torch.cuda.synchronize()
     lib.profile_read(reset=True)
     lib.profile_enable(True)
+    fl0 = float(lib.load().qch_dmma_flops())
     if world == 1:
         mg.PHASE_TIMING = True
         ms = time_steps(torch, lambda: eff.evolve(ch, grid, n_int, psi0, order=2, check=False), 1, lambda: None, 1)
@@ -607,12 +610,10 @@ def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
     g_ms = max_over_ranks(torch, sum(v[0] for v in gk.values()), world)
     frac_h = _herm_fraction(n)
     rp = int(lib.load().qch_zgemm_real_products())  # real DMMA products per complex product (3M: 3)
-    # executed DMMA flops: one GEMM launch = one product for every interval
-    # of a chunk (one chain launch per chunk); the Hermitian kernels compute
-    # frac_h of the 8 N^3 of a complex product
-    chunks = max(1, prof.get("chain_grid_kernel", (0, 1))[1])
-    gemm_per_interval = {k: c / chunks for k, (_t, c) in gk.items()}
-    fl_exec = sum((frac_h if "herm" in k else 1.0) * 2.0 * rp * n**3 * c for k, c in gemm_per_interval.items()) * n_int
+    # executed DMMA flops, counted by the library per launch (computed tiles
+    # x 128 x 64 x K x 2 x real products), summed over the ranks
+    fl_exec = sum_over_ranks(torch, float(lib.load().qch_dmma_flops()) - fl0, world)
+    gemm_per_interval = {k: c for k, (_t, c) in gk.items()}  # launches (one per chunk of intervals)
     ach = fl_exec / world / (g_ms * 1e-3) / 1e12 if g_ms else None
     fl_ref = 17 * 8 * n**3
     cpu = None
@@ -640,15 +641,15 @@ def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
                     "h2d_bytes_per_step": int(grid.signals.nbytes + psi0.nbytes), "d2h_bytes_per_step": int(d2h),
                     "path": "evolve(host psi0, host grid) -> host trajectory" if world == 1
                             else "sharding.evolve_relay + gather -> host trajectory on rank 0"},
-            "gemms_per_interval": gemm_per_interval,
+            "gemm_launches": gemm_per_interval,
             "roofline": {"bound": "tensor", "kernel": "zgemm_tma_kernel (DMMA, TMA-fed)", "achieved": ach,
                          "peak": fp64.get("dmma"), "unit": "TFLOP/s",
                          "frac": (ach / fp64["dmma"]) if ach and fp64.get("dmma") else None,
                          "peak_kind": "FP64 DMMA (mma.sync f64) measured live; cuBLAS zgemm "
                                       f"{fp64.get('cublas_zgemm', 0):.1f} TFLOP/s on the same box",
-                         "flops_basis": f"executed DMMA flops: {2 * rp} N^3 per full complex GEMM ({rp} real "
-                                        "products per complex product), the computed share "
-                                        f"({frac_h:.3f}) of it for the Hermitian half-GEMMs",
+                         "flops_basis": f"executed DMMA flops as counted by the library (qch_dmma_flops): "
+                                        f"{2 * rp} N^3 per full complex GEMM ({rp} real products per complex "
+                                        f"product), ~{frac_h:.3f} of it for the Hermitian half-GEMMs",
                          "gemm_ms": g_ms,
                          "reference_equivalent_tflops": fl_ref * n_int / (dev_ms * 1e-3) / 1e12,
                          "flops_per_interval_executed": fl_exec / n_int,
@@ -678,17 +679,15 @@ def sec_midsize(torch, eff, lib, args, fp64, L=8, n_int=2048):
     step()
     lib.profile_read(reset=True)
     lib.profile_enable(True)
+    fl0 = float(lib.load().qch_dmma_flops())
     ms = time_steps(torch, step, 3, lambda: None, 1)
+    fl = (float(lib.load().qch_dmma_flops()) - fl0) / 3  # executed DMMA flops per step (library count)
     lib.profile_enable(False)
     prof = lib.profile_read(reset=True)
     per = sum(ms) / len(ms)
     g_ms = sum(v[0] for k, v in prof.items() if k.startswith("zgemm")) / 3
     rp = int(lib.load().qch_zgemm_real_products())
     frac_h = _herm_fraction(n)
-    chunks = max(1, prof.get("chain_cta64_kernel", prof.get("chain_grid_kernel", (0, 1)))[1] / 3)
-    # executed DMMA flops: every GEMM launch covers one chunk of intervals
-    fl = sum((frac_h if "herm" in k else 1.0) * 2 * rp * n**3 * v[1] / 3 for k, v in prof.items()
-             if k.startswith("zgemm")) * n_int / chunks
     ach = fl / (g_ms * 1e-3) / 1e12 if g_ms else None
     chain_ms = prof.get("chain_grid_kernel", (0.0, 1))[0] / 3
     # CPU: the oracle (numpy restatement of evolve, 18-term Taylor, order 2) on 8 intervals
@@ -832,11 +831,19 @@ def main():
 
     import torch
 
-    torch.cuda.set_device(local)
+    # QCH_BENCH_BACKEND=gloo + QCH_BENCH_SAME_GPU=1: dry-run the multi-rank
+    # paths with every rank on GPU 0 (functional check only, not a timing)
+    backend = os.environ.get("QCH_BENCH_BACKEND", "nccl")
+    dev = 0 if os.environ.get("QCH_BENCH_SAME_GPU") == "1" else local
+    torch.cuda.set_device(dev)
+    local = dev
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2411_09982_b200 as eff
     from paper_2411_09982_b200 import _lib as lib
 

@@ -270,6 +270,10 @@ int qch_zgemm_herm_batched(const void* d_a, const void* d_b, void* d_c, int64_t 
  * the default: 6 N^3 tensor flops per complex GEMM) or 4 (QCH_ZGEMM_3M=0:
  * 8 N^3).  For roofline accounting. */
 int qch_zgemm_real_products(void);
+/* Executed DMMA flops of every TMA-kernel GEMM launched by this process
+ * (computed tiles x 128 x 64 x K x 2 x real products; diagnostics: the
+ * bench's tensor-pipe roofline divides its increase by the GEMM time). */
+double qch_dmma_flops(void);
 
 /* ------------------------------------------------ multi-GPU Magnus ------- */
 

@@ -120,6 +120,7 @@ PROTOTYPES = {
     "qch_magnus_chain_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, P_int64, c_void_p]),
     "qch_zgemm_herm_batched": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
     "qch_zgemm_real_products": (c_int, []),
+    "qch_dmma_flops": (c_double, []),
 }
 
 QCH_OK = 0

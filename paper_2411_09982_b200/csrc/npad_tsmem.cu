@@ -153,7 +153,9 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
   long long rescans = 0;
   int clock = 0;
 
+  long long cyc[5] = {0, 0, 0, 0, 0};  // QCH_NPAD_STATS: select, row u + rotate, block best, fold, rescans
   while (true) {
+    const long long c0 = cm.stats ? clock64() : 0;
     // ---- selection (every warp, identical result)
     const int pl = warp_argmax(mine);
     Cand piv = cand_none();
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
       pivots[2 * applied] = i;
       pivots[2 * applied + 1] = j;
     }
+    const long long c1 = cm.stats ? clock64() : 0;
     // ---- the partner row u: the ONE global round trip (all loads in flight)
     constexpr int kMaxCpt = 8;  // n <= 2048
     double2 ru[kMaxCpt];
@@ -238,7 +241,9 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
     // H[j, i] is a candidate of T-row t
     const Block2 blk = rotate_block(c, s, mkc(hii, 0.0), cconj(v), v, mkc(hjj, 0.0));
     if (tid == 0) cand_take(pt, make_cand(c2d(blk.ji), ((unsigned)i << 16) | (unsigned)j, ek));
+    const long long c2 = cm.stats ? clock64() : 0;
     const Cand bt = block_best_s(pt, s_part, lane, warp);  // barrier: rows and folds visible
+    const long long c3 = cm.stats ? clock64() : 0;
     ++clock;
     if (tid == 0) {
       const double2 bii = c2d(blk.ii), bij = c2d(blk.ij), bji = c2d(blk.ji), bjj = c2d(blk.jj);
@@ -265,6 +270,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
     }
     unsigned rm = __ballot_sync(kFull, need);
     __syncthreads();  // 2x2 block, diagonal and clocks visible; s_part reusable
+    const long long c4 = cm.stats ? clock64() : 0;
     // ---- rescans of T-rows: shared memory only
     while (rm) {
       const int kr = __ffs(rm) - 1;
@@ -285,8 +291,21 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
       if (lane == kr) mine = br;
       __syncthreads();  // s_part reuse
     }
+    if (cm.stats) {
+      const long long c5 = clock64();
+      cyc[0] += c1 - c0;
+      cyc[1] += c2 - c1;
+      cyc[2] += c3 - c2;
+      cyc[3] += c4 - c3;
+      cyc[4] += c5 - c4;
+    }
     ++applied;
   }
+  if (cm.stats && tid == 0 && applied > 0)
+    printf("npad tsmem driver: chain %d: %lld rotations, %.2f rescans/rot, cycles/rot: select %.0f, row u + rotate "
+           "%.0f, block best %.0f, fold %.0f, rescans %.0f\n",
+           blockIdx.x, applied, (double)rescans / applied, (double)cyc[0] / applied, (double)cyc[1] / applied,
+           (double)cyc[2] / applied, (double)cyc[3] / applied, (double)cyc[4] / applied);
 
   // ---- write back: T-rows and their columns, then the lazy columns of the
   // rotated partner rows where they are the newer copy

@@ -379,6 +379,8 @@ extern "C" int qch_zgemm_batched(const void* d_a, const void* d_b, void* d_c, in
 
 extern "C" int qch_zgemm_real_products(void) { return zgemm_use_3m() ? 3 : 4; }
 
+extern "C" double qch_dmma_flops(void) { return dmma_flops_total(); }
+
 extern "C" int qch_zgemm_herm_batched(const void* d_a, const void* d_b, void* d_c, int64_t n, int64_t batch,
                                       void* stream) {
   if (n <= 0 || batch <= 0) return QCH_OK;

@@ -31,6 +31,8 @@ int zt_gemm(int mode, bool herm, bool bh, const double2* a, const double2* b, in
 
 // true: 3 real DMMA products per complex product (default), false: 4
 bool zgemm_use_3m();
+// executed DMMA flops of the TMA kernel since load (accounting)
+double dmma_flops_total();
 
 // square / rectangular conveniences (zgemm.cu)
 int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, int64_t batch, int64_t sa, int64_t sb,

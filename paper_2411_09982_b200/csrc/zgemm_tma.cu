@@ -45,6 +45,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
+
 #include "zgemm.h"
 
 namespace qch {
@@ -334,6 +336,11 @@ static const char* zt_name(int mode, bool herm) {
   }
 }
 
+// executed DMMA flops of every launch (roofline accounting, qch_dmma_flops):
+// computed tiles x 128 x 64 complex outputs x K x (2 x real products)
+static std::atomic<double> g_dmma_flops{0.0};
+double dmma_flops_total() { return g_dmma_flops.load(); }
+
 template <int MODE, bool HERM, bool BH, bool M3>
 static int zt_launch(const CUtensorMap& ma, const CUtensorMap& mb, ZtArgs g, int64_t batch, cudaStream_t st) {
   const int smem = ZT_ST * ZT_STAGE + 2 * ZT_ST * 8 + 1024;
@@ -358,6 +365,12 @@ static int zt_launch(const CUtensorMap& ma, const CUtensorMap& mb, ZtArgs g, int
     g.nbatch = (int)std::min<int64_t>(batch - done, per);
     const int64_t work = (int64_t)g.tiles * g.nbatch;
     const int grid = (int)std::min<int64_t>(work, sm_count());  // persistent: one CTA per SM
+    {
+      const double f = (double)work * ZT_BM * ZT_BN * (double)g.k * 2.0 * (M3 ? 3.0 : 4.0);
+      double cur = g_dmma_flops.load();
+      while (!g_dmma_flops.compare_exchange_weak(cur, cur + f)) {
+      }
+    }
     zgemm_tma_kernel<MODE, HERM, BH, M3><<<grid, ZT_THREADS, smem, st>>>(ma, mb, g);
     QCH_LAUNCH_CHECK("zgemm_tma_kernel");
     note_launch(1);

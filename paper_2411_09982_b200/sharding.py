@@ -150,7 +150,7 @@ class ShardedEvolvePlan:
             _lib.dptr(self.sig), self.sig.shape[1], self.dt, self.dt_int, self.m_local, self.order,
             1 if self.check_u else 0, _lib.dptr(self.work), _lib.dptr(self.block), sp))
         if self.world > 1:
-            dist.all_gather_into_tensor(self.blocks, self.block, group=self.group)
+            dist.all_gather_into_tensor(self.blocks.view(-1), self.block.view(-1), group=self.group)
         else:
             self.blocks[0].copy_(self.block)
         _lib.check(lib.qch_magnus_apply_prefix_c128(_lib.dptr(self.blocks), self.n, self.rank, _lib.dptr(self.psi0),
@@ -263,6 +263,25 @@ class DeviceRelayCompute:
 _ERRCODE = {9: NormDrift}
 
 
+def _p2p(op, tensor, peer, group):
+    """send / recv of a device tensor; backends without device-memory
+    point-to-point (gloo) go through a host copy."""
+    import torch.distributed as dist
+
+    if tensor.is_cuda and dist.get_backend(group) != "nccl":
+        host = tensor.cpu()
+        if op == "send":
+            dist.send(host, dst=peer, group=group)
+        else:
+            dist.recv(host, src=peer, group=group)
+            tensor.copy_(host)
+        return
+    if op == "send":
+        dist.send(tensor, dst=peer, group=group)
+    else:
+        dist.recv(tensor, src=peer, group=group)
+
+
 @dataclass
 class RelayResult:
     num_intervals: int
@@ -357,7 +376,7 @@ def evolve_relay(ch, grid, num_intervals: int, psi0, *, order: int = 1, check: b
         elif world == 1:
             psi_in, in_err = carry
         else:
-            dist.recv(msg, src=(k - 1) % world, group=group)
+            _p2p("recv", msg, (k - 1) % world, group)
             st = complex(msg[n].item())
             psi_in = msg[:n].clone()
             in_err = None if st.real == 0 else (int(st.real), int(st.imag), "relayed")
@@ -377,7 +396,7 @@ def evolve_relay(ch, grid, num_intervals: int, psi0, *, order: int = 1, check: b
             else:
                 msg[:n].copy_(psi_out)
                 msg[n] = complex(err[0], err[1]) if err is not None else 0j
-                dist.send(msg, dst=(k + 1) % world, group=group)
+                _p2p("send", msg, (k + 1) % world, group)
     if err is not None:
         from .errors import NonFinite
 
