@@ -136,9 +136,11 @@ int qch_npad_sparse_entries_c128(const int64_t* d_indptr, const int32_t* d_indic
 /* Device-side builder of the transmon (x) resonator Hamiltonians of the NPAD
  * configs: for each b, params[4b..4b+3] =
  * {omega_q, alpha, omega_r, g}; H = wq n + a/2 n(n-1) (x) I + I (x) wr a^dag a
- * + g (b + b^dag) (x) (a + a^dag), index q*n_r + k.  d_h: (batch, nq*nr)^2. */
+ * + g (b + b^dag) (x) (a + a^dag), index q*n_r + k.  d_h: (batch, nq*nr)^2.
+ * d_maxabs (nullable): double[batch] = max_abs of each operator
+ * (operators.py:92-99), formed while the entries are written. */
 int qch_build_transmon_resonator_c128(void* d_h, int64_t batch, int64_t n_q, int64_t n_r,
-                                      const double* d_params, void* stream);
+                                      const double* d_params, double* d_maxabs, void* stream);
 /* spin_chain_hamiltonians (models.py:288-325), the drift built on the device
  * as a CSR: d_indptr (2^L + 1) int64, d_indices / d_data (capacity 2^L; the
  * diagonal's exact zeros are not stored, as scipy's diags -> csr drops them),

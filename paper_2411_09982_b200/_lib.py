@@ -47,7 +47,7 @@ PROTOTYPES = {
         c_int,
         [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p],
     ),
-    "qch_build_transmon_resonator_c128": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p]),
+    "qch_build_transmon_resonator_c128": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
     "qch_magnus_coefficients": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_double, c_int, c_void_p, c_void_p, c_void_p]),
     "qch_magnus_commutators_c128": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "qch_magnus_assemble_c128": (

@@ -235,31 +235,45 @@ __global__ void set_mask_kernel(unsigned char* mask, const int* tlist, int nt) {
 
 // ----------------------------------------------------------------------------
 // transmon (x) resonator builder
-__global__ void build_tr_kernel(double2* __restrict__ h, int64_t nq, int64_t nr, const double* __restrict__ prm) {
-  const int64_t n = nq * nr;
+__global__ void __launch_bounds__(256) build_tr_kernel(double2* __restrict__ h, int nq, int nr,
+                                                       const double* __restrict__ prm,
+                                                       unsigned long long* __restrict__ maxabs) {
+  // block (x, item): rows r = x, x + gridDim.x, ...; threads stride the
+  // columns (coalesced rows, 32-bit index math, no 64-bit divisions)
+  const int n = nq * nr;
   const int64_t b = blockIdx.y;
   const double wq = prm[4 * b], al = prm[4 * b + 1], wr = prm[4 * b + 2], g = prm[4 * b + 3];
-  double2* hb = h + b * n * n;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n * n; k += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = k / n, c = k - r * n;
-    int64_t q1 = r / nr, k1 = r - q1 * nr, q2 = c / nr, k2 = c - q2 * nr;
-    double v = 0.0;
-    if (r == c) {
-      // host builder (models.transmon_resonator_hamiltonian): n = b^dag b has
-      // diagonal sqrt(q)^2 (not exactly q), a^dag a likewise; same op order.
-      double sq = sqrt((double)q1), sk = sqrt((double)k1);
-      double nn = QMUL(sq, sq), kk = QMUL(sk, sk);
-      double hq = QADD(QMUL(wq, nn), QMUL(QMUL(0.5, al), QMUL(nn, QSUB(nn, 1.0))));
-      v = QADD(hq, QMUL(wr, kk));
-    } else {
-      int64_t dq = q1 - q2, dk = k1 - k2;
-      if ((dq == 1 || dq == -1) && (dk == 1 || dk == -1)) {
-        double bq = sqrt((double)(q1 > q2 ? q1 : q2));
-        double ak = sqrt((double)(k1 > k2 ? k1 : k2));
-        v = QMUL(g, QMUL(bq, ak));
+  double2* hb = h + b * (int64_t)n * n;
+  double m = 0.0;
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int q1 = r / nr, k1 = r - q1 * nr;
+    double2* row = hb + (int64_t)r * n;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      const int q2 = c / nr, k2 = c - q2 * nr;
+      double v = 0.0;
+      if (r == c) {
+        // host builder (models.transmon_resonator_hamiltonian): n = b^dag b has
+        // diagonal sqrt(q)^2 (not exactly q), a^dag a likewise; same op order.
+        const double sq = sqrt((double)q1), sk = sqrt((double)k1);
+        const double nn = QMUL(sq, sq), kk = QMUL(sk, sk);
+        const double hq = QADD(QMUL(wq, nn), QMUL(QMUL(0.5, al), QMUL(nn, QSUB(nn, 1.0))));
+        v = QADD(hq, QMUL(wr, kk));
+      } else {
+        const int dq = q1 - q2, dk = k1 - k2;
+        if ((dq == 1 || dq == -1) && (dk == 1 || dk == -1)) {
+          const double bq = sqrt((double)(q1 > q2 ? q1 : q2));
+          const double ak = sqrt((double)(k1 > k2 ? k1 : k2));
+          v = QMUL(g, QMUL(bq, ak));
+        }
       }
+      row[c] = make_double2(v, 0.0);
+      m = fmax(m, fabs(v));  // numpy |v + 0j| = |v|
     }
-    hb[k] = make_double2(v, 0.0);
+  }
+  if (maxabs != nullptr) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(maxabs + b, (unsigned long long)__double_as_longlong(m));
   }
 }
 
@@ -381,16 +395,22 @@ extern "C" int qch_npad_apply_rotations_c128(void* d_h, int64_t n, const int64_t
 }
 
 extern "C" int qch_build_transmon_resonator_c128(void* d_h, int64_t batch, int64_t n_q, int64_t n_r,
-                                                 const double* d_params, void* stream) {
+                                                 const double* d_params, double* d_maxabs, void* stream) {
   if (batch <= 0) return QCH_OK;
   if (n_q < 1 || n_r < 1) return fail(QCH_ERR_VALUE, "need n_q, n_r >= 1");
+  if (n_q * n_r >= 65536) return fail(QCH_ERR_UNSUPPORTED, "builder: dimension must be < 65536");
   cudaStream_t st = (cudaStream_t)stream;
-  int64_t n = n_q * n_r;
-  int bx = (int)std::min<int64_t>((n * n + 255) / 256, std::max<int64_t>(1, (int64_t)sm_count() * 8 / batch + 1));
-  dim3 grid(bx, (unsigned)batch);
-  build_tr_kernel<<<grid, 256, 0, st>>>((double2*)d_h, n_q, n_r, d_params);
-  QCH_LAUNCH_CHECK("build_tr_kernel");
-  note_launch(1);
+  const int n = (int)(n_q * n_r);
+  if (d_maxabs) QCH_CUDA(cudaMemsetAsync(d_maxabs, 0, sizeof(double) * batch, st));
+  const int bx = (int)std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)sm_count() * 16 / batch + 1));
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = std::min<int64_t>(batch - b0, 65535);
+    build_tr_kernel<<<dim3(bx, (unsigned)nb), 256, 0, st>>>((double2*)d_h + b0 * (int64_t)n * n, (int)n_q, (int)n_r,
+                                                           d_params + 4 * b0,
+                                                           (unsigned long long*)(d_maxabs ? d_maxabs + b0 : nullptr));
+    QCH_LAUNCH_CHECK("build_tr_kernel");
+    note_launch(1);
+  }
   return QCH_OK;
 }
 

@@ -558,25 +558,27 @@ def npad_run_batch(ops: Sequence[HermitianOperator], target=None, *, tol: float,
                        np.concatenate([p[3] for p in parts]))
 
 
-def build_transmon_resonator_batch(params: np.ndarray, n_q: int, n_r: int):
+def build_transmon_resonator_batch(params: np.ndarray, n_q: int, n_r: int, *, with_max_abs: bool = False):
     """Device-built transmon (x) resonator Hamiltonians, one per row of
     ``params`` = (omega_q, alpha, omega_r, g).  Same matrix as
-    models.transmon_resonator_hamiltonian."""
+    models.transmon_resonator_hamiltonian.  ``with_max_abs``: also return
+    each operator's max |H| (formed by the builder, no extra pass)."""
     t = _lib.require_cuda()
     params = np.ascontiguousarray(params, dtype=np.float64).reshape(-1, 4)
     b = params.shape[0]
     n = n_q * n_r
     mats = t.empty((b, n, n), dtype=t.complex128, device="cuda")
+    mx = t.empty(b, dtype=t.float64, device="cuda") if with_max_abs else None
     d_prm = _lib.to_device(params)
-    _lib.call("qch_build_transmon_resonator_c128", _lib.dptr(mats), b, n_q, n_r, _lib.dptr(d_prm), _lib.stream_ptr())
-    return mats
+    _lib.call("qch_build_transmon_resonator_c128", _lib.dptr(mats), b, n_q, n_r, _lib.dptr(d_prm), _lib.dptr(mx),
+              _lib.stream_ptr())
+    return (mats, mx) if with_max_abs else mats
 
 
 def npad_sweep_transmon(params: np.ndarray, n_q: int, n_r: int, target=None, *, tol: float,
                         max_iter: int | None = None) -> BatchResult:
     """Parameter sweep of config 4: build every (omega_q, alpha, omega_r, g)
     point on the device and run the batched greedy NPAD (new API)."""
-    t = _lib.require_cuda()
-    mats = build_transmon_resonator_batch(params, n_q, n_r)
-    applied, conv = _run_batch_inplace(mats, target, tol, max_iter, max_abs_batch(mats))
+    mats, mx = build_transmon_resonator_batch(params, n_q, n_r, with_max_abs=True)
+    applied, conv = _run_batch_inplace(mats, target, tol, max_iter, mx)
     return BatchResult([(0, mats)], _lib.to_host(applied), _lib.to_host(conv).astype(bool))

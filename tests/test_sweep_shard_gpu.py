@@ -61,6 +61,14 @@ def test_max_abs_batch_matches_single(E):
     for k in range(mats.shape[0]):
         assert got[k] == E.HermitianOperator(mats[k].cpu().numpy()).max_abs()
     assert isinstance(mats, torch.Tensor)
+    # the builder's own max (formed while writing) and its matrices equal the host builder
+    pts = E.sweep_points(4, 4)
+    m2, mx = npad.build_transmon_resonator_batch(pts, 4, 64, with_max_abs=True)
+    for k in (0, 7, 15):
+        wq, al, wr, g = pts[k]
+        host = E.transmon_resonator_hamiltonian(4, 64, omega_q=wq, alpha=al, omega_r=wr, g=g).data
+        np.testing.assert_array_equal(m2[k].cpu().numpy(), host)
+        assert float(mx[k].item()) == float(np.max(np.abs(host)))
 
 
 def _free_port():
