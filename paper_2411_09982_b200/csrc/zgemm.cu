@@ -1,4 +1,6 @@
-// zgemm.cu — batched complex128 GEMM on the FP64 tensor pipe of sm_100a.
+// zgemm.cu — the round-1 cp.async DMMA GEMM (kept for A/B comparison with
+// QCH_ZGEMM=cpasync) and the dispatchers onto the TMA kernel (zgemm_tma.cu),
+// the default.
 //
 // sm_100a has no tcgen05 kind::f64, so FP64 tensor work is the warp-level
 // DMMA (mma.sync.aligned.m8n8k4 f64 -> SASS DMMA.8x8x4).  Complex operands stay
@@ -12,9 +14,6 @@
 //
 // Epilogues (fused, no extra pass over C):
 //   STORE   C = A op(B)
-//   TAYLOR  T = (A B) * (1/k); O += T        (expm.py:66-68: term = term@a/k;
-//                                             out = out + term; numpy divides a
-//                                             complex by k as x*(1/k))
 //   DEFECT  sum |(A B^H) - I|^2 into a per-batch accumulator (unitarity audit,
 //           npad.py:257, expm.py:35-38)
 //   ACCUM   C += A B   (Paterson-Stockmeyer Horner steps of exp(-iH))
@@ -24,18 +23,16 @@
 
 namespace qch {
 
-enum { ZG_STORE = 0, ZG_TAYLOR = 1, ZG_DEFECT = 2, ZG_ACCUM = 3 };
+enum { ZG_STORE = 0, ZG_DEFECT = 2, ZG_ACCUM = 3 };
 
 struct ZgemmArgs {
   const double2* a;
   const double2* b;
-  double2* c;   // STORE: C; TAYLOR: T (new term)
-  double2* o;   // TAYLOR: accumulated series
+  double2* c;   // STORE / ACCUM: C
   double* acc;  // DEFECT: per-batch sum of squares
   int m, n, k;
   int64_t sa, sb, sc;  // batch strides (elements)
   int lda, ldb, ldc;
-  double inv_k;
 };
 
 constexpr int BM = 64, BN = 64, BK = 8, STAGES = 3;
@@ -190,11 +187,6 @@ __global__ void __launch_bounds__(128) zgemm_kernel(ZgemmArgs g) {
         } else if (MODE == ZG_ACCUM) {
           const double2 o = g.c[off];
           g.c[off] = make_double2(o.x + re, o.y + im);
-        } else if (MODE == ZG_TAYLOR) {
-          double tr = QMUL(re, g.inv_k), ti = QMUL(im, g.inv_k);
-          g.c[off] = make_double2(tr, ti);
-          double2 o = g.o[off];
-          g.o[off] = make_double2(QADD(o.x, tr), QADD(o.y, ti));
         } else {
           double dr = re - (r == cidx ? 1.0 : 0.0);
           dsum += dr * dr + im * im;
@@ -230,11 +222,9 @@ static int zgemm_launch(const ZgemmArgs& g, int64_t batch, cudaStream_t st) {
     h.a += done * g.sa;
     h.b += done * g.sb;
     if (h.c) h.c += done * g.sc;
-    if (h.o) h.o += done * g.sc;
     if (h.acc) h.acc += done;
     dim3 grid((g.n + BN - 1) / BN, (g.m + BM - 1) / BM, (unsigned)nb);
-    void* pr = prof_begin(MODE == ZG_TAYLOR   ? "zgemm_taylor"
-                          : MODE == ZG_STORE  ? "zgemm"
+    void* pr = prof_begin(MODE == ZG_STORE    ? "zgemm"
                           : MODE == ZG_ACCUM  ? "zgemm_accum"
                                               : "zgemm_defect",
                           st);
