@@ -122,6 +122,14 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // acquire/release fence at gpu scope (lighter than __threadfence()'s
 // sequentially consistent fence)
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// arrival at a group counter with release semantics (the aggregate stored
+// before it is visible to the group's leader): one round trip instead of a
+// fence followed by a relaxed atomic
+__device__ __forceinline__ int atom_add_release(int* p, int v) {
+  int old;
+  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -518,8 +526,7 @@ __global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
       if (lane == 0) {
         s_red[0] = x;  // the tile aggregate
         stcg_mat<N>(g.agg + t * N * N, x);
-        fence_acq_rel();  // release: the aggregate before the arrival
-        last = atomicAdd(g.gcount + gi, 1) == gsize - 1;  // last arrival of the group leads it
+        last = atom_add_release(g.gcount + gi, 1) == gsize - 1;  // last arrival of the group leads it
       }
       __syncwarp();
     }

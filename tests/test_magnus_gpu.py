@@ -290,3 +290,23 @@ def test_config5_order2_vs_oracle(E):
     # the second-order term is small at this grid spacing (dt = 25/4096) but
     # well above the tolerance: order 1 misses the golden by ~4e-9
     assert rel_fro(got1.amplitudes, gm["traj"]) > 10 * 1e-10
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_return_propagators_large_dim_vs_oracle(E, order):
+    # N = 64 (DMMA path): evolve(..., return_propagators=True) returns the
+    # reference's list of UnitaryPropagator (magnus.py:262-266), each equal to
+    # the oracle's exp(-i Hbar_n); check=True validates every one
+    ch = E.heisenberg_chain_hamiltonians(6)
+    grid = E.synthetic_transfer_pulse(3.0, 12 * 4 + 1, seed=11)
+    psi0 = np.zeros(64, dtype=complex)
+    psi0[0] = 1
+    traj, props = E.evolve(ch, grid, 12, psi0, order=order, check=True, return_propagators=True)
+    d0 = ch.drift.to_dense()
+    ctr = np.stack([c.to_dense() for c in ch.controls])
+    ref_traj, ref_u = magnus_oracle.evolve(d0, ctr, grid.signals, grid.t_start, grid.t_end, 12, psi0, order=order,
+                                           return_propagators=True)
+    assert len(props) == 12 and all(isinstance(p, E.UnitaryPropagator) for p in props)
+    assert rel_fro(np.stack([p.entries for p in props]), ref_u) <= 1e-12
+    assert rel_fro(traj.amplitudes, ref_traj) <= 1e-10
+    assert np.array_equal(traj.times, np.linspace(grid.t_start, grid.t_end, 13))
