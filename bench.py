@@ -557,13 +557,46 @@ def _herm_fraction(n, bm=128, bn=64):
     return sum(min(2 * r + 2, tn) for r in range(tm)) / (tm * tn)
 
 
+def _oz_pairs():
+    s = int(os.environ.get("QCH_OZ_SLICES", "8"))
+    return s * (s + 1) // 2
+
+
+def _dmma_sample(torch, eff, lib, ch, grid_full, psi0, n_int=32):
+    """The DMMA engine on the first n_int intervals of config 5 (the FP64
+    tensor-pipe roofline of the north star; the default engine is int8)."""
+    from paper_2411_09982_b200 import magnus as mg
+
+    old = lib.load().qch_set_herm_gemm(0)
+    try:
+        g = eff.ControlGrid(0.0, 25.0 * n_int / 4096, grid_full.signals[:, : n_int * 8 + 1])
+        d_psi = lib.to_device(psi0)
+        mg.evolve_device(ch, g, n_int, d_psi, check=False, order=2)  # warm-up (allocations)
+        torch.cuda.synchronize()
+        lib.profile_read(reset=True)
+        lib.profile_enable(True)
+        f0 = float(lib.load().qch_dmma_flops())
+        ms = time_steps(torch, lambda: mg.evolve_device(ch, g, n_int, d_psi, check=False, order=2), 1, lambda: None,
+                        1)[0]
+        fl = float(lib.load().qch_dmma_flops()) - f0
+        lib.profile_enable(False)
+        prof = lib.profile_read(reset=True)
+    finally:
+        lib.load().qch_set_herm_gemm(old)
+    g_ms = sum(v[0] for k, v in prof.items() if k.startswith("zgemm"))
+    return {"intervals": n_int, "intervals_per_s": n_int / (ms * 1e-3), "gemm_ms": g_ms,
+            "achieved_tflops": fl / (g_ms * 1e-3) / 1e12 if g_ms else None}
+
+
 def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
     """Config 5 at its stated size: Magnus order 2 on the 12-spin Heisenberg
     chain (dim 4096), ALL 4096 intervals.  One GPU: the public evolve()
     (host psi0 + signals in, host trajectory out), its device phase timed
     with CUDA events (value) and the whole call (e2e).  N GPUs: the relay
     (sharding.evolve_relay, chunks round-robin, psi passed rank to rank) +
-    the trajectory gather to the host."""
+    the trajectory gather to the host.  The Hermitian products run on the
+    int8 tensor cores (Ozaki slices, tcgen05) — the default engine; a
+    32-interval sample on the DMMA engine is reported beside it."""
     from oracle import expm_oracle
     from paper_2411_09982_b200 import magnus as mg
     from paper_2411_09982_b200 import sharding
@@ -582,6 +615,7 @@ def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
     lib.profile_read(reset=True)
     lib.profile_enable(True)
     fl0 = float(lib.load().qch_dmma_flops())
+    op0 = float(lib.load().qch_int8_ops())
     if world == 1:
         mg.PHASE_TIMING = True
         ms = time_steps(torch, lambda: eff.evolve(ch, grid, n_int, psi0, order=2, check=False), 1, lambda: None, 1)
@@ -606,20 +640,45 @@ def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
         d2h = (n_int + 1) * n * 16
     lib.profile_enable(False)
     prof = lib.profile_read(reset=True)
-    gk = {k: v for k, v in prof.items() if k.startswith("zgemm")}
-    g_ms = max_over_ranks(torch, sum(v[0] for v in gk.values()), world)
-    frac_h = _herm_fraction(n)
-    rp = int(lib.load().qch_zgemm_real_products())  # real DMMA products per complex product (3M: 3)
-    # executed DMMA flops, counted by the library per launch (computed tiles
-    # x 128 x 64 x K x 2 x real products), summed over the ranks
-    fl_exec = sum_over_ranks(torch, float(lib.load().qch_dmma_flops()) - fl0, world)
-    gemm_per_interval = {k: c for k, (_t, c) in gk.items()}  # launches (one per chunk of intervals)
-    ach = fl_exec / world / (g_ms * 1e-3) / 1e12 if g_ms else None
+    engine = int(lib.load().qch_set_herm_gemm(-1))
     fl_ref = 17 * 8 * n**3
+    # the dominant kernel of the default engine: oz_gemm (int8 tensor cores)
+    oz_ms = max_over_ranks(torch, prof.get("oz_gemm", (0.0, 0))[0], world)
+    ops = sum_over_ranks(torch, float(lib.load().qch_int8_ops()) - op0, world)
+    dm_ms = max_over_ranks(torch, sum(v[0] for k, v in prof.items() if k.startswith("zgemm")), world)
+    dm_fl = sum_over_ranks(torch, float(lib.load().qch_dmma_flops()) - fl0, world)
+    mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    i8_peak = 2.0 * mp.get("bf16_tflops", 1590.0)  # dense int8 = 2 x dense bf16 on sm_100
+    kernels_ms = {k: v[0] for k, v in prof.items()}
+    if engine == 1 and oz_ms:
+        ach = ops / world / (oz_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": "oz_gemm_kernel (tcgen05.mma kind::i8, TMEM, TMA; Ozaki slices)",
+                "achieved": ach, "peak": i8_peak, "unit": "TOPS (int8)", "frac": ach / i8_peak,
+                "peak_kind": "dense int8 = 2 x the measured cuBLAS bf16 burst of MEASURED_PEAKS.json (nominal 4500)",
+                "ops_basis": "int8 tensor ops issued by the library (qch_int8_ops): 3 real products per complex "
+                             "product x 36 slice pairs x 2 M N K per computed tile",
+                "gemm_ms": oz_ms,
+                "fp64_equivalent_tflops": ops / (0.75 * _oz_pairs()) / world / (oz_ms * 1e-3) / 1e12,
+                "fp64_equivalent_note": "complex-product flops the int8 GEMMs stand in for (8 M N K per computed "
+                                        "tile = int8 ops / (3 real products x slice pairs x 2 / 8)) / int8 GEMM "
+                                        f"time -- vs the live DMMA peak {fp64.get('dmma', 0):.1f} TFLOP/s",
+                "kernel_ms": kernels_ms,
+                "traffic": traffic_from_profiles("oz_gemm_kernel@oz")}
+    else:
+        ach = dm_fl / world / (dm_ms * 1e-3) / 1e12 if dm_ms else None
+        roof = {"bound": "tensor", "kernel": "zgemm_tma_kernel (DMMA, TMA-fed)", "achieved": ach,
+                "peak": fp64.get("dmma"), "unit": "TFLOP/s",
+                "frac": (ach / fp64["dmma"]) if ach and fp64.get("dmma") else None,
+                "gemm_ms": dm_ms, "kernel_ms": kernels_ms}
+    roof["reference_equivalent_tflops"] = fl_ref * n_int / (dev_ms * 1e-3) / 1e12
+    roof["flops_per_interval_reference"] = fl_ref
+    dmma = None
+    if world == 1 and rank == 0:
+        dmma = _dmma_sample(torch, eff, lib, ch, grid, psi0)
+        if dmma.get("achieved_tflops") and fp64.get("dmma"):
+            dmma["frac_of_dmma_peak"] = dmma["achieved_tflops"] / fp64["dmma"]
     cpu = None
     if rank == 0:  # the reference's _expm_minus_i (18-term Taylor, expm.py:56-71) on ONE interval, host cores
-        from paper_2411_09982_b200 import models
-
         try:
             from threadpoolctl import threadpool_info
 
@@ -637,24 +696,13 @@ def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
                         + ("one GPU" if world == 1 else f"relay over {world} GPUs"),
             "metric": "Magnus intervals/s", "unit": "intervals/s", "value": n_int / (dev_ms * 1e-3),
             "intervals": n_int, "n_gpus": world, "scaling": "strong", "ms_per_evolve": dev_ms,
+            "engine": "int8 tensor cores (Ozaki, tcgen05)" if engine == 1 else "DMMA",
             "e2e": {"value": n_int / (e2e_ms * 1e-3), "unit": "intervals/s", "ms": e2e_ms,
                     "h2d_bytes_per_step": int(grid.signals.nbytes + psi0.nbytes), "d2h_bytes_per_step": int(d2h),
                     "path": "evolve(host psi0, host grid) -> host trajectory" if world == 1
                             else "sharding.evolve_relay + gather -> host trajectory on rank 0"},
-            "gemm_launches": gemm_per_interval,
-            "roofline": {"bound": "tensor", "kernel": "zgemm_tma_kernel (DMMA, TMA-fed)", "achieved": ach,
-                         "peak": fp64.get("dmma"), "unit": "TFLOP/s",
-                         "frac": (ach / fp64["dmma"]) if ach and fp64.get("dmma") else None,
-                         "peak_kind": "FP64 DMMA (mma.sync f64) measured live; cuBLAS zgemm "
-                                      f"{fp64.get('cublas_zgemm', 0):.1f} TFLOP/s on the same box",
-                         "flops_basis": f"executed DMMA flops as counted by the library (qch_dmma_flops): "
-                                        f"{2 * rp} N^3 per full complex GEMM ({rp} real products per complex "
-                                        f"product), ~{frac_h:.3f} of it for the Hermitian half-GEMMs",
-                         "gemm_ms": g_ms,
-                         "reference_equivalent_tflops": fl_ref * n_int / (dev_ms * 1e-3) / 1e12,
-                         "flops_per_interval_executed": fl_exec / n_int,
-                         "flops_per_interval_reference": fl_ref,
-                         "traffic": traffic_from_profiles("zgemm_tma_kernel@c5")},
+            "roofline": roof,
+            "dmma_engine_sample": dmma,
             "cpu_baseline": cpu}
 
 

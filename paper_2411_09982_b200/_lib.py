@@ -121,6 +121,11 @@ PROTOTYPES = {
     "qch_zgemm_herm_batched": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p]),
     "qch_zgemm_real_products": (c_int, []),
     "qch_dmma_flops": (c_double, []),
+    "qch_set_herm_gemm": (c_int, [c_int]),
+    "qch_int8_ops": (c_double, []),
+    "qch_i8gemm_test": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
+    "qch_oz_real_test": (
+        c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),
 }
 
 QCH_OK = 0

@@ -319,7 +319,13 @@ int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream
   return zt_gemm(ZT_DEFECT, true, true, u, u, n, n, n, batch, nn, nn, g, st);
 }
 
+// Hermitian products of the exp(-iH) evaluation: Ozaki-sliced int8 tcgen05
+// GEMMs (ozgemm.cu) for 512 <= n <= 16384 by default, the DMMA kernel
+// otherwise or with QCH_HERM_GEMM=dmma
+static bool use_ozaki(int n) { return herm_engine() != 0 && n >= 512 && n % 16 == 0 && n <= 16384; }
+
 int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st) {
+  if (use_ozaki(n)) return zgemm_herm_ozaki(ZT_STORE, a, b, c, nullptr, nullptr, 0, n, batch, st);
   ZtArgs g{};
   g.c = c;
   const int64_t nn = (int64_t)n * n;
@@ -329,6 +335,7 @@ int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t ba
 int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const double2* const* p, const double* q,
                int nq, int n, int64_t batch, cudaStream_t st) {
   if (nq > 4) return fail(QCH_ERR_UNSUPPORTED, "zgemm_qacc: at most 4 power terms");
+  if (herm && use_ozaki(n)) return zgemm_herm_ozaki(ZT_QACC, a, b, c, p, q, nq, n, batch, st);
   ZtArgs g{};
   g.c = c;
   g.nq = nq;
@@ -343,6 +350,10 @@ int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const 
 
 int zgemm_ufin(const double2* a, const double2* b, const double2* cpart, double2* u, int n, int64_t batch,
                cudaStream_t st) {
+  if (use_ozaki(n)) {
+    const double2* pw[1] = {cpart};
+    return zgemm_herm_ozaki(ZT_UFIN, a, b, u, pw, nullptr, 0, n, batch, st);
+  }
   ZtArgs g{};
   g.c = u;
   g.p[0] = cpart;

@@ -34,6 +34,15 @@ bool zgemm_use_3m();
 // executed DMMA flops of the TMA kernel since load (accounting)
 double dmma_flops_total();
 
+// Hermitian products on the int8 tensor cores (ozgemm.cu: Ozaki slices,
+// tcgen05 kind::i8): C = [epilogue] (A B) for Hermitian A, B with A B
+// Hermitian; mode ZT_STORE / ZT_QACC (pw, q, nq) / ZT_UFIN (pw[0] = C part)
+int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, const double2* const* pw,
+                     const double* q, int nq, int n, int64_t batch, cudaStream_t st);
+double oz_int8_ops_total();
+int oz_slices();
+int herm_engine();  // 1: int8 tensor cores (Ozaki), 0: DMMA
+
 // square / rectangular conveniences (zgemm.cu)
 int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, int64_t batch, int64_t sa, int64_t sb,
           int64_t sc, cudaStream_t st);

@@ -1,0 +1,76 @@
+"""The int8 tensor-core path (tcgen05 kind::i8, TMEM accumulators, TMA):
+the int8 GEMM is exact (int32) against an integer reference; one Ozaki-sliced
+real product is at FP64 level with 8 slices (and degrades by 2^-7 per slice
+removed, as the scheme predicts); the Hermitian expm on both engines agrees
+with the oracle."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import rel_fro
+from oracle import expm_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2411_09982_b200 import _lib
+
+    return _lib
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 128, 128), (200, 136, 160), (256, 384, 512), (1024, 512, 4096)])
+def test_i8gemm_exact(L, m, n, k):
+    import torch
+
+    g = torch.Generator().manual_seed(m + n + k)
+    a = torch.randint(-127, 128, (m, k), generator=g, dtype=torch.int8)
+    b = torch.randint(-127, 128, (n, k), generator=g, dtype=torch.int8)
+    da, db = a.cuda(), b.cuda()
+    dc = torch.zeros(m, n, dtype=torch.int32, device="cuda")
+    L.call("qch_i8gemm_test", L.dptr(da), L.dptr(db), L.dptr(dc), m, n, k, L.stream_ptr())
+    ref = (a.long().double() @ b.long().double().T).round().long()
+    assert torch.equal(dc.cpu().long(), ref)
+
+
+@pytest.mark.parametrize("comp", [(0, 0), (1, 4), (2, 3)])
+def test_ozaki_real_product_accuracy(L, comp):
+    import torch
+
+    rng = np.random.default_rng(7)
+    m, n, k = 384, 256, 1024
+    x = rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k))
+    y = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+    x[5] *= 1e-7  # rows of very different scale keep their own exponent
+    f = {0: lambda z: z.real, 1: lambda z: z.imag, 2: lambda z: z.real + z.imag, 3: lambda z: z.real - z.imag,
+         4: lambda z: -z.imag}
+    ref = f[comp[0]](x) @ f[comp[1]](y).T
+    dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    errs = {}
+    for s in (6, 8):
+        out = torch.zeros(m, n, dtype=torch.float64, device="cuda")
+        L.call("qch_oz_real_test", L.dptr(dx), comp[0], L.dptr(dy), comp[1], L.dptr(out), m, n, k, s, L.stream_ptr())
+        got = out.cpu().numpy()
+        scale = np.abs(f[comp[0]](x)).max(axis=1)[:, None] * np.abs(f[comp[1]](y)).max(axis=1)[None, :] * k
+        errs[s] = float((np.abs(got - ref) / scale).max())
+    assert errs[8] <= 1e-16          # FP64 level relative to the row/column scale
+    assert errs[6] > 100 * errs[8]   # two slices less: ~2^-14 worse
+
+
+@pytest.mark.parametrize("n", [512, 640])
+def test_expm_both_engines_vs_oracle(L, n):
+    import paper_2411_09982_b200 as E
+
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = (a + a.conj().T) * (0.3 / np.sqrt(n))
+    ref = expm_oracle.expm_minus_i(h)
+    old = L.load().qch_set_herm_gemm(-1)
+    try:
+        for engine in (1, 0):
+            L.load().qch_set_herm_gemm(engine)
+            assert rel_fro(E.expm_unitary(h).entries, ref) <= 1e-12, engine
+    finally:
+        L.load().qch_set_herm_gemm(old)

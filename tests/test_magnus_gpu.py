@@ -310,3 +310,31 @@ def test_return_propagators_large_dim_vs_oracle(E, order):
     assert rel_fro(np.stack([p.entries for p in props]), ref_u) <= 1e-12
     assert rel_fro(traj.amplitudes, ref_traj) <= 1e-10
     assert np.array_equal(traj.times, np.linspace(grid.t_start, grid.t_end, 13))
+
+
+@pytest.mark.parametrize("n,scale,b", [(512, 0.2, 2), (1024, 0.05, 1), (768, 3.0, 1)])
+def test_expm_hermitian_int8_tensor_path_vs_oracle(E, n, scale, b):
+    # n >= 512: the Hermitian products run on the int8 tensor cores (Ozaki
+    # slices, tcgen05; ozgemm.cu) — same 1e-12 bar as the DMMA path against
+    # the reference's 18-term Taylor (scale 3: squarings on the DMMA path)
+    rng = np.random.default_rng(n)
+    hs = [_herm(rng, n, scale / np.sqrt(n)) for _ in range(b)]
+    for h, p in zip(hs, E.expm_batch(hs)):
+        assert rel_fro(p.entries, expm_oracle.expm_minus_i(h)) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [512, 1000, 1024])
+def test_zgemm_herm_int8_tensor_path_vs_numpy(E, n):
+    import torch
+    from paper_2411_09982_b200 import _lib
+
+    rng = np.random.default_rng(n + 1)
+    h = _herm(rng, n)
+    h2 = h @ h
+    out = torch.empty((1, n, n), dtype=torch.complex128, device="cuda")
+    dh2, dh = _lib.to_device(h2), _lib.to_device(h)  # (kept alive across the call)
+    _lib.call("qch_zgemm_herm_batched", _lib.dptr(dh2), _lib.dptr(dh), _lib.dptr(out), n, 1, _lib.stream_ptr())
+    got = out[0].cpu().numpy()
+    assert rel_fro(got, h2 @ h) <= 1e-14
+    iu = np.triu_indices(n, 1)
+    np.testing.assert_array_equal(got[iu], got.T[iu].conj())

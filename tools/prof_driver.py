@@ -98,6 +98,17 @@ def main():
             else:
                 lib.call("qch_zgemm_herm_batched", lib.dptr(h), lib.dptr(h), lib.dptr(c), n, 1, lib.stream_ptr())
         print(case, "done")
+    elif case == "oz4096":
+        from paper_2411_09982_b200 import _lib as lib
+
+        n = 4096
+        a = torch.randn(n, n, dtype=torch.complex128, device="cuda")
+        h = (a + a.mH) * 0.5
+        c = torch.empty((8, n, n), dtype=torch.complex128, device="cuda")
+        hb = h.expand(8, n, n).contiguous()
+        for _ in range(2):
+            lib.call("qch_zgemm_herm_batched", lib.dptr(hb), lib.dptr(hb), lib.dptr(c), n, 8, lib.stream_ptr())
+        print(case, "done")
     torch.cuda.synchronize()
 
 
