@@ -593,6 +593,15 @@ static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2
   herm_scale_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, nn, batch, sarr, hs);
   QCH_LAUNCH_CHECK("herm_scale_kernel");
   note_launch(1);
+  // int8 engine: each operand's Ozaki slices are cut once and reused by every
+  // product it enters (Hs: B and the final U; B: B^2 and B^3; B^q: every
+  // Paterson-Stockmeyer step); entries are dropped when their matrix is
+  // overwritten or no longer read
+  OzCache oc_store(n, batch, st);
+  OzCache* oc = herm_use_ozaki(n) ? &oc_store : nullptr;
+  auto drop = [&](const void* p) {
+    if (oc) oc->drop(p);
+  };
   const int dc = m / 2, dt = (m - 1) / 2;
   int q = 0;
   if (std::max(dc, dt) >= 1) {
@@ -601,9 +610,10 @@ static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2
       const int cst = herm_gemm_count(qq, dc, dt);
       if (cst < best) best = cst, q = qq;
     }
-    if (int rc = zgemm_herm(hs, hs, P[1], n, batch, st)) return rc;
+    if (int rc = zgemm_herm(hs, hs, P[1], n, batch, st, oc)) return rc;
     for (int j = 2; j <= q; ++j)
-      if (int rc = zgemm_herm(P[j - 1], P[1], P[j], n, batch, st)) return rc;
+      if (int rc = zgemm_herm(P[j - 1], P[1], P[j], n, batch, st, oc)) return rc;
+    for (int j = 1; j < q; ++j) drop(P[j]);  // only B^q is a GEMM operand from here on
   }
   double fac[20];
   fac[0] = 1.0;
@@ -619,6 +629,7 @@ static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2
     comb_kernel<<<grid_for(nn * batch), 256, 0, st>>>(a, nn, n, batch, out);
     QCH_LAUNCH_CHECK("comb_kernel");
     note_launch(1);
+    drop(out);
     return QCH_OK;
   };
   // p(B) = sum_{i<=d} coef_i B^i by Paterson-Stockmeyer into one of bufs[0..1]
@@ -646,7 +657,8 @@ static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2
       const double2* pp[4] = {P[1], P[2], P[3], P[4]};
       double qc[5] = {0, 0, 0, 0, 0};
       for (int i = 0; i < q; ++i) qc[i] = coef[j * q + i];
-      if (int rc = zgemm_qacc(true, P[q], bufs[cur], bufs[cur ^ 1], pp, qc, q - 1, n, batch, st)) return rc;
+      if (int rc = zgemm_qacc(true, P[q], bufs[cur], bufs[cur ^ 1], pp, qc, q - 1, n, batch, st, oc)) return rc;
+      drop(bufs[cur]);
       cur ^= 1;
     }
     *res = bufs[cur];
@@ -659,7 +671,9 @@ static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2
   double2* T = nullptr;
   if (int rc = poly(cc, dc, W[5], W[6], &C)) return rc;
   if (int rc = poly(tc, dt, W[7], C == W[5] ? W[6] : W[5], &T)) return rc;
-  if (int rc = zgemm_ufin(hs, T, C, u, n, batch, st)) return rc;
+  if (q) drop(P[q]);
+  if (int rc = zgemm_ufin(hs, T, C, u, n, batch, st, oc)) return rc;
+  if (oc) oc->clear();
   for (int step = 0; step < smax; ++step) {  // squarings (U is not Hermitian)
     if (int rc = zgemm(u, u, W[1], n, n, n, batch, nn, nn, nn, st)) return rc;
     select_square_kernel<<<grid_for(nn * batch), 256, 0, st>>>(u, W[1], nn, batch, sarr, step);

@@ -322,10 +322,11 @@ int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream
 // Hermitian products of the exp(-iH) evaluation: Ozaki-sliced int8 tcgen05
 // GEMMs (ozgemm.cu) for 512 <= n <= 16384 by default, the DMMA kernel
 // otherwise or with QCH_HERM_GEMM=dmma
-static bool use_ozaki(int n) { return herm_engine() != 0 && n >= 512 && n % 16 == 0 && n <= 16384; }
+bool herm_use_ozaki(int n) { return herm_engine() != 0 && n >= 512 && n % 16 == 0 && n <= 16384; }
+static bool use_ozaki(int n) { return herm_use_ozaki(n); }
 
-int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st) {
-  if (use_ozaki(n)) return zgemm_herm_ozaki(ZT_STORE, a, b, c, nullptr, nullptr, 0, n, batch, st);
+int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st, OzCache* oc) {
+  if (use_ozaki(n)) return zgemm_herm_ozaki(ZT_STORE, a, b, c, nullptr, nullptr, 0, n, batch, st, oc);
   ZtArgs g{};
   g.c = c;
   const int64_t nn = (int64_t)n * n;
@@ -333,9 +334,9 @@ int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t ba
 }
 
 int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const double2* const* p, const double* q,
-               int nq, int n, int64_t batch, cudaStream_t st) {
+               int nq, int n, int64_t batch, cudaStream_t st, OzCache* oc) {
   if (nq > 4) return fail(QCH_ERR_UNSUPPORTED, "zgemm_qacc: at most 4 power terms");
-  if (herm && use_ozaki(n)) return zgemm_herm_ozaki(ZT_QACC, a, b, c, p, q, nq, n, batch, st);
+  if (herm && use_ozaki(n)) return zgemm_herm_ozaki(ZT_QACC, a, b, c, p, q, nq, n, batch, st, oc);
   ZtArgs g{};
   g.c = c;
   g.nq = nq;
@@ -349,10 +350,10 @@ int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const 
 }
 
 int zgemm_ufin(const double2* a, const double2* b, const double2* cpart, double2* u, int n, int64_t batch,
-               cudaStream_t st) {
+               cudaStream_t st, OzCache* oc) {
   if (use_ozaki(n)) {
     const double2* pw[1] = {cpart};
-    return zgemm_herm_ozaki(ZT_UFIN, a, b, u, pw, nullptr, 0, n, batch, st);
+    return zgemm_herm_ozaki(ZT_UFIN, a, b, u, pw, nullptr, 0, n, batch, st, oc);
   }
   ZtArgs g{};
   g.c = u;

@@ -1,6 +1,8 @@
 // zgemm.h — complex128 GEMMs on the FP64 tensor pipe (DMMA), shared between
 // the translation units of libqcheff (not part of the public C-ABI).
 #pragma once
+#include <vector>
+
 #include "qch_internal.h"
 
 namespace qch {
@@ -37,8 +39,31 @@ double dmma_flops_total();
 // Hermitian products on the int8 tensor cores (ozgemm.cu: Ozaki slices,
 // tcgen05 kind::i8): C = [epilogue] (A B) for Hermitian A, B with A B
 // Hermitian; mode ZT_STORE / ZT_QACC (pw, q, nq) / ZT_UFIN (pw[0] = C part)
+// Slices are cached per source matrix for the duration of one OzCache (an
+// exp(-iH) evaluation reuses Hs, B and B^q on several products); the owner
+// drops an entry when it overwrites the matrix.  Component q of an entry:
+// 0 Re, 1 Im, 2 Re + Im, 3 Re - Im (slice sets [batch][s][n][n] int8).
+struct OzCache {
+  struct Entry {
+    const void* src = nullptr;
+    int8_t* sl[4] = {nullptr, nullptr, nullptr, nullptr};
+    int* ex[4] = {nullptr, nullptr, nullptr, nullptr};
+  };
+  int n;
+  int64_t batch;
+  cudaStream_t st;
+  std::vector<Entry> ent;
+  OzCache(int n_, int64_t batch_, cudaStream_t st_) : n(n_), batch(batch_), st(st_) {}
+  ~OzCache();
+  OzCache(const OzCache&) = delete;
+  OzCache& operator=(const OzCache&) = delete;
+  int get(const double2* src, unsigned mask, const Entry** out);
+  void drop(const void* src);
+  void clear();
+};
 int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, const double2* const* pw,
-                     const double* q, int nq, int n, int64_t batch, cudaStream_t st);
+                     const double* q, int nq, int n, int64_t batch, cudaStream_t st, OzCache* cache = nullptr);
+bool herm_use_ozaki(int n);
 double oz_int8_ops_total();
 int oz_slices();
 int herm_engine();  // 1: int8 tensor cores (Ozaki), 0: DMMA
@@ -49,12 +74,13 @@ int zgemm(const double2* a, const double2* b, double2* c, int m, int n, int k, i
 int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st);
 int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st);
 // Hermitian products of commuting Hermitian n x n factors (batched)
-int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st);
+int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st,
+               OzCache* oc = nullptr);
 // C = q0 I + sum_i q_i P_i + A B  (nq <= 4), Hermitian when herm
 int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const double2* const* p, const double* q,
-               int nq, int n, int64_t batch, cudaStream_t st);
+               int nq, int n, int64_t batch, cudaStream_t st, OzCache* oc = nullptr);
 // U = C - i (A B), A B Hermitian
 int zgemm_ufin(const double2* a, const double2* b, const double2* cpart, double2* u, int n, int64_t batch,
-               cudaStream_t st);
+               cudaStream_t st, OzCache* oc = nullptr);
 
 }  // namespace qch

@@ -74,3 +74,32 @@ def test_expm_both_engines_vs_oracle(L, n):
             assert rel_fro(E.expm_unitary(h).entries, ref) <= 1e-12, engine
     finally:
         L.load().qch_set_herm_gemm(old)
+
+
+@pytest.mark.parametrize("n,batch", [(512, 1), (528, 3)])
+def test_herm_products_int8_vs_fp64(L, n, batch):
+    """qch_zgemm_herm_batched on the int8 engine: A A (one slicing for both
+    sides) and A p(A) (distinct operands) for a batch, against numpy, with the
+    lower-triangle result mirrored exactly (off-diagonal C Hermitian bit for bit)."""
+    import torch
+
+    rng = np.random.default_rng(n + batch)
+    a = rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))
+    a = (a + np.conj(np.swapaxes(a, 1, 2))) / np.sqrt(n)
+    p = a @ a * 0.5 - 0.25 * a  # a polynomial of a: commutes with a, A p Hermitian
+    p = (p + np.conj(np.swapaxes(p, 1, 2))) / 2
+    ddev = lambda z: torch.from_numpy(np.ascontiguousarray(z)).cuda()
+    old = L.load().qch_set_herm_gemm(1)
+    try:
+        for x, y in ((a, a), (a, p)):
+            dx = ddev(x)
+            dy = dx if y is x else ddev(y)
+            dc = torch.zeros_like(dx)
+            L.call("qch_zgemm_herm_batched", L.dptr(dx), L.dptr(dy), L.dptr(dc), n, batch, L.stream_ptr())
+            got = dc.cpu().numpy()
+            ref = x @ y
+            assert np.abs(got - ref).max() <= 1e-13 * np.abs(ref).max()
+            off = ~np.eye(n, dtype=bool)
+            np.testing.assert_array_equal(got[:, off], np.conj(np.swapaxes(got, 1, 2))[:, off])
+    finally:
+        L.load().qch_set_herm_gemm(old)

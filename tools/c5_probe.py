@@ -1,7 +1,7 @@
 """Config 5 probe: Magnus on the 12-spin Heisenberg chain (dim 4096), order 2,
 the first n intervals through evolve_device, with the per-kernel profile.
 
-    python tools/c5_probe.py [n_intervals] [check]
+    python tools/c5_probe.py [n_intervals] [check|nocheck] [repeats]
 """
 from __future__ import annotations
 
@@ -30,22 +30,24 @@ def main():
     psi0[0] = 1
     d_psi = _lib.to_device(psi0)
     ch.device_operators()
-    mg.evolve_device(ch, grid, min(n_int, 2), d_psi, check=check, order=2)
+    mg.evolve_device(ch, grid, min(n_int, 8), d_psi, check=check, order=2)  # one full chunk: pool mapped
     torch.cuda.synchronize()
-    _lib.profile_read(reset=True)
-    _lib.profile_enable(True)
-    t0 = time.perf_counter()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    mg.evolve_device(ch, grid, n_int, d_psi, check=check, order=2)
-    e.record()
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
-    _lib.profile_enable(False)
-    prof = _lib.profile_read(reset=True)
-    ms = s.elapsed_time(e)
-    print(f"config 5: {n_int} intervals order 2 check={check}: {ms:.1f} ms (wall {wall * 1e3:.1f}) -> "
-          f"{n_int / (ms * 1e-3):.2f} intervals/s", flush=True)
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    for rep in range(reps):
+        _lib.profile_read(reset=True)
+        _lib.profile_enable(True)
+        t0 = time.perf_counter()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        mg.evolve_device(ch, grid, n_int, d_psi, check=check, order=2)
+        e.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        _lib.profile_enable(False)
+        prof = _lib.profile_read(reset=True)
+        ms = s.elapsed_time(e)
+        print(f"config 5: {n_int} intervals order 2 check={check}: {ms:.1f} ms (wall {wall * 1e3:.1f}) -> "
+              f"{n_int / (ms * 1e-3):.2f} intervals/s", flush=True)
     n = 4096
     for k, (tot, cnt) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
         extra = ""
