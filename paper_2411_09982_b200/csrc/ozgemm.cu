@@ -443,8 +443,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const int c0 = n0 + half * (BN / 2) + cb;
         if (rok && c0 < g.n) {
           double* o = orow + c0;
-          const bool cfull = c0 + 32 <= g.n;
-#pragma unroll
+          const bool cfull = c0 + 32 <= g.n;  // ldo is even: paired accesses stay 16-byte aligned; a pair
+#pragma unroll                             // straddling column n writes the row's padding column
           for (int e = 0; e < 32; e += 2) {
             if (!cfull && c0 + e >= g.n) break;
             double2 acc = D ? *(const double2*)(o + e) : make_double2(0.0, 0.0);
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             acc.y = fma((double)(int)v[e + 1], scl, acc.y);
             if (last) {
               acc.x = ldexp(acc.x, er + ebb[c0 + e]);
-              acc.y = ldexp(acc.y, er + ebb[c0 + e + 1]);
+              acc.y = ldexp(acc.y, er + ebb[c0 + e + 1 < g.n ? c0 + e + 1 : c0 + e]);
             }
             *(double2*)(o + e) = acc;
           }
@@ -498,6 +498,9 @@ __device__ __forceinline__ double oz_comp(double2 v, int comp) {
     default: return -v.y;
   }
 }
+
+// slice row stride in bytes: columns rounded up to 16 (the TMA stride unit)
+__host__ __device__ __forceinline__ int oz_ld(int cols) { return (cols + 15) & ~15; }
 
 struct OzSliceOut {
   int8_t* sl[4];  // [batch][s][rows][cols]
@@ -552,8 +555,9 @@ __device__ __forceinline__ unsigned long long oz_fixed(double y, int e) {
 template <int S>
 __global__ void __launch_bounds__(256) oz_cut_kernel(const double2* __restrict__ x, int rows, int cols,
                                                      int64_t xstride, OzSliceOut o, int64_t groups) {
-  const int gpr = cols >> 3;
-  const int64_t plane = (int64_t)rows * cols;
+  const int ld = oz_ld(cols);  // slice row stride: padding columns are written as zeros
+  const int gpr = ld >> 3;
+  const int64_t plane = (int64_t)rows * ld;
   for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups;
        gi += (int64_t)gridDim.x * blockDim.x) {
     const int64_t br = gi / gpr;  // b * rows + r
@@ -562,9 +566,14 @@ __global__ void __launch_bounds__(256) oz_cut_kernel(const double2* __restrict__
     const int r = (int)(br - b * rows);
     const double2* xr = x + b * xstride + (int64_t)r * cols + c8;
     double2 v[8];
+    if (c8 + 8 <= cols) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = xr[j];
-    const int64_t off = b * (int64_t)S * plane + (int64_t)r * cols + c8;
+      for (int j = 0; j < 8; ++j) v[j] = xr[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = c8 + j < cols ? xr[j] : make_double2(0.0, 0.0);
+    }
+    const int64_t off = b * (int64_t)S * plane + (int64_t)r * ld + c8;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (q >= o.nc) break;
@@ -601,18 +610,18 @@ __global__ void __launch_bounds__(256) oz_cut_kernel(const double2* __restrict__
 
 static int oz_slicev(const double2* x, int rows, int cols, int64_t batch, int64_t xstride, int s, const OzSliceOut& o,
                      cudaStream_t st) {
-  if (cols % 8) return fail(QCH_ERR_UNSUPPORTED, "ozaki slices: columns must be a multiple of 8");
+  const int ld = oz_ld(cols);
   for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
     const int64_t nb = std::min<int64_t>(batch - b0, 65535);
     OzSliceOut ob = o;
     for (int q = 0; q < o.nc; ++q) {
-      ob.sl[q] = o.sl[q] + b0 * (int64_t)s * rows * cols;
+      ob.sl[q] = o.sl[q] + b0 * (int64_t)s * rows * ld;
       ob.ex[q] = o.ex[q] + b0 * rows;
     }
     void* pr = prof_begin("oz_slice", st);
     const double2* xb = x + b0 * xstride;
     oz_rowexp_kernel<<<dim3(rows, (unsigned)nb), 256, 0, st>>>(xb, rows, cols, xstride, ob);
-    const int64_t groups = nb * rows * (int64_t)(cols / 8);
+    const int64_t groups = nb * rows * (int64_t)(ld / 8);
     const int blocks = (int)std::min<int64_t>((groups + 255) / 256, (int64_t)sm_count() * 64);
     switch (s) {
 #define OZ_SL(k) \
@@ -640,13 +649,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 oz_encode() {
   return fn;
 }
 
-// slices [planes][rows][cols] int8 as a 3-d map, box 128 B x 128 rows
+// slices [planes][rows][ld] int8 as a 3-d map (columns beyond cols read as
+// zeros), box 128 B x box_rows
 static int oz_map(CUtensorMap* map, const int8_t* ptr, int64_t rows, int64_t cols, int64_t planes,
                   unsigned box_rows = 128) {
   auto fn = oz_encode();
   if (!fn) return fail(QCH_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int64_t ld = oz_ld((int)cols);
   cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)planes};
-  cuuint64_t strides[2] = {(cuuint64_t)cols, (cuuint64_t)(rows * cols)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld, (cuuint64_t)(rows * ld)};
   cuuint32_t box[3] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows, 1u};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)ptr, dims, strides, box, es,
@@ -716,9 +727,10 @@ int oz_gemm(const int8_t* xs, const int* ea, const int8_t* ys, const int* eb, in
             int64_t batch, double* out, int ldo, int64_t so, const int* tiles, int ntiles, cudaStream_t st,
             double* ops) {
   if (s < 1 || s > OZ_MAX_S) return fail(QCH_ERR_VALUE, "ozaki: 1..8 slices");
+  if (ldo % 2 || ldo < n || so % 2) return fail(QCH_ERR_VALUE, "ozaki: the output row stride must be even and >= n");
   // exact int32 accumulation: (slices per diagonal) K 127^2 < 2^31
-  if (k % 16 || (int64_t)s * k * 127 * 127 >= (int64_t)1 << 31)
-    return fail(QCH_ERR_UNSUPPORTED, "ozaki: K must be a multiple of 16 and s K 127^2 < 2^31");
+  if ((int64_t)s * k * 127 * 127 >= (int64_t)1 << 31)
+    return fail(QCH_ERR_UNSUPPORTED, "ozaki: s K 127^2 must stay below 2^31");
   if (batch > 65535) return fail(QCH_ERR_UNSUPPORTED, "ozaki: batch > 65535");
   const int cfg = oz_cfg();
   const int rows_per_tile = oz_tile_rows(), bn = oz_tile_cols();
@@ -783,7 +795,8 @@ struct OzCombine {
   int nq;
   int mode;  // 0 STORE, 2 QACC, 3 UFIN (zgemm.h numbering)
   int n;
-  int tn;  // 32-tiles per side
+  int ldp;  // row stride of P1..P3 (n rounded up to even)
+  int tn;   // 32-tiles per side
 };
 
 __global__ void __launch_bounds__(256) oz_combine_kernel(OzCombine a) {
@@ -802,7 +815,8 @@ __global__ void __launch_bounds__(256) oz_combine_kernel(OzCombine a) {
     const int rl = ty + 8 * k, r = I * 32 + rl;
     if (r >= a.n || c >= a.n || r < c) continue;
     const int64_t e = boff + (int64_t)r * a.n + c;
-    const double v1 = a.p1[e], v2 = a.p2[e], v3 = a.p3[e];
+    const int64_t ep = (int64_t)blockIdx.y * a.n * a.ldp + (int64_t)r * a.ldp + c;
+    const double v1 = a.p1[ep], v2 = a.p2[ep], v3 = a.p3[ep];
     const double re = v1 + v2, im = (v3 - v1) + v2;
     double2 d, m;
     if (a.mode == 3) {  // U = C - i S
@@ -926,7 +940,7 @@ int OzCache::get(const double2* src, unsigned mask, const OzCache::Entry** out) 
   OzSliceOut o{};
   for (int q = 0; q < 4; ++q)
     if ((mask >> q & 1) && !e->sl[q]) {
-      QCH_CUDA(cudaMallocAsync((void**)&e->sl[q], (size_t)S * nn * batch, st));
+      QCH_CUDA(cudaMallocAsync((void**)&e->sl[q], (size_t)S * n * oz_ld(n) * batch, st));
       QCH_CUDA(cudaMallocAsync((void**)&e->ex[q], sizeof(int) * (size_t)n * batch, st));
       o.sl[o.nc] = e->sl[q];
       o.ex[o.nc] = e->ex[q];
@@ -954,7 +968,9 @@ int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, c
   if (int rc = oc->get(b, 0xB, &Y)) return rc;  // B: Re, Im, Re - Im
   if (int rc = oc->get(a, ma, &X)) return rc;   // re-lookup (the entry vector may have grown)
   double* P = nullptr;
-  QCH_CUDA(cudaMallocAsync((void**)&P, 3 * sizeof(double) * (size_t)nn * batch, st));
+  const int ldp = (n + 1) & ~1;  // even: the GEMM epilogue's paired stores stay 16-byte aligned
+  const int64_t np_ = (int64_t)n * ldp;
+  QCH_CUDA(cudaMallocAsync((void**)&P, 3 * sizeof(double) * (size_t)np_ * batch, st));
   const int yc[3] = {0, 1, 3};
   int rc = QCH_OK;
   const int* tiles = nullptr;
@@ -963,7 +979,7 @@ int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, c
   double ops = 0.0;
   for (int v = 0; v < 3 && rc == QCH_OK; ++v) {
     double o = 0.0;
-    rc = oz_gemm(X->sl[v], X->ex[v], Y->sl[yc[v]], Y->ex[yc[v]], n, n, n, S, batch, P + v * nn * batch, n, nn, tiles,
+    rc = oz_gemm(X->sl[v], X->ex[v], Y->sl[yc[v]], Y->ex[yc[v]], n, n, n, S, batch, P + v * np_ * batch, ldp, np_, tiles,
                  ntiles, st, &o);
     ops += o;
   }
@@ -973,12 +989,13 @@ int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, c
     }
     OzCombine cm{};
     cm.p1 = P;
-    cm.p2 = P + nn * batch;
-    cm.p3 = P + 2 * nn * batch;
+    cm.p2 = P + np_ * batch;
+    cm.p3 = P + 2 * np_ * batch;
     cm.c = c;
     cm.nq = nq;
     cm.mode = mode;
     cm.n = n;
+    cm.ldp = ldp;
     cm.tn = (n + 31) / 32;
     for (int i = 0; i < 4; ++i) cm.pw[i] = (pw && i < (mode == 3 ? 1 : nq)) ? pw[i] : nullptr;
     for (int i = 0; i < 5; ++i) cm.q[i] = (q && i <= nq) ? q[i] : 0.0;
@@ -986,9 +1003,9 @@ int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, c
     for (int64_t b0 = 0; b0 < batch && rc == QCH_OK; b0 += 65535) {
       const int64_t nb = std::min<int64_t>(batch - b0, 65535);
       OzCombine cb = cm;
-      cb.p1 += b0 * nn;
-      cb.p2 += b0 * nn;
-      cb.p3 += b0 * nn;
+      cb.p1 += b0 * np_;
+      cb.p2 += b0 * np_;
+      cb.p3 += b0 * np_;
       cb.c += b0 * nn;
       for (int i = 0; i < 4; ++i)
         if (cb.pw[i]) cb.pw[i] += b0 * nn;
@@ -1021,11 +1038,12 @@ extern "C" double qch_int8_ops(void) { return oz_int8_ops_total(); }
 extern "C" int qch_oz_real_test(const void* d_x, int xcomp, const void* d_y, int ycomp, void* d_out, int64_t m,
                                 int64_t n, int64_t k, int s, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (n % 2) return fail(QCH_ERR_VALUE, "qch_oz_real_test: n must be even (paired FP64 stores)");
   int8_t *xs = nullptr, *ys = nullptr;
   int *ea = nullptr, *eb = nullptr;
   ensure_pool();
-  QCH_CUDA(cudaMallocAsync((void**)&xs, (size_t)s * m * k, st));
-  QCH_CUDA(cudaMallocAsync((void**)&ys, (size_t)s * n * k, st));
+  QCH_CUDA(cudaMallocAsync((void**)&xs, (size_t)s * m * oz_ld((int)k), st));
+  QCH_CUDA(cudaMallocAsync((void**)&ys, (size_t)s * n * oz_ld((int)k), st));
   QCH_CUDA(cudaMallocAsync((void**)&ea, sizeof(int) * m, st));
   QCH_CUDA(cudaMallocAsync((void**)&eb, sizeof(int) * n, st));
   int rc = oz_slice((const double2*)d_x, (int)m, (int)k, 1, m * k, xcomp, s, xs, ea, st);
