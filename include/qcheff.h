@@ -280,12 +280,12 @@ double qch_dmma_flops(void);
 /* -------------------------------------- int8 tensor-core (tcgen05) ----- */
 
 /* The Hermitian products of exp(-iH) (qch_zgemm_herm_batched and the
- * expm's Paterson-Stockmeyer / cos-sin steps) for 512 <= n <= 16384 run by
- * default on the int8 tensor cores: each FP64 operand is cut into 8 exact
+ * expm's Paterson-Stockmeyer / cos-sin steps) for any 512 <= n <= 16384 run
+ * by default on the int8 tensor cores: each FP64 operand is cut into 8 exact
  * int8 slices (7 bits each, per-row power-of-two scale: the Ozaki scheme),
  * the 36 slice pairs with i + j <= 7 are multiplied with tcgen05.mma
- * kind::i8 (exact int32 in TMEM) and folded into FP64 — ~1e-15 relative,
- * FP64 level — in the Gauss / 3M complex form.  engine: 1 = int8 tensor
+ * kind::i8 (cta_group::2, 256 x 256 tiles, exact int32 in TMEM) and folded
+ * into FP64 — FP64 level — in the Gauss / 3M complex form.  engine: 1 = int8 tensor
  * cores, 0 = DMMA, -1 = query; returns the previous setting. */
 int qch_set_herm_gemm(int engine);
 /* int8 tensor operations (2 per MAC) issued by the Ozaki GEMMs so far (accounting). */
@@ -293,7 +293,7 @@ double qch_int8_ops(void);
 /* Diagnostics of the two building blocks: C_i32 (m x n) = A_i8 (m x k) .
  * B_i8 (n x k)^T on tcgen05 kind::i8 (k % 16 == 0), and P_f64 (m x n) =
  * X Y^T for one real component of complex matrices x (m x k), y (n x k)
- * (comp 0 Re, 1 Im, 2 Re+Im, 3 Re-Im, 4 -Im) through s slices. */
+ * (comp 0 Re, 1 Im, 2 Re+Im, 3 Re-Im, 4 -Im) through s slices (n even). */
 int qch_i8gemm_test(const void* d_a, const void* d_b, void* d_c, int64_t m, int64_t n, int64_t k, void* stream);
 int qch_oz_real_test(const void* d_x, int xcomp, const void* d_y, int ycomp, void* d_out, int64_t m, int64_t n,
                      int64_t k, int s, void* stream);
