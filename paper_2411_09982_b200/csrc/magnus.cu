@@ -134,19 +134,54 @@ __global__ void antiherm_kernel(const double2* __restrict__ p, int n, double2* _
   }
 }
 
-// per-matrix max row sum of |(-i H)|: one thread per row, numpy pairwise
-__global__ void rownorm_kernel(const double2* __restrict__ h, int n, int64_t batch,
-                               unsigned long long* __restrict__ norm) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// per-matrix max row sum of |(-i H)|, numpy's pairwise order: one WARP per
+// row — the top D levels of numpy's split tree (n -> n2 = n/2 - (n/2)%8 and
+// n - n2, every node above depth D larger than 128) are spread over the
+// 2^D lanes (lane bits = left/right choices, deepest level in bit 0), each
+// lane sums its subtree with np_pairwise_rec, and the 2^D partial sums are
+// combined by xor shuffles in tree order (fp addition commutes, so the
+// result is numpy's bit for bit).
+static int rownorm_depth(int n) {
+  auto ok = [](auto&& self, int size, int d) -> bool {
+    if (d == 0) return true;
+    if (size <= 128) return false;
+    int n2 = size / 2;
+    n2 -= n2 % 8;
+    return self(self, n2, d - 1) && self(self, size - n2, d - 1);
+  };
+  int D = 0;
+  while (D < 5 && ok(ok, n, D + 1)) ++D;
+  return D;
+}
+
+__global__ void __launch_bounds__(256) rownorm_kernel(const double2* __restrict__ h, int n, int64_t batch, int D,
+                                                      unsigned long long* __restrict__ norm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= (int64_t)n * batch) return;
-  int64_t b = t / n, r = t - b * n;
+  const int64_t b = t / n, r = t - b * n;
   const double2* row = h + b * (int64_t)n * n + r * n;
   auto f = [&](int c) {
-    double2 v = row[c];
+    const double2 v = row[c];
     return np_cabs(v.y, -v.x);
   };
-  double s = np_pairwise(f, n);
-  atomicMax(norm + b, (unsigned long long)__double_as_longlong(s));
+  double s = 0.0;
+  if (lane < (1 << D)) {
+    int off = 0, size = n;
+    for (int lv = 0; lv < D; ++lv) {
+      int n2 = size / 2;
+      n2 -= n2 % 8;
+      if ((lane >> (D - 1 - lv)) & 1) {
+        off += n2;
+        size -= n2;
+      } else {
+        size = n2;
+      }
+    }
+    s = np_pairwise_rec(f, off, size);
+  }
+  for (int k = 0; k < D; ++k) s = QADD(s, __shfl_xor_sync(0xffffffffu, s, 1 << k));
+  if (lane == 0) atomicMax(norm + b, (unsigned long long)__double_as_longlong(s));
 }
 
 // a = (-i H) / 2**s ; out = I + a ; term = a  (Taylor k = 1)
@@ -691,7 +726,7 @@ static int expm_generic(const double2* h, int64_t batch, int n, double2* u, doub
   const int64_t nn = (int64_t)n * n;
   unsigned* hflag = (unsigned*)(norm + batch);
   QCH_CUDA(cudaMemsetAsync(norm, 0, sizeof(unsigned long long) * 2 * batch, st));
-  rownorm_kernel<<<(int)((n * batch + 127) / 128), 128, 0, st>>>(h, n, batch, norm);
+  rownorm_kernel<<<(int)((n * batch + 7) / 8), 256, 0, st>>>(h, n, batch, rownorm_depth(n), norm);
   herm_check_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, n, batch, hflag);
   QCH_LAUNCH_CHECK("herm_check_kernel");
   note_launch(2);
