@@ -224,15 +224,26 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
 }
 
+// I 2^k exactly (I an int32 diagonal sum): one multiply by a constructed
+// power of two in the normal range, ldexp outside it
+__device__ __forceinline__ double oz_scaled(int I, int k) {
+  const double x = (double)I;
+  if (k >= -1022 && k <= 1023) return x * __longlong_as_double((long long)(k + 1023) << 52);
+  return ldexp(x, k);
+}
+
 // ---- wide / CTA-pair variants: FP64 accumulation in the output ----
 // The 128 x 128 kernel above keeps its FP64 accumulator in registers (64 per
 // epilogue thread), which caps the tile at 128 columns: per 128 x 128 x 32
 // MMA it stages 8 KB through shared memory (TMA write + MMA read = 2 x 8 KB
 // per 68 clk at int8 peak, well above the 128 B/clk shared-memory port).
-// Here the epilogue folds each diagonal straight into the output row in
-// global memory (P <- P + 2^-7(D+2) D_int, the same FMA in the same order;
-// the tile's rows are L2-resident and the epilogue of diagonal D overlaps
-// the MMAs of D+1), so the tile can be 128 x 256 (one CTA, TMEM 2 x 256
+// Here the epilogue folds each diagonal straight into the output in global
+// memory: diagonal 0 is stored, later ones are FP64 reductions at L2
+// (red.global.add.f64, no read round trip), each contribution already
+// carrying its full power of two D_int 2^(e_r + f_c - 7(D+2)) — exact, so the
+// sums round exactly as the register version's FMAs followed by the final
+// ldexp; the epilogue of diagonal D overlaps the MMAs of D+1), so the tile
+// can be 128 x 256 (one CTA, TMEM 2 x 256
 // columns) or 256 x BN on a CTA pair (cta_group::2: the MMA issued by the
 // even CTA reads A rows 0..127 / 128..255 and B rows 0..BN/2-1 / BN/2..BN-1
 // from the even / odd CTA's shared memory; each CTA's TMEM holds its own 128
@@ -424,8 +435,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const int buf = D & 1;
       oz_wait(oz_smem(tfull + buf), (unsigned)((D >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const double scl = ldexp(1.0, -7 * (D + 2));
-      const bool last = D == S - 1;
+      const int kD = er - 7 * (D + 2);  // + the column exponent: the contribution's power of two
 #pragma unroll 1
       for (int cb = 0; cb < BN / 2; cb += 32) {
         uint32_t v[32];
@@ -443,18 +453,21 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         const int c0 = n0 + half * (BN / 2) + cb;
         if (rok && c0 < g.n) {
           double* o = orow + c0;
-          const bool cfull = c0 + 32 <= g.n;  // ldo is even: paired accesses stay 16-byte aligned; a pair
-#pragma unroll                             // straddling column n writes the row's padding column
-          for (int e = 0; e < 32; e += 2) {
-            if (!cfull && c0 + e >= g.n) break;
-            double2 acc = D ? *(const double2*)(o + e) : make_double2(0.0, 0.0);
-            acc.x = fma((double)(int)v[e], scl, acc.x);
-            acc.y = fma((double)(int)v[e + 1], scl, acc.y);
-            if (last) {
-              acc.x = ldexp(acc.x, er + ebb[c0 + e]);
-              acc.y = ldexp(acc.y, er + ebb[c0 + e + 1 < g.n ? c0 + e + 1 : c0 + e]);
+          if (D == 0) {  // first diagonal: plain stores (paired; ldo is even, so 16-byte aligned; a pair
+                         // straddling column n writes the row's padding column)
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              if (c0 + e >= g.n) break;
+              const int e1 = c0 + e + 1 < g.n ? c0 + e + 1 : c0 + e;
+              *(double2*)(o + e) = make_double2(oz_scaled((int)v[e], kD + ebb[c0 + e]),
+                                                oz_scaled((int)v[e + 1], kD + ebb[e1]));
             }
-            *(double2*)(o + e) = acc;
+          } else {  // later diagonals: fire-and-forget FP64 reductions at L2 (no read round trip)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              if (c0 + e >= g.n) break;
+              atomicAdd(o + e, oz_scaled((int)v[e], kD + ebb[c0 + e]));
+            }
           }
         }
       }
