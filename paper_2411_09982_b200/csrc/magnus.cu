@@ -735,11 +735,12 @@ static int expm_generic(const double2* h, int64_t batch, int n, double2* u, doub
   QCH_CUDA(cudaStreamSynchronize(st));
   std::vector<int> hs(batch);
   int m = 1, smax = 0;
-  bool herm = true;
+  bool herm = true, finite = true;
   const unsigned* hf = (const unsigned*)(hn.data() + batch);
   for (int64_t b = 0; b < batch; ++b) {
     double nu;
     memcpy(&nu, &hn[b], sizeof nu);
+    if (!std::isfinite(nu)) finite = false;
     int s = 0;
     if (nu > kScaleTarget) s = (int)ceil(log2(nu / kScaleTarget));
     hs[b] = s;
@@ -749,8 +750,11 @@ static int expm_generic(const double2* h, int64_t batch, int n, double2* u, doub
   }
   QCH_CUDA(cudaMemcpyAsync(sarr, hs.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, st));
   static const bool force_ps = getenv("QCH_EXPM") && strcmp(getenv("QCH_EXPM"), "ps") == 0;
-  if (herm && !force_ps) return expm_herm(h, batch, n, u, work, sarr, m, smax, st);
-  return expm_ps(h, batch, n, u, work, sarr, norm, m, smax, st);
+  herm_force_dmma(!finite);  // NaN / Inf: the DMMA products propagate them (numpy's behaviour)
+  const int rc = (herm && !force_ps) ? expm_herm(h, batch, n, u, work, sarr, m, smax, st)
+                                     : expm_ps(h, batch, n, u, work, sarr, norm, m, smax, st);
+  herm_force_dmma(false);
+  return rc;
 }
 
 static int validate_generic(const double2* u, int64_t batch, int n, double2* scratch, double* dbuf,

@@ -322,7 +322,9 @@ int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream
 // Hermitian products of the exp(-iH) evaluation: Ozaki-sliced int8 tcgen05
 // GEMMs (ozgemm.cu) for 512 <= n <= 16384 by default, the DMMA kernel
 // otherwise or with QCH_HERM_GEMM=dmma
-bool herm_use_ozaki(int n) { return herm_engine() != 0 && n >= 512 && n <= 16384; }
+static thread_local int t_herm_force_dmma = 0;
+void herm_force_dmma(bool on) { t_herm_force_dmma = on ? 1 : 0; }
+bool herm_use_ozaki(int n) { return herm_engine() != 0 && !t_herm_force_dmma && n >= 512 && n <= 16384; }
 static bool use_ozaki(int n) { return herm_use_ozaki(n); }
 
 int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st, OzCache* oc) {

@@ -64,6 +64,10 @@ struct OzCache {
 int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, const double2* const* pw,
                      const double* q, int nq, int n, int64_t batch, cudaStream_t st, OzCache* cache = nullptr);
 bool herm_use_ozaki(int n);
+// this thread's next Hermitian products on DMMA regardless of the engine
+// (non-finite operands: the int8 slices cannot carry NaN / Inf, DMMA
+// propagates them as numpy does)
+void herm_force_dmma(bool on);
 double oz_int8_ops_total();
 int oz_slices();
 int herm_engine();  // 1: int8 tensor cores (Ozaki), 0: DMMA

@@ -103,3 +103,25 @@ def test_herm_products_int8_vs_fp64(L, n, batch):
             np.testing.assert_array_equal(got[:, off], np.conj(np.swapaxes(got, 1, 2))[:, off])
     finally:
         L.load().qch_set_herm_gemm(old)
+
+
+def test_nonfinite_operator_takes_dmma_and_propagates_nan(L):
+    """A NaN in an N > 4 operator reaching the propagator stage: the int8
+    slices cannot carry it, so that batch runs on the DMMA products, which
+    propagate the NaN as numpy's expm would — the trajectory must not come
+    back finite (an error, or NaN states, as the reference)."""
+    import paper_2411_09982_b200 as E
+
+    ch = E.heisenberg_chain_hamiltonians(9)  # dim 512: the int8 engine's range
+    d = ch.drift.to_dense().copy()
+    d[3, 3] = np.nan
+    ch2 = E.ControlledHamiltonian(E.HermitianOperator(d, validate=False), ch.controls)
+    pulse = E.synthetic_transfer_pulse(1.0, 2 * 8 + 1, seed=1)
+    grid = E.ControlGrid(0.0, 1.0, pulse.signals)
+    psi0 = np.zeros(512, dtype=complex)
+    psi0[0] = 1
+    try:
+        traj = E.evolve(ch2, grid, 2, psi0, order=2, check=False)
+    except (E.NonFinite, E.NormDrift):
+        return
+    assert np.isnan(np.asarray(traj.amplitudes)[1:]).any()
