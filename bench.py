@@ -576,11 +576,6 @@ def _herm_fraction(n, bm=128, bn=64):
     return sum(min(2 * r + 2, tn) for r in range(tm)) / (tm * tn)
 
 
-def _oz_pairs():
-    s = int(os.environ.get("QCH_OZ_SLICES", "8"))
-    return s * (s + 1) // 2
-
-
 def _dmma_sample(torch, eff, lib, ch, grid_full, psi0, n_int=32):
     """The DMMA engine on the first n_int intervals of config 5 (the FP64
     tensor-pipe roofline of the north star; the default engine is int8)."""
@@ -635,6 +630,7 @@ def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
     lib.profile_enable(True)
     fl0 = float(lib.load().qch_dmma_flops())
     op0 = float(lib.load().qch_int8_ops())
+    eq0 = float(lib.load().qch_int8_fp64_equiv_flops())
     if world == 1:
         mg.PHASE_TIMING = True
         ms = time_steps(torch, lambda: eff.evolve(ch, grid, n_int, psi0, order=2, check=False), 1, lambda: None, 1)
@@ -664,6 +660,7 @@ def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
     # the dominant kernel of the default engine: oz_gemm (int8 tensor cores)
     oz_ms = max_over_ranks(torch, prof.get("oz_gemm", (0.0, 0))[0], world)
     ops = sum_over_ranks(torch, float(lib.load().qch_int8_ops()) - op0, world)
+    eqf = sum_over_ranks(torch, float(lib.load().qch_int8_fp64_equiv_flops()) - eq0, world)
     dm_ms = max_over_ranks(torch, sum(v[0] for k, v in prof.items() if k.startswith("zgemm")), world)
     dm_fl = sum_over_ranks(torch, float(lib.load().qch_dmma_flops()) - fl0, world)
     mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -679,12 +676,13 @@ def sec_magnus4096(torch, eff, lib, args, fp64, world=1, rank=0, n_int=4096):
                 "achieved": ach, "peak": i8_peak, "unit": "TOPS (int8)", "frac": ach / i8_peak,
                 "peak_kind": i8_kind, "nominal_peak": 4500.0,
                 "ops_basis": "int8 tensor ops issued by the library (qch_int8_ops): 3 real products per complex "
-                             "product x 36 slice pairs x 2 M N K per computed tile",
+                             "product x the slice pairs each product uses (adaptive plan: 36 / 28 / 21 / 15 for "
+                             "8 / 7 / 6 / 5 slices) x 2 M N K per computed tile",
                 "gemm_ms": oz_ms,
-                "fp64_equivalent_tflops": ops / (0.75 * _oz_pairs()) / world / (oz_ms * 1e-3) / 1e12,
-                "fp64_equivalent_note": "complex-product flops the int8 GEMMs stand in for (8 M N K per computed "
-                                        "tile = int8 ops / (3 real products x slice pairs x 2 / 8)) / int8 GEMM "
-                                        f"time -- vs the live DMMA peak {fp64.get('dmma', 0):.1f} TFLOP/s",
+                "fp64_equivalent_tflops": eqf / world / (oz_ms * 1e-3) / 1e12,
+                "fp64_equivalent_note": "complex-product flops the int8 GEMMs stand in for (8 M N K over the computed "
+                                        "tiles, qch_int8_fp64_equiv_flops) / int8 GEMM time -- vs the live DMMA peak "
+                                        f"{fp64.get('dmma', 0):.1f} TFLOP/s",
                 "kernel_ms": kernels_ms,
                 "traffic": traffic_from_profiles("oz_gemmw_kernel@oz")}
     else:

@@ -288,8 +288,11 @@ double qch_dmma_flops(void);
  * into FP64 — FP64 level — in the Gauss / 3M complex form.  engine: 1 = int8 tensor
  * cores, 0 = DMMA, -1 = query; returns the previous setting. */
 int qch_set_herm_gemm(int engine);
-/* int8 tensor operations (2 per MAC) issued by the Ozaki GEMMs so far (accounting). */
+/* int8 tensor operations (2 per MAC) issued by the Ozaki GEMMs so far, and
+ * the FP64 complex-product flops (8 M N K over the computed tiles) those
+ * GEMMs stood in for (accounting). */
 double qch_int8_ops(void);
+double qch_int8_fp64_equiv_flops(void);
 /* Diagnostics of the two building blocks: C_i32 (m x n) = A_i8 (m x k) .
  * B_i8 (n x k)^T on tcgen05 kind::i8 (k % 16 == 0), and P_f64 (m x n) =
  * X Y^T for one real component of complex matrices x (m x k), y (n x k)

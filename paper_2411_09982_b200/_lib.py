@@ -123,6 +123,7 @@ PROTOTYPES = {
     "qch_dmma_flops": (c_double, []),
     "qch_set_herm_gemm": (c_int, [c_int]),
     "qch_int8_ops": (c_double, []),
+    "qch_int8_fp64_equiv_flops": (c_double, []),
     "qch_i8gemm_test": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
     "qch_oz_real_test": (
         c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p]),

@@ -17,6 +17,8 @@
 //    complex GEMM with the fused "term = term@a/k; out += term" epilogue
 //    (zgemm.cu), squaring, then the sequential ordered product.
 #include <algorithm>
+#include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -618,8 +620,30 @@ static int herm_gemm_count(int q, int dc, int dt) {
   return q + g(dc) + g(dt) + 1;
 }
 
+// Slices per int8 (Ozaki) product of expm_herm.  A product whose result
+// reaches U through small Taylor coefficients or high powers of B needs
+// fewer correct bits: with nu = max ||Hs||_inf over the batch, every product
+// k gets a bound E_k = (weight of its result in U) x ||X|| ||Y|| on the size
+// of its contribution, and uses 8 - floor(log2(E_ref / E_k) / 7) slices (>= 4),
+// E_ref = the smaller of the two full-weight products (B = Hs Hs and the
+// final Hs T).  Each slice removed scales a product's error by 2^7, so every
+// product's error stays below the full-precision products' own — the
+// result keeps the all-8-slice accuracy within a small factor (tests).
+// QCH_OZ_ADAPT=0: every product on all slices.
+struct OzPlan {
+  bool on = false;
+  double nu = 0.0, eref = 0.0;
+  int slices(double e) const {
+    if (!on || !(e > 0.0) || !(eref > 0.0)) return 0;
+    const double r = eref / e;
+    if (!(r > 1.0)) return 0;
+    const int drop = (int)std::floor(std::log2(r) / 7.0);
+    return std::max(4, 8 - drop);
+  }
+};
+
 static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2* work, int* sarr, int m, int smax,
-                     cudaStream_t st) {
+                     cudaStream_t st, double nu_max) {
   const int64_t nn = (int64_t)n * n;
   double2* W[8];
   for (int i = 0; i < 8; ++i) W[i] = work + i * batch * nn;
@@ -645,14 +669,48 @@ static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2
       const int cst = herm_gemm_count(qq, dc, dt);
       if (cst < best) best = cst, q = qq;
     }
-    if (int rc = zgemm_herm(hs, hs, P[1], n, batch, st, oc)) return rc;
-    for (int j = 2; j <= q; ++j)
-      if (int rc = zgemm_herm(P[j - 1], P[1], P[j], n, batch, st, oc)) return rc;
-    for (int j = 1; j < q; ++j) drop(P[j]);  // only B^q is a GEMM operand from here on
   }
   double fac[20];
   fac[0] = 1.0;
   for (int k = 1; k < 20; ++k) fac[k] = fac[k - 1] * k;
+  double cc[20], tc[20];
+  for (int j = 0; j <= dc; ++j) cc[j] = ((j & 1) ? -1.0 : 1.0) / fac[2 * j];
+  for (int j = 0; j <= dt; ++j) tc[j] = ((j & 1) ? -1.0 : 1.0) / fac[2 * j + 1];
+  // slice plan (int8 engine): norm bounds from nu, weights from the coefficients
+  OzPlan pl;
+  const bool adapt = !(getenv("QCH_OZ_ADAPT") && atoi(getenv("QCH_OZ_ADAPT")) == 0);  // read per call
+  const double nu = nu_max, nb = nu * nu;  // ||Hs||, ||B|| bounds
+  auto tail = [&](const double* c, int d, int from) {  // ||sum_{i >= from} c_i B^(i - from)||
+    double t = 0.0, p = 1.0;
+    for (int i = from; i <= d; ++i, p *= nb) t += std::fabs(c[i]) * p;
+    return t;
+  };
+  double e_pow[5] = {0, 0, 0, 0, 0};
+  if (oc && adapt && q >= 1) {
+    pl.on = true;
+    pl.nu = nu;
+    double w[6] = {0, 0, 0, 0, 0, 0};  // weight of B^j in U
+    for (int j = q; j >= 1; --j) {
+      w[j] = (j <= dc ? std::fabs(cc[j]) : 0.0) + nu * (j <= dt ? std::fabs(tc[j]) : 0.0);
+      if (j == q) w[j] += tail(cc, dc, q) + nu * tail(tc, dt, q);  // B^q times the Horner accumulators
+      if (j < q) w[j] += nb * w[j + 1];                              // B^j -> B^(j+1) = B^j B
+    }
+    for (int j = 1; j <= q; ++j) e_pow[j] = w[j] * std::pow(nb, j);  // ||B^(j-1)|| ||B|| (j = 1: ||Hs||^2)
+    const double e_ufin = nu * tail(tc, dt, 0);
+    pl.eref = std::min(e_pow[1], e_ufin);
+    static const bool show = getenv("QCH_OZ_PLAN") != nullptr;
+    if (show) {
+      fprintf(stderr, "[qch oz plan] n %d nu %.4g m %d q %d | slices: B^1..B^%d", n, nu, m, q, q);
+      for (int j = 1; j <= q; ++j) fprintf(stderr, " %d", pl.slices(e_pow[j]) ? pl.slices(e_pow[j]) : 8);
+      fprintf(stderr, " | U %d\n", pl.slices(e_ufin) ? pl.slices(e_ufin) : 8);
+    }
+  }
+  if (q >= 1) {
+    if (int rc = zgemm_herm(hs, hs, P[1], n, batch, st, oc, pl.slices(e_pow[1]))) return rc;
+    for (int j = 2; j <= q; ++j)
+      if (int rc = zgemm_herm(P[j - 1], P[1], P[j], n, batch, st, oc, pl.slices(e_pow[j]))) return rc;
+    for (int j = 1; j < q; ++j) drop(P[j]);  // only B^q is a GEMM operand from here on
+  }
   auto comb = [&](double2* out, const double* coef, int deg) -> int {  // sum_{i<=deg} coef_i P_i
     CombArgs a{};
     a.c[0] = coef[0];
@@ -668,7 +726,8 @@ static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2
     return QCH_OK;
   };
   // p(B) = sum_{i<=d} coef_i B^i by Paterson-Stockmeyer into one of bufs[0..1]
-  auto poly = [&](const double* coef, int d, double2* b0, double2* b1, double2** res) -> int {
+  // wpoly: weight of the polynomial in U (C: 1, T: nu — it is multiplied by Hs)
+  auto poly = [&](const double* coef, int d, double wpoly, double2* b0, double2* b1, double2** res) -> int {
     double2* bufs[2] = {b0, b1};
     int cur = 0;
     if (d < q || q == 0) {
@@ -692,20 +751,22 @@ static int expm_herm(const double2* h, int64_t batch, int n, double2* u, double2
       const double2* pp[4] = {P[1], P[2], P[3], P[4]};
       double qc[5] = {0, 0, 0, 0, 0};
       for (int i = 0; i < q; ++i) qc[i] = coef[j * q + i];
-      if (int rc = zgemm_qacc(true, P[q], bufs[cur], bufs[cur ^ 1], pp, qc, q - 1, n, batch, st, oc)) return rc;
+      // this step's product B^q X (||X|| <= tail from (j+1) q) reaches U through j more steps (x B^q each)
+      const double e = wpoly * std::pow(nb, q * (j + 1)) * tail(coef, d, (j + 1) * q);
+      static const bool show = getenv("QCH_OZ_PLAN") != nullptr;
+      if (show && pl.on) fprintf(stderr, "[qch oz plan]   Horner step %d (w %.3g): slices %d\n", j, wpoly, pl.slices(e) ? pl.slices(e) : 8);
+      if (int rc = zgemm_qacc(true, P[q], bufs[cur], bufs[cur ^ 1], pp, qc, q - 1, n, batch, st, oc, pl.slices(e)))
+        return rc;
       drop(bufs[cur]);
       cur ^= 1;
     }
     *res = bufs[cur];
     return QCH_OK;
   };
-  double cc[20], tc[20];
-  for (int j = 0; j <= dc; ++j) cc[j] = ((j & 1) ? -1.0 : 1.0) / fac[2 * j];
-  for (int j = 0; j <= dt; ++j) tc[j] = ((j & 1) ? -1.0 : 1.0) / fac[2 * j + 1];
   double2* C = nullptr;
   double2* T = nullptr;
-  if (int rc = poly(cc, dc, W[5], W[6], &C)) return rc;
-  if (int rc = poly(tc, dt, W[7], C == W[5] ? W[6] : W[5], &T)) return rc;
+  if (int rc = poly(cc, dc, 1.0, W[5], W[6], &C)) return rc;
+  if (int rc = poly(tc, dt, nu, W[7], C == W[5] ? W[6] : W[5], &T)) return rc;
   if (q) drop(P[q]);
   if (int rc = zgemm_ufin(hs, T, C, u, n, batch, st, oc)) return rc;
   if (oc) oc->clear();
@@ -736,11 +797,13 @@ static int expm_generic(const double2* h, int64_t batch, int n, double2* u, doub
   std::vector<int> hs(batch);
   int m = 1, smax = 0;
   bool herm = true, finite = true;
+  double nu_max = 0.0;  // max ||Hs||_inf (after scaling) over the batch
   const unsigned* hf = (const unsigned*)(hn.data() + batch);
   for (int64_t b = 0; b < batch; ++b) {
     double nu;
     memcpy(&nu, &hn[b], sizeof nu);
     if (!std::isfinite(nu)) finite = false;
+    nu_max = std::max(nu_max, ldexp(nu, -(nu > kScaleTarget ? (int)ceil(log2(nu / kScaleTarget)) : 0)));
     int s = 0;
     if (nu > kScaleTarget) s = (int)ceil(log2(nu / kScaleTarget));
     hs[b] = s;
@@ -751,7 +814,7 @@ static int expm_generic(const double2* h, int64_t batch, int n, double2* u, doub
   QCH_CUDA(cudaMemcpyAsync(sarr, hs.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, st));
   static const bool force_ps = getenv("QCH_EXPM") && strcmp(getenv("QCH_EXPM"), "ps") == 0;
   herm_force_dmma(!finite);  // NaN / Inf: the DMMA products propagate them (numpy's behaviour)
-  const int rc = (herm && !force_ps) ? expm_herm(h, batch, n, u, work, sarr, m, smax, st)
+  const int rc = (herm && !force_ps) ? expm_herm(h, batch, n, u, work, sarr, m, smax, st, nu_max)
                                      : expm_ps(h, batch, n, u, work, sarr, norm, m, smax, st);
   herm_force_dmma(false);
   return rc;

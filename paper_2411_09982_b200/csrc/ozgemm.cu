@@ -73,7 +73,8 @@ struct OzArgs {
   const int* ea;   // [batch][m] row exponents of X
   const int* eb;   // [batch][n] row exponents of Y
   double* out;     // [batch][m][ldo] (P = X Y^T)
-  int m, n, k, s;  // s slices
+  int m, n, k, s;  // s: leading slices used (digits), <= sp
+  int sp;          // slice planes stored per batch item
   int ldo;
   int64_t so;      // batch stride of out
   const int* tiles;  // optional tile list (ti << 16 | tj); null: all tiles
@@ -138,8 +139,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             const unsigned fb = oz_smem(full + q);
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(OZ_STAGE) : "memory");
             const unsigned dA = oz_smem(base + q * OZ_STAGE);
-            oz_tma3(dA, &tmA, kt * OZ_BK, m0, bz * S + i, fb);
-            oz_tma3(dA + OZ_BM * OZ_BK, &tmB, kt * OZ_BK, n0, bz * S + (D - i), fb);
+            oz_tma3(dA, &tmA, kt * OZ_BK, m0, bz * g.sp + i, fb);
+            oz_tma3(dA + OZ_BM * OZ_BK, &tmB, kt * OZ_BK, n0, bz * g.sp + (D - i), fb);
           }
     }
   } else if (warp == 1) {
@@ -352,13 +353,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               if (rank == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(2 * W::STAGE)
                              : "memory");
-              oz_tma3_pair(dA, &tmA, kt * OZ_BK, m0, bz * S + i, fb);
-              oz_tma3_pair(dA + OZ_BM * OZ_BK, &tmB, kt * OZ_BK, nb0, bz * S + (D - i), fb);
+              oz_tma3_pair(dA, &tmA, kt * OZ_BK, m0, bz * g.sp + i, fb);
+              oz_tma3_pair(dA + OZ_BM * OZ_BK, &tmB, kt * OZ_BK, nb0, bz * g.sp + (D - i), fb);
             } else {
               asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(W::STAGE)
                            : "memory");
-              oz_tma3(dA, &tmA, kt * OZ_BK, m0, bz * S + i, fb);
-              oz_tma3(dA + OZ_BM * OZ_BK, &tmB, kt * OZ_BK, nb0, bz * S + (D - i), fb);
+              oz_tma3(dA, &tmA, kt * OZ_BK, m0, bz * g.sp + i, fb);
+              oz_tma3(dA + OZ_BM * OZ_BK, &tmB, kt * OZ_BK, nb0, bz * g.sp + (D - i), fb);
             }
           }
     }
@@ -738,8 +739,10 @@ static int oz_launch_w(const CUtensorMap& ma, const CUtensorMap& mb, const OzArg
 
 int oz_gemm(const int8_t* xs, const int* ea, const int8_t* ys, const int* eb, int m, int n, int k, int s,
             int64_t batch, double* out, int ldo, int64_t so, const int* tiles, int ntiles, cudaStream_t st,
-            double* ops) {
-  if (s < 1 || s > OZ_MAX_S) return fail(QCH_ERR_VALUE, "ozaki: 1..8 slices");
+            double* ops, int sp) {
+  if (sp <= 0) sp = s;  // planes stored per item (the leading s of them are used: the digits of a shorter
+                        // slicing are the leading digits of a longer one)
+  if (s < 1 || s > OZ_MAX_S || s > sp) return fail(QCH_ERR_VALUE, "ozaki: 1..8 slices, at most the stored ones");
   if (ldo % 2 || ldo < n || so % 2) return fail(QCH_ERR_VALUE, "ozaki: the output row stride must be even and >= n");
   // exact int32 accumulation: (slices per diagonal) K 127^2 < 2^31
   if ((int64_t)s * k * 127 * 127 >= (int64_t)1 << 31)
@@ -748,8 +751,8 @@ int oz_gemm(const int8_t* xs, const int* ea, const int8_t* ys, const int* eb, in
   const int cfg = oz_cfg();
   const int rows_per_tile = oz_tile_rows(), bn = oz_tile_cols();
   CUtensorMap ma, mb;
-  if (int rc = oz_map(&ma, xs, m, k, batch * s)) return rc;
-  if (int rc = oz_map(&mb, ys, n, k, batch * s, cfg >= 2 ? bn / 2 : bn)) return rc;
+  if (int rc = oz_map(&ma, xs, m, k, batch * sp)) return rc;
+  if (int rc = oz_map(&mb, ys, n, k, batch * sp, cfg >= 2 ? bn / 2 : bn)) return rc;
   OzArgs g{};
   g.ea = ea;
   g.eb = eb;
@@ -758,6 +761,7 @@ int oz_gemm(const int8_t* xs, const int* ea, const int8_t* ys, const int* eb, in
   g.n = n;
   g.k = k;
   g.s = s;
+  g.sp = sp;
   g.ldo = ldo;
   g.so = so;
   g.tiles = tiles;
@@ -913,7 +917,13 @@ int oz_slices() {
 }
 
 static std::atomic<double> g_i8_ops{0.0};
+static std::atomic<double> g_i8_fp64eq{0.0};  // complex-product flops (8 M N K, computed tiles) stood in for
 double oz_int8_ops_total() { return g_i8_ops.load(); }
+static void atomic_add_d(std::atomic<double>& a, double v) {
+  double cur = a.load();
+  while (!a.compare_exchange_weak(cur, cur + v)) {
+  }
+}
 
 // ---- slice cache (OzCache, zgemm.h) ----
 OzCache::~OzCache() { clear(); }
@@ -967,13 +977,14 @@ int OzCache::get(const double2* src, unsigned mask, const OzCache::Entry** out) 
 }
 
 int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, const double2* const* pw,
-                     const double* q, int nq, int n, int64_t batch, cudaStream_t st, OzCache* cache) {
+                     const double* q, int nq, int n, int64_t batch, cudaStream_t st, OzCache* cache, int s_use) {
   if (c == a || c == b) return fail(QCH_ERR_VALUE, "ozaki Hermitian product: output aliases an operand");
   ensure_pool();
   OzCache local(n, batch, st);
   OzCache* oc = cache ? cache : &local;
   if (oc->n != n || oc->batch != batch) return fail(QCH_ERR_VALUE, "ozaki slice cache: shape mismatch");
-  const int S = oz_slices();
+  const int SP = oz_slices();                               // slices cut and stored
+  const int S = (s_use > 0 && s_use < SP) ? s_use : SP;     // leading slices this product uses
   const int64_t nn = (int64_t)n * n;
   const OzCache::Entry *X = nullptr, *Y = nullptr;
   const unsigned ma = a == b ? 0xF : 0x7;  // A: Re, Im, Re + Im (+ Re - Im when it is also B)
@@ -993,13 +1004,12 @@ int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, c
   for (int v = 0; v < 3 && rc == QCH_OK; ++v) {
     double o = 0.0;
     rc = oz_gemm(X->sl[v], X->ex[v], Y->sl[yc[v]], Y->ex[yc[v]], n, n, n, S, batch, P + v * np_ * batch, ldp, np_, tiles,
-                 ntiles, st, &o);
+                 ntiles, st, &o, SP);
     ops += o;
   }
   if (rc == QCH_OK) {
-    double cur = g_i8_ops.load();
-    while (!g_i8_ops.compare_exchange_weak(cur, cur + ops)) {
-    }
+    atomic_add_d(g_i8_ops, ops);
+    atomic_add_d(g_i8_fp64eq, 8.0 * ntiles * (double)oz_tile_rows() * oz_tile_cols() * n * batch);
     OzCombine cm{};
     cm.p1 = P;
     cm.p2 = P + np_ * batch;
@@ -1045,6 +1055,7 @@ extern "C" int qch_set_herm_gemm(int engine) {
 }
 
 extern "C" double qch_int8_ops(void) { return oz_int8_ops_total(); }
+extern "C" double qch_int8_fp64_equiv_flops(void) { return g_i8_fp64eq.load(); }
 
 // experimental: P (m x n, f64) = X Y^T for real components of complex matrices
 // x (m x k) and y (n x k) (comp as oz_slice_kernel), s slices
@@ -1062,7 +1073,8 @@ extern "C" int qch_oz_real_test(const void* d_x, int xcomp, const void* d_y, int
   int rc = oz_slice((const double2*)d_x, (int)m, (int)k, 1, m * k, xcomp, s, xs, ea, st);
   if (!rc) rc = oz_slice((const double2*)d_y, (int)n, (int)k, 1, n * k, ycomp, s, ys, eb, st);
   if (!rc)
-    rc = oz_gemm(xs, ea, ys, eb, (int)m, (int)n, (int)k, s, 1, (double*)d_out, (int)n, m * n, nullptr, 0, st, nullptr);
+    rc = oz_gemm(xs, ea, ys, eb, (int)m, (int)n, (int)k, s, 1, (double*)d_out, (int)n, m * n, nullptr, 0, st, nullptr,
+                 s);
   cudaFreeAsync(xs, st);
   cudaFreeAsync(ys, st);
   cudaFreeAsync(ea, st);

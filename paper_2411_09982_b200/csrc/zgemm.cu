@@ -327,8 +327,9 @@ void herm_force_dmma(bool on) { t_herm_force_dmma = on ? 1 : 0; }
 bool herm_use_ozaki(int n) { return herm_engine() != 0 && !t_herm_force_dmma && n >= 512 && n <= 16384; }
 static bool use_ozaki(int n) { return herm_use_ozaki(n); }
 
-int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st, OzCache* oc) {
-  if (use_ozaki(n)) return zgemm_herm_ozaki(ZT_STORE, a, b, c, nullptr, nullptr, 0, n, batch, st, oc);
+int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st, OzCache* oc,
+               int s_use) {
+  if (use_ozaki(n)) return zgemm_herm_ozaki(ZT_STORE, a, b, c, nullptr, nullptr, 0, n, batch, st, oc, s_use);
   ZtArgs g{};
   g.c = c;
   const int64_t nn = (int64_t)n * n;
@@ -336,9 +337,9 @@ int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t ba
 }
 
 int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const double2* const* p, const double* q,
-               int nq, int n, int64_t batch, cudaStream_t st, OzCache* oc) {
+               int nq, int n, int64_t batch, cudaStream_t st, OzCache* oc, int s_use) {
   if (nq > 4) return fail(QCH_ERR_UNSUPPORTED, "zgemm_qacc: at most 4 power terms");
-  if (herm && use_ozaki(n)) return zgemm_herm_ozaki(ZT_QACC, a, b, c, p, q, nq, n, batch, st, oc);
+  if (herm && use_ozaki(n)) return zgemm_herm_ozaki(ZT_QACC, a, b, c, p, q, nq, n, batch, st, oc, s_use);
   ZtArgs g{};
   g.c = c;
   g.nq = nq;
@@ -352,10 +353,10 @@ int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const 
 }
 
 int zgemm_ufin(const double2* a, const double2* b, const double2* cpart, double2* u, int n, int64_t batch,
-               cudaStream_t st, OzCache* oc) {
+               cudaStream_t st, OzCache* oc, int s_use) {
   if (use_ozaki(n)) {
     const double2* pw[1] = {cpart};
-    return zgemm_herm_ozaki(ZT_UFIN, a, b, u, pw, nullptr, 0, n, batch, st, oc);
+    return zgemm_herm_ozaki(ZT_UFIN, a, b, u, pw, nullptr, 0, n, batch, st, oc, s_use);
   }
   ZtArgs g{};
   g.c = u;

@@ -61,8 +61,11 @@ struct OzCache {
   void drop(const void* src);
   void clear();
 };
+// s_use: leading slices this product uses (0 = all; the expm passes fewer
+// for products whose contribution to U is small, see expm_herm)
 int zgemm_herm_ozaki(int mode, const double2* a, const double2* b, double2* c, const double2* const* pw,
-                     const double* q, int nq, int n, int64_t batch, cudaStream_t st, OzCache* cache = nullptr);
+                     const double* q, int nq, int n, int64_t batch, cudaStream_t st, OzCache* cache = nullptr,
+                     int s_use = 0);
 bool herm_use_ozaki(int n);
 // this thread's next Hermitian products on DMMA regardless of the engine
 // (non-finite operands: the int8 slices cannot carry NaN / Inf, DMMA
@@ -79,12 +82,12 @@ int zgemm_accum(const double2* a, const double2* b, double2* c, int n, int64_t b
 int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream_t st);
 // Hermitian products of commuting Hermitian n x n factors (batched)
 int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st,
-               OzCache* oc = nullptr);
+               OzCache* oc = nullptr, int s_use = 0);
 // C = q0 I + sum_i q_i P_i + A B  (nq <= 4), Hermitian when herm
 int zgemm_qacc(bool herm, const double2* a, const double2* b, double2* c, const double2* const* p, const double* q,
-               int nq, int n, int64_t batch, cudaStream_t st, OzCache* oc = nullptr);
+               int nq, int n, int64_t batch, cudaStream_t st, OzCache* oc = nullptr, int s_use = 0);
 // U = C - i (A B), A B Hermitian
 int zgemm_ufin(const double2* a, const double2* b, const double2* cpart, double2* u, int n, int64_t batch,
-               cudaStream_t st, OzCache* oc = nullptr);
+               cudaStream_t st, OzCache* oc = nullptr, int s_use = 0);
 
 }  // namespace qch

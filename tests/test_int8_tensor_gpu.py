@@ -125,3 +125,23 @@ def test_nonfinite_operator_takes_dmma_and_propagates_nan(L):
     except (E.NonFinite, E.NormDrift):
         return
     assert np.isnan(np.asarray(traj.amplitudes)[1:]).any()
+
+
+@pytest.mark.parametrize("scale", [0.05, 0.45, 3.0])
+def test_adaptive_slice_plan_matches_full_slices(L, scale, monkeypatch):
+    """The adaptive plan (fewer slices for the products that reach U through
+    small coefficients / high powers) against every product on 8 slices and
+    against the oracle, over norms below, near and above the scaling target."""
+    import paper_2411_09982_b200 as E
+
+    n = 640
+    rng = np.random.default_rng(int(scale * 100))
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = (a + a.conj().T)
+    h *= scale / np.abs(h).sum(axis=1).max()  # ||H||_inf = scale
+    monkeypatch.setenv("QCH_OZ_ADAPT", "0")
+    full = E.expm_unitary(h).entries
+    monkeypatch.setenv("QCH_OZ_ADAPT", "1")
+    adapt = E.expm_unitary(h).entries
+    assert rel_fro(adapt, full) <= 1e-15
+    assert rel_fro(adapt, expm_oracle.expm_minus_i(h)) <= 1e-12
