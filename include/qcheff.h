@@ -285,7 +285,9 @@ double qch_dmma_flops(void);
  * int8 slices (7 bits each, per-row power-of-two scale: the Ozaki scheme),
  * the 36 slice pairs with i + j <= 7 are multiplied with tcgen05.mma
  * kind::i8 (cta_group::2, 256 x 256 tiles, exact int32 in TMEM) and folded
- * into FP64 — FP64 level — in the Gauss / 3M complex form.  engine: 1 = int8 tensor
+ * into FP64 — FP64 level — in the Gauss / 3M complex form.  Inside the
+ * expm, products that reach U only through small Taylor weights use fewer
+ * leading slices (an error-bound plan, QCH_OZ_ADAPT=0 disables).  engine: 1 = int8 tensor
  * cores, 0 = DMMA, -1 = query; returns the previous setting. */
 int qch_set_herm_gemm(int engine);
 /* int8 tensor operations (2 per MAC) issued by the Ozaki GEMMs so far, and
