@@ -1,4 +1,7 @@
 // capi.cu — error plumbing, device queries and the launch counter of libqcheff.
+#include <map>
+#include <mutex>
+
 #include "qch_internal.h"
 
 namespace qch {
@@ -36,6 +39,19 @@ void ensure_pool() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   done[dev] = true;
+}
+
+cudaError_t smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{func, dev}];
+  if (have >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
 }
 
 int max_smem_optin() {

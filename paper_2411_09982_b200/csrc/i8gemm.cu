@@ -202,11 +202,7 @@ static int i8_run(const void* d_a, const void* d_b, void* d_c, int64_t m, int64_
   if (int rc = i8_map(&mb, d_b, n, k, 128)) return rc;
   constexpr int ST = BN == 128 ? 6 : 4;
   const int smem = ST * (I8_BM + BN) * I8_BK + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    QCH_CUDA(cudaFuncSetAttribute(i8gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  QCH_CUDA(smem_attr((const void*)i8gemm_kernel<BN>, smem));
   const int tiles = (int)(((m + I8_BM - 1) / I8_BM) * ((n + BN - 1) / BN));
   void* pr = prof_begin("i8gemm", st);
   i8gemm_kernel<BN><<<tiles, I8_THREADS, smem, st>>>(ma, mb, (int32_t*)d_c, (int)m, (int)n, (int)k);

@@ -988,12 +988,7 @@ static int chain_run(const double2* u, int64_t N, int64_t cm, const double2* psi
   if (N <= 64) {
     void* pr = prof_begin("chain_cta64_kernel", st);
     const size_t ring = sizeof(double2) * kChainStages * (size_t)N * N;
-    static bool attr64 = false;
-    if (!attr64) {
-      QCH_CUDA(cudaFuncSetAttribute(chain_cta64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(sizeof(double2) * kChainStages * 64 * 64)));
-      attr64 = true;
-    }
+    QCH_CUDA(smem_attr((const void*)chain_cta64_kernel, (int)(sizeof(double2) * kChainStages * 64 * 64)));
     chain_cta64_kernel<<<1, 256, ring, st>>>(u, (int)N, cm, psi, traj_rows, m0, bad_norm);
     prof_end(pr, st);
     QCH_LAUNCH_CHECK("chain_cta64_kernel");

@@ -692,12 +692,13 @@ static int fused_launch(FusedArgs& g, cudaStream_t st) {
   if (smem_optin == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    QCH_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    int v = 0;
+    QCH_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa;
     QCH_CUDA(cudaFuncGetAttributes(&fa, magnus_fused_kernel<N>));
-    smem_optin -= (int)fa.sharedSizeBytes;  // dynamic share of the opt-in maximum
-    QCH_CUDA(cudaFuncSetAttribute(magnus_fused_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
+    smem_optin = v - (int)fa.sharedSizeBytes;  // dynamic share of the opt-in maximum
   }
+  QCH_CUDA(smem_attr((const void*)magnus_fused_kernel<N>, smem_optin));  // per device
   const size_t wbytes = (((size_t)g.s.ca.K * g.win + 1) & ~(size_t)1) * sizeof(double);
   const size_t tbytes = sizeof(double2) * (size_t)kTile * N;
   const size_t sbase = fused_smem<N>(g.s.ca.K) + (g.win > 0 && wbytes >= tbytes ? 0 : tbytes);

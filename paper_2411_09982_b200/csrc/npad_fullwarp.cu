@@ -297,14 +297,8 @@ bool npad_full_warp_ok(const NpadCommon2& cm, bool herm, bool trows) {
 
 int npad_launch_full_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (size_t)cm.n * kPitch;
-  static bool attr = false;
-  if (!attr) {
-    QCH_CUDA(cudaFuncSetAttribute(npad_full_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double2) * kMaxN * kPitch)));
-    QCH_CUDA(cudaFuncSetAttribute(npad_full_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double2) * kMaxN * kPitch)));
-    attr = true;
-  }
+  QCH_CUDA(smem_attr((const void*)npad_full_warp_kernel<false>, (int)(sizeof(double2) * kMaxN * kPitch)));
+  QCH_CUDA(smem_attr((const void*)npad_full_warp_kernel<true>, (int)(sizeof(double2) * kMaxN * kPitch)));
   void* pr = prof_begin("npad_run_kernel", st);
   if (cm.ek)
     npad_full_warp_kernel<true><<<njobs, 32, smem, st>>>(jobs, cm);

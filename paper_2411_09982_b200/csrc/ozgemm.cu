@@ -27,6 +27,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "zgemm.h"
@@ -716,11 +719,7 @@ template <int BN, bool PAIR>
 static int oz_launch_w(const CUtensorMap& ma, const CUtensorMap& mb, const OzArgs& g, int64_t batch,
                        cudaStream_t st) {
   using W = OzW<BN, PAIR>;
-  static bool attr = false;
-  if (!attr) {
-    QCH_CUDA(cudaFuncSetAttribute(oz_gemmw_kernel<BN, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, W::SMEM));
-    attr = true;
-  }
+  QCH_CUDA(smem_attr((const void*)oz_gemmw_kernel<BN, PAIR>, W::SMEM));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((PAIR ? 2 : 1) * g.ntiles, (unsigned)batch);
   cfg.blockDim = dim3(OZ_THREADS);
@@ -776,11 +775,7 @@ int oz_gemm(const int8_t* xs, const int* ea, const int8_t* ys, const int* eb, in
     case 3: rc = oz_launch_w<256, true>(ma, mb, g, batch, st); break;
     default: {
       const int smem = OZ_ST * OZ_STAGE + 1024 + 256;
-      static bool attr = false;
-      if (!attr) {
-        QCH_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-      }
+      QCH_CUDA(smem_attr((const void*)oz_gemm_kernel, smem));
       oz_gemm_kernel<<<dim3(g.ntiles, (unsigned)batch), OZ_THREADS, smem, st>>>(ma, mb, g);
     }
   }
@@ -872,10 +867,20 @@ __global__ void __launch_bounds__(256) oz_combine_kernel(OzCombine a) {
 // tiles meeting the lower triangle (R rows x C columns as oz_cfg), in super-tiles of 1024 x 1024 so the ~148 concurrent CTAs share
 // A and B slice panels (an L2-resident working set)
 static int oz_lower_tiles(int n, const int** out, int* count, cudaStream_t st) {
-  static int cached_n = -1, cached_r = -1, cached_c = -1, cached_cnt = 0;
-  static int* d_list = nullptr;
+  struct Key {
+    int dev, n, r, c;
+    bool operator<(const Key& o) const {
+      return std::tie(dev, n, r, c) < std::tie(o.dev, o.n, o.r, o.c);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, std::pair<int*, int>> lists;  // device tile lists, kept for the process
   const int R = oz_tile_rows(), C = oz_tile_cols();
-  if (cached_n != n || cached_r != R || cached_c != C) {
+  int dev = 0;
+  QCH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = lists.find(Key{dev, n, R, C});
+  if (it == lists.end()) {
     const int TI = (n + R - 1) / R, TJ = (n + C - 1) / C;
     const int GI = 1024 / R, GJ = 1024 / C;
     std::vector<int> h;
@@ -884,18 +889,14 @@ static int oz_lower_tiles(int n, const int** out, int* count, cudaStream_t st) {
         for (int i = bi; i < std::min(TI, bi + GI); ++i)
           for (int j = bj; j < std::min(TJ, bj + GJ); ++j)
             if (j * C <= i * R + R - 1) h.push_back((i << 16) | j);
-    if (d_list) cudaFree(d_list);
-    d_list = nullptr;
-    QCH_CUDA(cudaMalloc((void**)&d_list, sizeof(int) * h.size()));
-    QCH_CUDA(cudaMemcpyAsync(d_list, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, st));
+    int* d = nullptr;
+    QCH_CUDA(cudaMalloc((void**)&d, sizeof(int) * h.size()));
+    QCH_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, st));
     QCH_CUDA(cudaStreamSynchronize(st));
-    cached_n = n;
-    cached_r = R;
-    cached_c = C;
-    cached_cnt = (int)h.size();
+    it = lists.emplace(Key{dev, n, R, C}, std::make_pair(d, (int)h.size())).first;
   }
-  *out = d_list;
-  *count = cached_cnt;
+  *out = it->second.first;
+  *count = it->second.second;
   return QCH_OK;
 }
 

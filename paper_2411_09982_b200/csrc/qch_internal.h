@@ -36,5 +36,8 @@ void prof_end(void* h, cudaStream_t st);
 int sm_count();
 void ensure_pool();
 int max_smem_optin();
+// raise a kernel's dynamic shared-memory limit on the CURRENT device (the
+// attribute is per device; thread-safe, each (kernel, device) set once)
+cudaError_t smem_attr(const void* func, int bytes);
 
 }  // namespace qch

@@ -210,11 +210,7 @@ static size_t zgemm_smem(bool bh) {
 template <int MODE, bool BH>
 static int zgemm_launch(const ZgemmArgs& g, int64_t batch, cudaStream_t st) {
   size_t smem = zgemm_smem(BH);
-  static bool attr = false;
-  if (!attr) {
-    QCH_CUDA(cudaFuncSetAttribute(zgemm_kernel<MODE, BH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  QCH_CUDA(smem_attr((const void*)zgemm_kernel<MODE, BH>, (int)smem));
   int64_t done = 0;
   while (done < batch) {  // gridDim.z <= 65535
     int64_t nb = std::min<int64_t>(batch - done, 65535);

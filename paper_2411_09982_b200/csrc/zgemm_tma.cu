@@ -344,12 +344,7 @@ double dmma_flops_total() { return g_dmma_flops.load(); }
 template <int MODE, bool HERM, bool BH, bool M3>
 static int zt_launch(const CUtensorMap& ma, const CUtensorMap& mb, ZtArgs g, int64_t batch, cudaStream_t st) {
   const int smem = ZT_ST * ZT_STAGE + 2 * ZT_ST * 8 + 1024;
-  static bool attr = false;
-  if (!attr) {
-    QCH_CUDA(cudaFuncSetAttribute(zgemm_tma_kernel<MODE, HERM, BH, M3>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  QCH_CUDA(smem_attr((const void*)zgemm_tma_kernel<MODE, HERM, BH, M3>, smem));
   g.tm = (g.m + ZT_BM - 1) / ZT_BM;
   g.tn = (g.n + ZT_BN - 1) / ZT_BN;
   if (HERM) {
