@@ -320,7 +320,11 @@ int zgemm_defect(const double2* u, double* acc, int n, int64_t batch, cudaStream
 // otherwise or with QCH_HERM_GEMM=dmma
 static thread_local int t_herm_force_dmma = 0;
 void herm_force_dmma(bool on) { t_herm_force_dmma = on ? 1 : 0; }
-bool herm_use_ozaki(int n) { return herm_engine() != 0 && !t_herm_force_dmma && n >= 512 && n <= 16384; }
+static int oz_min_n() {
+  static const int v = getenv("QCH_OZ_MIN_N") ? std::max(16, atoi(getenv("QCH_OZ_MIN_N"))) : 512;
+  return v;
+}
+bool herm_use_ozaki(int n) { return herm_engine() != 0 && !t_herm_force_dmma && n >= oz_min_n() && n <= 16384; }
 static bool use_ozaki(int n) { return herm_use_ozaki(n); }
 
 int zgemm_herm(const double2* a, const double2* b, double2* c, int n, int64_t batch, cudaStream_t st, OzCache* oc,
