@@ -4,23 +4,31 @@
 //
 // Slicing.  Row r of a real operand X is scaled by 2^-e_r (e_r: the frexp
 // exponent of the row's max |x|, so |x 2^-e_r| < 1) and cut into s int8
-// slices, 7 bits each: t = 128 x; a = trunc(t) (|a| <= 127); x = t - a — all
-// exact in FP64.  X[r,k] = 2^e_r sum_i a_i[r,k] 2^-7(i+1) + O(2^(e_r - 7s)).
+// slices of 7 bits — the base-128 digits of |x 2^-e_r| with the sign of x:
+// X[r,k] = 2^e_r sum_i a_i[r,k] 2^-7(i+1) + O(2^(e_r - 7s)).
 // Product.  (X Y^T)[r,c] = 2^(e_r + f_c) sum_{i,j} 2^-7(i+j+2) (a_i b_j^T)[r,c];
-// the int8 products are EXACT in int32 (K 127^2 (i+j+1) < 2^31 for K <= 4096,
+// the int8 products are EXACT in int32 (K 127^2 (i+j+1) < 2^31 for K <= 16384,
 // s <= 8) and the pairs with i + j <= s - 1 are kept (s(s+1)/2 int8 GEMMs):
-// the dropped tail and the slicing residual are below 2^-7s relative to
-// 2^(e_r + f_c) K — s = 7 gives ~1e-15 of the row/column scale, the FP64
-// rounding level of a K = 4096 dot product.  One kernel per real product:
-// for each diagonal D = i + j the pairs accumulate in one TMEM buffer (int32),
-// the epilogue warps fold it into FP64 registers as 2^-7(D+2) D_int, the two
-// TMEM buffers alternating so the MMAs of diagonal D+1 overlap the epilogue of
-// diagonal D.
+// the dropped tail and the slicing residual are below ~2^-7s of
+// 2^(e_r + f_c) K — s = 8 is the FP64 rounding level of the dot product.
+// A product may use only the leading s' < s slices of a stored cut (the
+// digits of a shorter cut are the leading digits of a longer one).
 //
+// GEMM kernels (one launch per real product; for each diagonal D = i + j the
+// pairs accumulate in one of two TMEM buffers while the epilogue warps fold
+// the other into FP64):
+//  * oz_gemmw_kernel<256, true> (default): a CTA pair (cta_group::2) owns a
+//    256 x 256 tile; each CTA stages 128 A rows + 128 B rows per 128-byte K
+//    block (TMA, 128-byte swizzle, 6 stages), the even CTA issues the M = 256
+//    MMAs, the diagonals are folded into the output in global memory (store,
+//    then FP64 reductions at L2 with the exponents applied per contribution);
+//  * oz_gemmw_kernel<256, false> / <128, true>: one CTA 128 x 256, pair
+//    256 x 128 (QCH_OZ_CFG=w256 / p128);
+//  * oz_gemm_kernel: one CTA, 128 x 128, FP64 accumulators in registers
+//    (QCH_OZ_CFG=r128; the first version, the baseline of the others).
 // Warp roles (320 threads): warp 0 TMA producer (one lane), warp 1 TMEM
 // allocator + MMA issuer (one lane), warps 2-9 epilogue (warp w: TMEM lane
-// quarter w % 4, columns 64 ((w-2) / 4) ..).  Tile 128 x 128, K stage 128 B
-// (one 128-byte swizzle row), 4 UMMA k-steps (K = 32) per stage, 6 stages.
+// quarter w % 4, column half (w - 2) / 4).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
