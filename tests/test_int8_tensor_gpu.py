@@ -127,7 +127,7 @@ def test_nonfinite_operator_takes_dmma_and_propagates_nan(L):
     assert np.isnan(np.asarray(traj.amplitudes)[1:]).any()
 
 
-@pytest.mark.parametrize("scale", [0.05, 0.45, 3.0])
+@pytest.mark.parametrize("scale", [1e-6, 1e-3, 0.05, 0.45, 3.0])
 def test_adaptive_slice_plan_matches_full_slices(L, scale, monkeypatch):
     """The adaptive plan (fewer slices for the products that reach U through
     small coefficients / high powers) against every product on 8 slices and
@@ -145,3 +145,30 @@ def test_adaptive_slice_plan_matches_full_slices(L, scale, monkeypatch):
     adapt = E.expm_unitary(h).entries
     assert rel_fro(adapt, full) <= 1e-15
     assert rel_fro(adapt, expm_oracle.expm_minus_i(h)) <= 1e-12
+
+
+def test_int8_expm_rows_of_disparate_scale(L):
+    """Per-row exponents: a Hermitian operator whose rows span 12 orders of
+    magnitude (a diagonal similarity of a random Hermitian keeps it
+    Hermitian only for real scalings, so use a block-diagonal mix) — the
+    int8 engine against the DMMA engine and the oracle."""
+    import paper_2411_09982_b200 as E
+
+    n = 576
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = (a + a.conj().T) / np.sqrt(n)
+    d = np.logspace(-12, 0, n)
+    h = h * np.sqrt(np.outer(d, d))  # Hermitian, row/column scales from 1e-12 to 1
+    h *= 0.4 / np.abs(h).sum(axis=1).max()
+    old = L.load().qch_set_herm_gemm(-1)
+    try:
+        L.load().qch_set_herm_gemm(1)
+        u8 = E.expm_unitary(h).entries
+        L.load().qch_set_herm_gemm(0)
+        ud = E.expm_unitary(h).entries
+    finally:
+        L.load().qch_set_herm_gemm(old)
+    ref = expm_oracle.expm_minus_i(h)
+    assert rel_fro(u8, ref) <= 1e-13
+    assert rel_fro(u8, ud) <= 1e-13
