@@ -244,22 +244,62 @@ __global__ void indptr_kernel(SpArgs g) {
   g.out_indptr[x] = g.indptr[x] + shift;
 }
 
-// entries of unchanged rows to their shifted slots (coalesced both ways)
+// entries of unchanged rows to their shifted slots (coalesced both ways).
+// A warp moves chunks of 32 x kCopyU consecutive entries; the few changed
+// rows split the CSR into segments of constant shift, so a chunk that does
+// not touch a changed row (nearly all of them) is moved with one shift and
+// kCopyU independent loads in flight per lane; a chunk that does falls back
+// to the per-entry lookup.
+constexpr int kCopyU = 8;
+__device__ __forceinline__ int64_t seg_of(const SpArgs& g, int64_t m, int64_t e) {
+  int64_t lo = 0, hi = m;  // changed rows whose old range ends at or before e
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (g.chg_end[mid] <= e) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
 __global__ void copy_kernel(SpArgs g) {
   const int64_t m = g.po->nchanged;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.nnz; e += (int64_t)gridDim.x * blockDim.x) {
-    // changed rows whose old range ends at or before e shift it; e inside a
-    // changed row is rewritten by rows_kernel
-    int64_t lo = 0, hi = m;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (g.chg_end[mid] <= e) lo = mid + 1;
-      else hi = mid;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  constexpr int64_t kChunk = 32 * kCopyU;
+  for (int64_t base = w * kChunk; base < g.nnz; base += nw * kChunk) {
+    const int64_t end = base + kChunk < g.nnz ? base + kChunk : g.nnz;
+    const int64_t lo = seg_of(g, m, base);
+    // the next changed row's old start: the chunk is uniform if it ends before it
+    const bool uniform = lo == m || g.indptr[g.chg_row[lo]] >= end;
+    if (uniform) {
+      const int64_t shift = (lo == 0) ? 0 : g.chg_pref[lo - 1] + g.chg_delta[lo - 1];
+      int32_t ci[kCopyU];
+      double2 cv[kCopyU];
+#pragma unroll
+      for (int k = 0; k < kCopyU; ++k) {
+        const int64_t e = base + k * 32 + lane;
+        if (e < end) {
+          ci[k] = g.indices[e];
+          cv[k] = g.data[e];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kCopyU; ++k) {
+        const int64_t e = base + k * 32 + lane;
+        if (e < end) {
+          g.out_indices[e + shift] = ci[k];
+          g.out_data[e + shift] = cv[k];
+        }
+      }
+    } else {
+      for (int64_t e = base + lane; e < end; e += 32) {
+        const int64_t l2 = seg_of(g, m, e);
+        if (l2 < m && g.indptr[g.chg_row[l2]] <= e) continue;  // inside changed row chg_row[l2]: rows_kernel
+        const int64_t shift = (l2 == 0) ? 0 : g.chg_pref[l2 - 1] + g.chg_delta[l2 - 1];
+        g.out_indices[e + shift] = g.indices[e];
+        g.out_data[e + shift] = g.data[e];
+      }
     }
-    if (lo < m && g.indptr[g.chg_row[lo]] <= e) continue;  // inside changed row chg_row[lo]
-    const int64_t shift = (lo == 0) ? 0 : g.chg_pref[lo - 1] + g.chg_delta[lo - 1];
-    g.out_indices[e + shift] = g.indices[e];
-    g.out_data[e + shift] = g.data[e];
   }
 }
 
