@@ -140,19 +140,6 @@ class ShardedEvolvePlan:
         self.psi_start = t.empty(self.n, dtype=t.complex128, device="cuda")
         self.traj = t.empty((self.m_local + 1, self.n), dtype=t.complex128, device="cuda")
         self.flags = t.empty(2, dtype=t.int64, device="cuda")
-        # the two device halves of a step (pass 1; apply-prefix + pass 2) as
-        # CUDA graphs around the eager NCCL all-gather: one graph launch each
-        # instead of 2 memsets + 3 kernels + a copy from Python
-        self._prepare()
-        self._finish()
-        t.cuda.synchronize()
-        self.graph_a, self.graph_b = t.cuda.CUDAGraph(), t.cuda.CUDAGraph()
-        with t.cuda.graph(self.graph_a):
-            self._prepare()
-            if self.world == 1:
-                self.blocks[0].copy_(self.block)
-        with t.cuda.graph(self.graph_b):
-            self._finish()
 
     def _prepare(self):
         lib, sp = _lib.load(), _lib.stream_ptr()
@@ -172,10 +159,12 @@ class ShardedEvolvePlan:
     def run(self):
         import torch.distributed as dist
 
-        self.graph_a.replay()
+        self._prepare()
         if self.world > 1:
             dist.all_gather_into_tensor(self.blocks.view(-1), self.block.view(-1), group=self.group)
-        self.graph_b.replay()
+        else:
+            self.blocks[0].copy_(self.block)
+        self._finish()
         return self.traj
 
     def check(self) -> None:
