@@ -81,6 +81,40 @@ __global__ void nonfinite_kernel(const double2* __restrict__ h, int64_t per, int
   }
 }
 
+// Hbar for intervals [m0, m0+mb) (magnus.py:185-189 + second order), K a
+// compile-time constant: the operator entries stay in registers (a runtime-K
+// array of them lands in local memory: 2.5x slower at config 5)
+template <int K>
+__global__ void assemble_k_kernel(const double2* __restrict__ h0, const double2* __restrict__ hk,
+                                  const double2* __restrict__ comm, int64_t nn, const double* __restrict__ c1,
+                                  const double* __restrict__ c2, int64_t m0, int64_t mb, double dt_int, int order,
+                                  double2* __restrict__ out) {
+  constexpr int NC = K + K * (K - 1) / 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
+    const cplx d = d2c(h0[e]);
+    cplx ops[K], cm[NC];
+#pragma unroll
+    for (int k = 0; k < K; ++k) ops[k] = d2c(hk[k * nn + e]);
+    if (order >= 2) {
+#pragma unroll
+      for (int q = 0; q < NC; ++q) cm[q] = d2c(comm[q * nn + e]);
+    }
+    for (int64_t m = 0; m < mb; ++m) {
+      const int64_t gm = m0 + m;
+      cplx v = np_rmul(dt_int, d);
+#pragma unroll
+      for (int k = 0; k < K; ++k) v = cadd(v, np_rmul(c1[gm * K + k], ops[k]));
+      if (order >= 2) {
+        cplx x = mkc(0, 0);
+#pragma unroll
+        for (int q = 0; q < NC; ++q) x = cadd(x, np_rmul(c2[gm * NC + q], cm[q]));
+        v = cadd(v, np_cmul(mkc(0.0, -0.5), x));
+      }
+      out[m * nn + e] = c2d(v);
+    }
+  }
+}
+
 // Hbar for intervals [m0, m0+mb) (magnus.py:185-189 + second order)
 __global__ void assemble_kernel(const double2* __restrict__ h0, const double2* __restrict__ hk,
                                 const double2* __restrict__ comm, int K, int64_t nn, const double* __restrict__ c1,
@@ -886,9 +920,17 @@ extern "C" int qch_magnus_assemble_c128(const void* d_h0, const void* d_hk, cons
                                         const double* d_c1, const double* d_c2, int64_t m0, int64_t mb, double dt_int,
                                         int order, void* d_hbar, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  assemble_kernel<<<grid_for(N * N), 256, 0, st>>>((const double2*)d_h0, (const double2*)d_hk,
-                                                    (const double2*)d_comm, (int)K, N * N, d_c1, d_c2, m0, mb, dt_int,
-                                                    order, (double2*)d_hbar);
+  const double2 *h0 = (const double2*)d_h0, *hk = (const double2*)d_hk, *cm = (const double2*)d_comm;
+  double2* out = (double2*)d_hbar;
+  const unsigned gb = (unsigned)grid_for(N * N);
+  switch (K) {  // operator entries in registers for the common control counts
+    case 1: assemble_k_kernel<1><<<gb, 256, 0, st>>>(h0, hk, cm, N * N, d_c1, d_c2, m0, mb, dt_int, order, out); break;
+    case 2: assemble_k_kernel<2><<<gb, 256, 0, st>>>(h0, hk, cm, N * N, d_c1, d_c2, m0, mb, dt_int, order, out); break;
+    case 3: assemble_k_kernel<3><<<gb, 256, 0, st>>>(h0, hk, cm, N * N, d_c1, d_c2, m0, mb, dt_int, order, out); break;
+    case 4: assemble_k_kernel<4><<<gb, 256, 0, st>>>(h0, hk, cm, N * N, d_c1, d_c2, m0, mb, dt_int, order, out); break;
+    default:
+      assemble_kernel<<<gb, 256, 0, st>>>(h0, hk, cm, (int)K, N * N, d_c1, d_c2, m0, mb, dt_int, order, out);
+  }
   QCH_LAUNCH_CHECK("assemble_kernel");
   note_launch(1);
   return QCH_OK;
