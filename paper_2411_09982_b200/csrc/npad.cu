@@ -238,8 +238,11 @@ __global__ void set_mask_kernel(unsigned char* mask, const int* tlist, int nt) {
 __global__ void __launch_bounds__(256) build_tr_kernel(double2* __restrict__ h, int nq, int nr,
                                                        const double* __restrict__ prm,
                                                        unsigned long long* __restrict__ maxabs) {
-  // block (x, item): rows r = x, x + gridDim.x, ...; threads stride the
-  // columns (coalesced rows, 32-bit index math, no 64-bit divisions)
+  // block (x, item): rows r = x, x + gridDim.x, ...  A row holds at most 5
+  // nonzeros (the diagonal and the couplings (q1 +- 1, k1 +- 1)): the block
+  // streams the row's zeros with 16-byte stores (no index math), then one
+  // thread per nonzero writes it — same values and order of operations as
+  // the host builder, written once.
   const int n = nq * nr;
   const int64_t b = blockIdx.y;
   const double wq = prm[4 * b], al = prm[4 * b + 1], wr = prm[4 * b + 2], g = prm[4 * b + 3];
@@ -248,26 +251,27 @@ __global__ void __launch_bounds__(256) build_tr_kernel(double2* __restrict__ h, 
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
     const int q1 = r / nr, k1 = r - q1 * nr;
     double2* row = hb + (int64_t)r * n;
-    for (int c = threadIdx.x; c < n; c += blockDim.x) {
-      const int q2 = c / nr, k2 = c - q2 * nr;
-      double v = 0.0;
-      if (r == c) {
-        // host builder (models.transmon_resonator_hamiltonian): n = b^dag b has
-        // diagonal sqrt(q)^2 (not exactly q), a^dag a likewise; same op order.
-        const double sq = sqrt((double)q1), sk = sqrt((double)k1);
-        const double nn = QMUL(sq, sq), kk = QMUL(sk, sk);
-        const double hq = QADD(QMUL(wq, nn), QMUL(QMUL(0.5, al), QMUL(nn, QSUB(nn, 1.0))));
-        v = QADD(hq, QMUL(wr, kk));
-      } else {
-        const int dq = q1 - q2, dk = k1 - k2;
-        if ((dq == 1 || dq == -1) && (dk == 1 || dk == -1)) {
-          const double bq = sqrt((double)(q1 > q2 ? q1 : q2));
-          const double ak = sqrt((double)(k1 > k2 ? k1 : k2));
-          v = QMUL(g, QMUL(bq, ak));
-        }
-      }
-      row[c] = make_double2(v, 0.0);
+    for (int c = threadIdx.x; c < n; c += blockDim.x) row[c] = make_double2(0.0, 0.0);
+    __syncthreads();  // zeros before the nonzeros (different threads)
+    const int t = threadIdx.x;
+    if (t == 0) {
+      // host builder (models.transmon_resonator_hamiltonian): n = b^dag b has
+      // diagonal sqrt(q)^2 (not exactly q), a^dag a likewise; same op order.
+      const double sq = sqrt((double)q1), sk = sqrt((double)k1);
+      const double nn = QMUL(sq, sq), kk = QMUL(sk, sk);
+      const double hq = QADD(QMUL(wq, nn), QMUL(QMUL(0.5, al), QMUL(nn, QSUB(nn, 1.0))));
+      const double v = QADD(hq, QMUL(wr, kk));
+      row[r] = make_double2(v, 0.0);
       m = fmax(m, fabs(v));  // numpy |v + 0j| = |v|
+    } else if (t <= 4) {
+      const int q2 = q1 + ((t & 1) ? 1 : -1), k2 = k1 + ((t & 2) ? 1 : -1);
+      if (q2 >= 0 && q2 < nq && k2 >= 0 && k2 < nr) {
+        const double bq = sqrt((double)(q1 > q2 ? q1 : q2));
+        const double ak = sqrt((double)(k1 > k2 ? k1 : k2));
+        const double v = QMUL(g, QMUL(bq, ak));
+        row[q2 * nr + k2] = make_double2(v, 0.0);
+        m = fmax(m, fabs(v));
+      }
     }
   }
   if (maxabs != nullptr) {
