@@ -171,14 +171,23 @@ __global__ void pair_kernel(SpArgs g) {
   *g.counter = 2;
 }
 
-// rows x != i, j: entries in columns i / j now and after the rotation
-__global__ void classify_kernel(SpArgs g) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= g.n || x == g.i || x == g.j) return;
-  const int64_t r0 = g.indptr[x], r1 = g.indptr[x + 1];
-  const int old_cnt = (find_col(g.indices + r0, r1 - r0, g.i) >= 0) + (find_col(g.indices + r0, r1 - r0, g.j) >= 0);
-  const int64_t la = g.po->la, lb = g.po->lb;
-  const int new_cnt = (find_col(g.a_col, la, (int32_t)x) >= 0) + (find_col(g.b_col, lb, (int32_t)x) >= 0);
+// rows x != i, j: entries in columns i / j now and after the rotation.
+// kClassU rows per thread with their loads issued together (each row costs
+// two dependent loads: indptr, then its first / last column); a row is
+// searched only when its column range can hold i or j, or x can be a column
+// of the new rows i, j.
+constexpr int kClassU = 4;
+__device__ __forceinline__ void classify_row(const SpArgs& g, int64_t x, int64_t r0, int64_t r1, int32_t cfirst,
+                                             int32_t clast, int32_t lo_ij, int32_t hi_ij, int32_t amin, int32_t amax) {
+  if (x == g.i || x == g.j) return;
+  int old_cnt = 0;
+  if (r1 > r0 && cfirst <= hi_ij && clast >= lo_ij)
+    old_cnt = (find_col(g.indices + r0, r1 - r0, g.i) >= 0) + (find_col(g.indices + r0, r1 - r0, g.j) >= 0);
+  int new_cnt = 0;
+  if (x >= amin && x <= amax) {
+    const int64_t la = g.po->la, lb = g.po->lb;
+    new_cnt = (find_col(g.a_col, la, (int32_t)x) >= 0) + (find_col(g.b_col, lb, (int32_t)x) >= 0);
+  }
   if (old_cnt == 0 && new_cnt == 0) return;
   const unsigned long long k = atomicAdd(g.counter, 1ull);
   if (k >= (unsigned long long)kMaxChanged) {
@@ -187,6 +196,41 @@ __global__ void classify_kernel(SpArgs g) {
   }
   g.chg_row[k] = (int32_t)x;
   g.chg_delta[k] = new_cnt - old_cnt;
+}
+__global__ void classify_kernel(SpArgs g) {
+  const int32_t lo_ij = min(g.i, g.j), hi_ij = max(g.i, g.j);
+  // column range of the new rows i, j (sorted lists)
+  const int64_t la = g.po->la, lb = g.po->lb;
+  int32_t amin = 0x7fffffff, amax = -1;
+  if (la > 0) {
+    amin = min(amin, g.a_col[0]);
+    amax = max(amax, g.a_col[la - 1]);
+  }
+  if (lb > 0) {
+    amin = min(amin, g.b_col[0]);
+    amax = max(amax, g.b_col[lb - 1]);
+  }
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; base < g.n; base += nth * kClassU) {
+    int64_t r0[kClassU], r1[kClassU];
+    int32_t cf[kClassU], cl[kClassU];
+#pragma unroll
+    for (int u = 0; u < kClassU; ++u) {
+      const int64_t x = base + u * nth;
+      r0[u] = x < g.n ? g.indptr[x] : 0;
+      r1[u] = x < g.n ? g.indptr[x + 1] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kClassU; ++u) {
+      cf[u] = r1[u] > r0[u] ? g.indices[r0[u]] : 0;
+      cl[u] = r1[u] > r0[u] ? g.indices[r1[u] - 1] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kClassU; ++u) {
+      const int64_t x = base + u * nth;
+      if (x < g.n) classify_row(g, x, r0[u], r1[u], cf[u], cl[u], lo_ij, hi_ij, amin, amax);
+    }
+  }
 }
 
 // sort the changed rows, prefix sums of the nnz changes, total
@@ -426,7 +470,9 @@ extern "C" int qch_npad_sparse_rotate_c128(const int64_t* d_indptr, const int32_
   QCH_CUDA(cudaMemsetAsync(g.po, 0, sizeof(PairOut), st));
   void* pr = prof_begin("npad_sparse_rotate", st);
   pair_kernel<<<1, 32, 0, st>>>(g);
-  classify_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(g);
+  classify_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 256 * kClassU - 1) / (256 * kClassU),
+                                                                        (int64_t)sm_count() * 32)),
+                    256, 0, st>>>(g);
   sort_changed_kernel<<<1, 256, 0, st>>>(g);
   QCH_LAUNCH_CHECK("sparse rotate (pair/classify/sort)");
   PairOut po;
