@@ -20,6 +20,8 @@
 #include <cstdio>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "qch_internal.h"
@@ -468,6 +470,171 @@ __global__ void __launch_bounds__(256) chain_cta64_kernel(const double2* __restr
       if (!(fabs(sqrt(t) - 1.0) <= 1e-6)) atomicMin(bad_norm, (unsigned long long)(m0 + m));
     }
   }
+}
+
+// The ordered product for 64 < N <= 32 CPL in ONE thread-block cluster of
+// kCcCtas CTAs, with no grid barrier: CTA g owns rows [8 RPW g, 8 RPW g +
+// 8 RPW), warp w rows 8 RPW g + RPW w + q.  Each CTA keeps the state in two
+// shared-memory buffers; a row's new amplitude is pushed into EVERY CTA's
+// next buffer by st.async (DSMEM), whose completion counts bytes on the
+// receiver's mbarrier, so a CTA starts step m + 1 the moment the N
+// amplitudes of step m have landed (no fence, no cluster barrier per step).
+// The propagator rows a warp needs for step m + 1 are loaded into registers
+// right after its step-m amplitudes leave (prefetched into L2 `pfd` steps
+// ahead).  The per-warp norm partials ride to CTA 0 on three rotating norm
+// mbarriers of their own (off the state's critical path), and CTA 0 checks
+// step m - 1 during step m.  Buffer reuse is safe by causality: a CTA only
+// receives the step m + 1 amplitudes once every warp of the cluster (itself
+// included) has consumed its step m inputs.  Summation order per row equals
+// chain_grid_kernel's (lane-strided FMAs, then the xor-shuffle tree).
+constexpr int kCcCtas = 16;  // 8 CTAs measured slower (1.15 vs 0.94 us per step at N = 128)
+template <int RPW, int CPL>
+__global__ void __launch_bounds__(256, 1) chain_cluster_kernel(const double2* __restrict__ u, int n, int64_t mb,
+                                                               const double2* __restrict__ psi_in,
+                                                               double2* __restrict__ traj_rows, int64_t m0,
+                                                               unsigned long long* bad_norm, int pfd) {
+  __shared__ __align__(16) double2 s_x[2][32 * CPL];
+  __shared__ double s_nrm[3][kCcCtas * 8];
+  __shared__ __align__(8) unsigned long long s_bar[2];
+  __shared__ __align__(8) unsigned long long s_nbar[3];  // CTA 0: norm partials of a step
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned g;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(g));
+  const int rw = (int)g * 8 * RPW + warp * RPW;  // this warp's first row
+  const int64_t nn = (int64_t)n * n;
+  const unsigned kNormBytes = kCcCtas * 8 * sizeof(double);
+  for (int c = threadIdx.x; c < n; c += 256) s_x[0][c] = psi_in[c];
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[k])) : "memory");
+    for (int k = 0; k < 3; ++k) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_nbar[k])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const int64_t wrow_bytes = (int64_t)max(0, min(RPW, n - rw)) * n * sizeof(double2);
+  auto pf_l2 = [&](const double2* um) {  // this warp's rows of one propagator into L2
+    const char* p = (const char*)(um + (int64_t)rw * n);
+    for (int64_t off = (int64_t)lane * 128; off < wrow_bytes; off += 32 * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(p + off));
+  };
+  double2 ua[RPW][CPL];
+  auto load = [&](const double2* um) {
+#pragma unroll
+    for (int q = 0; q < RPW; ++q)
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        const int c = lane + 32 * j;
+        ua[q][j] = (rw + q < n && c < n) ? __ldcs(um + (int64_t)(rw + q) * n + c) : make_double2(0.0, 0.0);
+      }
+  };
+  load(u);
+  for (int k = 1; k < pfd && k < mb; ++k) pf_l2(u + k * nn);
+  // every CTA's barriers initialised before any peer signals them
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  const unsigned bar0 = smem_u32(&s_bar[0]), bar1 = smem_u32(&s_bar[1]);
+  auto wait_par = [](unsigned bar, unsigned par) {
+    asm volatile(
+        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(bar),
+        "r"(par)
+        : "memory");
+  };
+  // CTA 0, warp 0: the norm of step m (slot k = m % 3, use m / 3 of that slot)
+  auto check = [&](int64_t m, int k) {
+    wait_par(smem_u32(&s_nbar[k]), (unsigned)((m / 3) & 1));
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < kCcCtas * 8 / 32; ++i) t += s_nrm[k][lane + 32 * i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane == 0 && !(fabs(sqrt(t) - 1.0) <= 1e-6)) atomicMin(bad_norm, (unsigned long long)(m0 + m));
+  };
+  const double2* um_next = u + nn;
+  const double2* um_pf = u + pfd * nn;
+  double2* trow = traj_rows;
+  int k3 = 0;  // m % 3
+  for (int64_t m = 0; m < mb; ++m) {
+    if (m > 0) wait_par((m & 1) ? bar1 : bar0, (unsigned)(((m - 1) >> 1) & 1));  // the step-m state is here
+    const unsigned nb = (unsigned)((m + 1) & 1), bar_nb = nb ? bar1 : bar0;
+    if (threadIdx.x == 0) {
+      if (m + 1 < mb)  // arm the phase that delivers step m + 1
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar_nb),
+                     "r"((unsigned)n * (unsigned)sizeof(double2))
+                     : "memory");
+      if (g == 0)  // and, on CTA 0, the norm partials of step m
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(&s_nbar[k3])),
+                     "r"(kNormBytes)
+                     : "memory");
+    }
+    const double2* x = s_x[m & 1];
+    double ar[RPW], ai[RPW];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) ar[q] = ai[q] = 0.0;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int c = lane + 32 * j;
+      if (c < n) {
+        const double2 b = x[c];
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+          const double2 a = ua[q][j];
+          ar[q] = fma(a.x, b.x, ar[q]);
+          ar[q] = fma(-a.y, b.y, ar[q]);
+          ai[q] = fma(a.x, b.y, ai[q]);
+          ai[q] = fma(a.y, b.x, ai[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) {
+        ar[q] += __shfl_xor_sync(0xffffffffu, ar[q], off);
+        ai[q] += __shfl_xor_sync(0xffffffffu, ai[q], off);
+      }
+    if (m + 1 < mb && lane < kCcCtas) {  // lane l -> CTA l's next state buffer
+      unsigned rb;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar_nb), "r"(lane));
+#pragma unroll
+      for (int q = 0; q < RPW; ++q)
+        if (rw + q < n) {
+          unsigned ra;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(&s_x[nb][rw + q])), "r"(lane));
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+                       "d"(ar[q]), "d"(ai[q]), "r"(rb)
+                       : "memory");
+        }
+    }
+    if (lane == 31) {  // this warp's norm partial -> CTA 0
+      double part = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPW; ++q)
+        if (rw + q < n) part += ar[q] * ar[q] + ai[q] * ai[q];
+      unsigned ra, rb;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(smem_u32(&s_nrm[k3][g * 8 + warp])));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(smem_u32(&s_nbar[k3])));
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(part),
+                   "r"(rb)
+                   : "memory");
+    }
+    if (lane >= 16 && lane < 16 + RPW) {
+      const int q = lane - 16;
+      double yr = ar[0], yi = ai[0];
+#pragma unroll
+      for (int k = 1; k < RPW; ++k)
+        if (q == k) yr = ar[k], yi = ai[k];
+      if (rw + q < n) __stcg(trow + rw + q, make_double2(yr, yi));
+    }
+    trow += n;
+    if (m + 1 < mb) {
+      load(um_next);
+      um_next += nn;
+      if (m + pfd < mb) pf_l2(um_pf);
+      um_pf += nn;
+    }
+    if (g == 0 && warp == 0 && m > 0) check(m - 1, k3 == 0 ? 2 : k3 - 1);
+    k3 = k3 == 2 ? 0 : k3 + 1;
+  }
+  if (g == 0 && warp == 0) check(mb - 1, k3 == 0 ? 2 : k3 - 1);
+  // no CTA leaves while a peer may still signal it
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // tr(U U^dag) = sum |U_ij|^2, one CTA per matrix (for |det U|, see below)
@@ -1022,6 +1189,55 @@ static int small_report(unsigned long long* d_bad, int check, int64_t* bad_index
   return QCH_OK;
 }
 
+// Largest N the one-cluster ordered product takes (QCH_CHAIN_CLUSTER_MAX,
+// at most 384, 0 disables it); above, the cooperative grid kernel (at
+// N = 512 the cluster's 16 SMs cannot pull the propagator fast enough:
+// 6.2 vs 5.1 us per step).
+static int64_t chain_cluster_max() {
+  static const int64_t v = [] {
+    const char* e = getenv("QCH_CHAIN_CLUSTER_MAX");
+    return e ? std::min<int64_t>(384, atoll(e)) : (int64_t)384;
+  }();
+  return v;
+}
+
+using chain_cluster_fn = void (*)(const double2*, int, int64_t, const double2*, double2*, int64_t,
+                                  unsigned long long*, int);
+static chain_cluster_fn chain_cluster_for(int64_t N) {
+  return N <= 128 ? chain_cluster_kernel<1, 4>
+       : N <= 256 ? chain_cluster_kernel<2, 8>
+                  : chain_cluster_kernel<3, 12>;
+}
+
+// A G-CTA (non-portable above 8) cluster of chain_cluster_kernel is
+// schedulable on this device; the attribute is set once per (kernel, device).
+static bool cluster_ok(const void* kern, int G) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  int& st = done[{kern, dev}];
+  if (st == 0) {
+    st = -1;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(256);
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) == cudaSuccess && nc > 0) st = 1;
+    }
+    cudaGetLastError();
+  }
+  return st == 1;
+}
+
 // The ordered product psi <- U_m psi over cm propagators (magnus.py:249-252),
 // rows into traj_rows (cm, N), NormDrift index (m0 + m) into bad_norm.
 // chainw: 64 B device scratch.
@@ -1034,6 +1250,24 @@ static int chain_run(const double2* u, int64_t N, int64_t cm, const double2* psi
     chain_cta64_kernel<<<1, 256, ring, st>>>(u, (int)N, cm, psi, traj_rows, m0, bad_norm);
     prof_end(pr, st);
     QCH_LAUNCH_CHECK("chain_cta64_kernel");
+    note_launch(1);
+  } else if (N <= chain_cluster_max() && cluster_ok((const void*)chain_cluster_for(N), kCcCtas)) {
+    auto kern = chain_cluster_for(N);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCcCtas;
+    at[0].val.clusterDim.y = at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(kCcCtas);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    void* pr = prof_begin("chain_cluster_kernel", st);
+    static const int pfd = getenv("QCH_CHAIN_PFD") ? std::max(2, atoi(getenv("QCH_CHAIN_PFD"))) : 4;
+    QCH_CUDA(cudaLaunchKernelEx(&cfg, kern, u, (int)N, cm, psi, traj_rows, m0, bad_norm, pfd));
+    prof_end(pr, st);
+    QCH_LAUNCH_CHECK("chain_cluster_kernel");
     note_launch(1);
   } else {
     // rows per CTA: one CTA for small N, up to one per SM for large N
