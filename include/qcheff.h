@@ -184,6 +184,11 @@ int qch_magnus_assemble_c128(const void* d_h0, const void* d_hk, const void* d_c
 int qch_expm_minus_i_batch_c128(const void* d_h, int64_t batch, int64_t n, void* d_u, void* d_work,
                                 int64_t* bad_index, void* stream);
 
+/* The scaling norm of _expm_minus_i (expm.py:59) for a batch: d_out[b] =
+ * max_r sum_c |(-i H_b)_rc|, numpy's pairwise summation order bit for bit
+ * (the value that picks the number of squarings).  Asynchronous. */
+int qch_expm_norm_c128(const void* d_h, int64_t batch, int64_t n, double* d_out, void* stream);
+
 /* UnitaryPropagator.validate (expm.py:40-47) for a batch: returns
  * QCH_ERR_NONFINITE (and *bad_index) for the first propagator with
  * ||UU^dag - I||_F > 1e-10*n or ||det U| - 1| > 1e-8. */

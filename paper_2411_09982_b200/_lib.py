@@ -55,6 +55,7 @@ PROTOTYPES = {
         [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_int64, c_int64, c_double, c_int, c_void_p, c_void_p],
     ),
     "qch_expm_minus_i_batch_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, P_int64, c_void_p]),
+    "qch_expm_norm_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "qch_validate_unitary_batch_c128": (c_int, [c_void_p, c_int64, c_int64, P_int64, c_void_p]),
     "qch_unitarity_defect_c128": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "qch_magnus_evolve_c128": (

@@ -172,53 +172,59 @@ __global__ void antiherm_kernel(const double2* __restrict__ p, int n, double2* _
   }
 }
 
-// per-matrix max row sum of |(-i H)|, numpy's pairwise order: one WARP per
-// row — the top D levels of numpy's split tree (n -> n2 = n/2 - (n/2)%8 and
-// n - n2, every node above depth D larger than 128) are spread over the
-// 2^D lanes (lane bits = left/right choices, deepest level in bit 0), each
-// lane sums its subtree with np_pairwise_rec, and the 2^D partial sums are
-// combined by xor shuffles in tree order (fp addition commutes, so the
-// result is numpy's bit for bit).
-static int rownorm_depth(int n) {
-  auto ok = [](auto&& self, int size, int d) -> bool {
-    if (d == 0) return true;
-    if (size <= 128) return false;
-    int n2 = size / 2;
-    n2 -= n2 % 8;
-    return self(self, n2, d - 1) && self(self, size - n2, d - 1);
-  };
-  int D = 0;
-  while (D < 5 && ok(ok, n, D + 1)) ++D;
-  return D;
+// per-matrix max row sum of |(-i H)| in numpy's pairwise order (expm.py:59,
+// np.abs(a).sum(axis=1)): one WARP per row walks numpy's split tree (n -> n2
+// = n/2 - (n/2)%8 and n - n2 while n > 128) uniformly; at each leaf of <= 128
+// entries all 32 lanes evaluate |z| (the expensive part: a division and a
+// square root per entry) into a per-warp shared buffer, lanes 0..7 run
+// numpy's eight accumulators, and a 3-level shuffle tree combines them in
+// numpy's order, so the result is numpy's bit for bit.
+__device__ double rownorm_leaf(const double2* __restrict__ row, int off, int n, double* buf, int lane) {
+  for (int i = lane; i < n; i += 32) {
+    const double2 v = row[off + i];
+    buf[i] = np_cabs(v.y, -v.x);
+  }
+  __syncwarp();
+  double res = 0.0;
+  if (n < 8) {
+    if (lane == 0)
+      for (int i = 0; i < n; ++i) res = QADD(res, buf[i]);
+  } else {
+    const int n8 = n - (n % 8);
+    double r = 0.0;
+    if (lane < 8) {
+      r = buf[lane];
+      for (int i = 8; i < n8; i += 8) r = QADD(r, buf[i + lane]);
+    }
+    r = QADD(r, __shfl_down_sync(0xffffffffu, r, 1));  // lanes 0,2,4,6: r0+r1, r2+r3, ...
+    r = QADD(r, __shfl_down_sync(0xffffffffu, r, 2));  // lanes 0,4
+    r = QADD(r, __shfl_down_sync(0xffffffffu, r, 4));  // lane 0
+    if (lane == 0) {
+      res = r;
+      for (int i = n8; i < n; ++i) res = QADD(res, buf[i]);
+    }
+  }
+  __syncwarp();  // buf is reused by the next leaf
+  return __shfl_sync(0xffffffffu, res, 0);
 }
 
-__global__ void __launch_bounds__(256) rownorm_kernel(const double2* __restrict__ h, int n, int64_t batch, int D,
+__device__ __noinline__ double rownorm_rec(const double2* __restrict__ row, int off, int n, double* buf, int lane) {
+  if (n <= 128) return rownorm_leaf(row, off, n, buf, lane);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  const double a = rownorm_rec(row, off, n2, buf, lane);
+  const double b = rownorm_rec(row, off + n2, n - n2, buf, lane);
+  return QADD(a, b);
+}
+
+__global__ void __launch_bounds__(256) rownorm_kernel(const double2* __restrict__ h, int n, int64_t batch,
                                                       unsigned long long* __restrict__ norm) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  __shared__ double s_buf[8][128];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
   if (t >= (int64_t)n * batch) return;
   const int64_t b = t / n, r = t - b * n;
-  const double2* row = h + b * (int64_t)n * n + r * n;
-  auto f = [&](int c) {
-    const double2 v = row[c];
-    return np_cabs(v.y, -v.x);
-  };
-  double s = 0.0;
-  if (lane < (1 << D)) {
-    int off = 0, size = n;
-    for (int lv = 0; lv < D; ++lv) {
-      int n2 = size / 2;
-      n2 -= n2 % 8;
-      if ((lane >> (D - 1 - lv)) & 1) {
-        off += n2;
-        size -= n2;
-      } else {
-        size = n2;
-      }
-    }
-    s = np_pairwise_rec(f, off, size);
-  }
-  for (int k = 0; k < D; ++k) s = QADD(s, __shfl_xor_sync(0xffffffffu, s, 1 << k));
+  const double s = rownorm_rec(h + b * (int64_t)n * n + r * n, 0, n, s_buf[warp], lane);
   if (lane == 0) atomicMax(norm + b, (unsigned long long)__double_as_longlong(s));
 }
 
@@ -286,9 +292,9 @@ __global__ void select_square_kernel(double2* __restrict__ out, const double2* _
 
 // Ordered product psi <- U_m psi over a chunk of intervals for N > 4 (the
 // reference's sequential loop, magnus.py:249-252), with the NormDrift check
-// of every row (:270-273).  G CTAs (G = 1 for small N; a cooperative grid
-// for large N, where one SM cannot pull an N x N propagator per step fast
-// enough): CTA g owns rows [g R, g R + R); each warp computes one row at a
+// of every row (:270-273), for N above the one-cluster chain's range (or
+// when a 16-CTA cluster cannot be scheduled).  G CTAs (a cooperative grid:
+// one SM cannot pull an N x N propagator per step fast enough): CTA g owns rows [g R, g R + R); each warp computes one row at a
 // time with its lanes striding the columns (coalesced 512-byte reads of U),
 // reads x = the previous trajectory row straight from L2, and writes its
 // y_r into the trajectory.  Steps are separated by a grid barrier (monotone
@@ -375,104 +381,9 @@ __global__ void __launch_bounds__(kChainThreads) chain_grid_kernel(const double2
   }
 }
 
-// The ordered product for N <= 64 in ONE CTA: the propagators stream
-// through a 3-stage shared-memory ring by TMA bulk copies (one
-// cp.async.bulk of n*n*16 contiguous bytes per interval, completion on an
-// mbarrier), so up to three intervals' propagators are in flight while the
-// state advances — one SM alone could not keep enough plain loads in flight
-// to cover HBM latency at one propagator per step.  Warp w owns rows
-// 8w..8w+7, lane l columns l and l+32; the state lives in shared memory.
-constexpr int kChainStages = 3;
-
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-__global__ void __launch_bounds__(256) chain_cta64_kernel(const double2* __restrict__ u, int n, int64_t mb,
-                                                          const double2* __restrict__ psi_in,
-                                                          double2* __restrict__ traj_rows, int64_t m0,
-                                                          unsigned long long* bad_norm) {
-  extern __shared__ __align__(128) double2 s_ring[];  // kChainStages x n x n
-  __shared__ __align__(8) unsigned long long s_bar[kChainStages];
-  __shared__ double2 s_x[2][64];
-  __shared__ double s_nrm[2][8];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nn = (int64_t)n * n;
-  const unsigned bytes = (unsigned)(nn * sizeof(double2));
-  if (threadIdx.x < 64) s_x[0][threadIdx.x] = threadIdx.x < n ? psi_in[threadIdx.x] : make_double2(0.0, 0.0);
-  if (threadIdx.x >= 64 && threadIdx.x < 128) s_x[1][threadIdx.x - 64] = make_double2(0.0, 0.0);
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < kChainStages; ++q)
-      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[q])) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int64_t m) {  // thread 0: propagator m into its stage
-    if (m >= mb) return;
-    const int q = (int)(m % kChainStages);
-    const unsigned bar = smem_u32(&s_bar[q]);
-    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(s_ring + (int64_t)q * nn)),
-        "l"(u + m * nn), "r"(bytes), "r"(bar)
-        : "memory");
-  };
-  if (threadIdx.x == 0)
-    for (int q = 0; q < kChainStages; ++q) issue(q);
-  for (int64_t m = 0; m < mb; ++m) {
-    const int q = (int)(m % kChainStages);
-    const unsigned par = (unsigned)((m / kChainStages) & 1);
-    asm volatile(
-        "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(
-            smem_u32(&s_bar[q])),
-        "r"(par)
-        : "memory");
-    const double2* um = s_ring + (int64_t)q * nn;
-    const double2* x = s_x[m & 1];
-    const double2 x0 = x[lane], x1 = x[lane + 32];
-    double yr[8], yi[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int r = warp * 8 + k;
-      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-      if (r < n) {
-        if (lane < n) a0 = um[r * n + lane];
-        if (lane + 32 < n) a1 = um[r * n + lane + 32];
-      }
-      yr[k] = fma(a0.x, x0.x, fma(-a0.y, x0.y, fma(a1.x, x1.x, -a1.y * x1.y)));
-      yi[k] = fma(a0.x, x0.y, fma(a0.y, x0.x, fma(a1.x, x1.y, a1.y * x1.x)));
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        yr[k] += __shfl_xor_sync(0xffffffffu, yr[k], off);
-        yi[k] += __shfl_xor_sync(0xffffffffu, yi[k], off);
-      }
-    if (lane == 0) {
-      double part = 0.0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int r = warp * 8 + k;
-        if (r < n) {
-          s_x[(m + 1) & 1][r] = make_double2(yr[k], yi[k]);
-          __stcg(traj_rows + m * n + r, make_double2(yr[k], yi[k]));
-          part += yr[k] * yr[k] + yi[k] * yi[k];
-        }
-      }
-      s_nrm[m & 1][warp] = part;
-    }
-    __syncthreads();  // stage q fully read; the new state visible
-    if (threadIdx.x == 0) {
-      issue(m + kChainStages);
-      double t = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) t += s_nrm[m & 1][w];
-      if (!(fabs(sqrt(t) - 1.0) <= 1e-6)) atomicMin(bad_norm, (unsigned long long)(m0 + m));
-    }
-  }
-}
-
-// The ordered product for 64 < N <= 32 CPL in ONE thread-block cluster of
+// The ordered product for 4 < N <= 32 CPL in ONE thread-block cluster of
 // kCcCtas CTAs, with no grid barrier: CTA g owns rows [8 RPW g, 8 RPW g +
 // 8 RPW), warp w rows 8 RPW g + RPW w + q.  Each CTA keeps the state in two
 // shared-memory buffers; a row's new amplitude is pushed into EVERY CTA's
@@ -988,7 +899,7 @@ static int expm_generic(const double2* h, int64_t batch, int n, double2* u, doub
   const int64_t nn = (int64_t)n * n;
   unsigned* hflag = (unsigned*)(norm + batch);
   QCH_CUDA(cudaMemsetAsync(norm, 0, sizeof(unsigned long long) * 2 * batch, st));
-  rownorm_kernel<<<(int)((n * batch + 7) / 8), 256, 0, st>>>(h, n, batch, rownorm_depth(n), norm);
+  rownorm_kernel<<<(int)((n * batch + 7) / 8), 256, 0, st>>>(h, n, batch, norm);
   herm_check_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, n, batch, hflag);
   QCH_LAUNCH_CHECK("herm_check_kernel");
   note_launch(2);
@@ -1111,6 +1022,20 @@ static int report_bad(unsigned long long* d_bad, int64_t* bad_index, int code, c
     if (bad_index) *bad_index = (int64_t)b;
     return fail(code, std::string(what) + " (item " + std::to_string(b) + ")");
   }
+  return QCH_OK;
+}
+
+// The scaling norm of _expm_minus_i (expm.py:59) per batch item, numpy's
+// value bit for bit: max_r sum_c |(-i H)_rc| in pairwise order.
+extern "C" int qch_expm_norm_c128(const void* d_h, int64_t batch, int64_t n, double* d_out, void* stream) {
+  if (batch <= 0) return QCH_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  QCH_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double) * batch, st));
+  if (n <= 0) return QCH_OK;
+  rownorm_kernel<<<(int)((n * batch + 7) / 8), 256, 0, st>>>((const double2*)d_h, (int)n, batch,
+                                                             (unsigned long long*)d_out);
+  QCH_LAUNCH_CHECK("rownorm_kernel");
+  note_launch(1);
   return QCH_OK;
 }
 
@@ -1243,15 +1168,7 @@ static bool cluster_ok(const void* kern, int G) {
 // chainw: 64 B device scratch.
 static int chain_run(const double2* u, int64_t N, int64_t cm, const double2* psi, double2* traj_rows, int64_t m0,
                      void* chainw, unsigned long long* bad_norm, cudaStream_t st) {
-  if (N <= 64) {
-    void* pr = prof_begin("chain_cta64_kernel", st);
-    const size_t ring = sizeof(double2) * kChainStages * (size_t)N * N;
-    QCH_CUDA(smem_attr((const void*)chain_cta64_kernel, (int)(sizeof(double2) * kChainStages * 64 * 64)));
-    chain_cta64_kernel<<<1, 256, ring, st>>>(u, (int)N, cm, psi, traj_rows, m0, bad_norm);
-    prof_end(pr, st);
-    QCH_LAUNCH_CHECK("chain_cta64_kernel");
-    note_launch(1);
-  } else if (N <= chain_cluster_max() && cluster_ok((const void*)chain_cluster_for(N), kCcCtas)) {
+  if (N <= chain_cluster_max() && cluster_ok((const void*)chain_cluster_for(N), kCcCtas)) {
     auto kern = chain_cluster_for(N);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];

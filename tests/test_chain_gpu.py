@@ -1,7 +1,6 @@
 """The ordered product psi <- U_m psi (magnus.py:249-252) through
-qch_magnus_chain_c128 at every kernel's size range: the TMA ring CTA
-(N <= 64), the one-cluster DSMEM chain (64 < N <= 384) and the cooperative
-grid (larger N), including ragged N and chunks of 1..3 intervals, against a
+qch_magnus_chain_c128 at both kernels' size ranges: the one-cluster DSMEM
+chain (4 < N <= 384) and the cooperative grid (larger N), including ragged N and chunks of 1..3 intervals, against a
 numpy sequential product (fp64, bar 1e-12 relative per row); and the
 NormDrift check (magnus.py:270-273) flagging the first non-unitary interval
 with its index."""
@@ -38,8 +37,9 @@ def _ref(us, psi):
     return np.stack(out)
 
 
-@pytest.mark.parametrize("n,m", [(48, 5), (65, 7), (100, 3), (128, 40), (129, 2), (200, 17), (256, 33), (256, 1),
-                                 (300, 9), (384, 12), (385, 4), (512, 6)])
+@pytest.mark.parametrize("n,m", [(5, 9), (8, 3), (17, 30), (48, 5), (64, 64), (65, 7), (100, 3), (128, 40),
+                                 (129, 2), (200, 17), (256, 33), (256, 1), (300, 9), (384, 12), (385, 4),
+                                 (512, 6)])
 def test_chain_vs_numpy(n, m):
     us = _unitaries(n, m, seed=n + m)
     rng = np.random.default_rng(n)
@@ -52,7 +52,7 @@ def test_chain_vs_numpy(n, m):
     assert e.max() <= 1e-12, (e.max(), int(e.argmax()))
 
 
-@pytest.mark.parametrize("n", [100, 256, 384, 600])
+@pytest.mark.parametrize("n", [6, 100, 256, 384, 600])
 def test_chain_norm_drift_index(n):
     m = 11
     us = _unitaries(n, m, seed=3)
