@@ -767,7 +767,7 @@ def sec_midsize(torch, eff, lib, args, fp64, L=8, n_int=2048):
     rp = int(lib.load().qch_zgemm_real_products())
     frac_h = _herm_fraction(n)
     ach = fl / (g_ms * 1e-3) / 1e12 if g_ms else None
-    chain_ms = prof.get("chain_grid_kernel", (0.0, 1))[0] / 3
+    chain_ms = sum(v[0] for k, v in prof.items() if k.startswith("chain_")) / 3
     # CPU: the oracle (numpy restatement of evolve, 18-term Taylor, order 2) on 8 intervals
     k_cpu = 8
     d0 = ch.drift.to_dense()

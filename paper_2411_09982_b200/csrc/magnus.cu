@@ -1215,6 +1215,13 @@ static int chain_run(const double2* u, int64_t N, int64_t cm, const double2* psi
   return QCH_OK;
 }
 
+// intervals per chunk of the N > 4 evolve at most (QCH_EVOLVE_CHUNK, for
+// tests of the chunk hand-over; default 4096)
+static int64_t evolve_chunk_cap() {
+  static const int64_t v = getenv("QCH_EVOLVE_CHUNK") ? std::max(1LL, atoll(getenv("QCH_EVOLVE_CHUNK"))) : 4096;
+  return v;
+}
+
 static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_comm_in, int64_t K, int64_t N,
                               const double* d_sig, int64_t S, double t_start, double t_end, int64_t M, int order,
                               const void* d_psi0, void* d_traj, void* d_props, int check, int64_t* bad_index,
@@ -1269,7 +1276,7 @@ static int magnus_evolve_impl(const void* d_h0, const void* d_hk, const void* d_
     // chunk so that 10 matrices per interval (Hbar, U, 8 of expm work) stay within ~20 GiB
     const size_t per = sizeof(double2) * (size_t)nn;
     int64_t mb = std::max<int64_t>(1, std::min<int64_t>(M, (int64_t)((20ull << 30) / (10 * per))));
-    mb = std::min<int64_t>(mb, 4096);
+    mb = std::min<int64_t>(mb, evolve_chunk_cap());
     DevBuf buf(st);
     QCH_CUDA(buf.alloc(per * mb * 10 + sizeof(double2) * N + sizeof(int) * mb + sizeof(unsigned long long) * 2 * mb +
                        sizeof(double) * 2 * mb + 64));
