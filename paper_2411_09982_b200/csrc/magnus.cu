@@ -173,59 +173,110 @@ __global__ void antiherm_kernel(const double2* __restrict__ p, int n, double2* _
 }
 
 // per-matrix max row sum of |(-i H)| in numpy's pairwise order (expm.py:59,
-// np.abs(a).sum(axis=1)): one WARP per row walks numpy's split tree (n -> n2
-// = n/2 - (n/2)%8 and n - n2 while n > 128) uniformly; at each leaf of <= 128
-// entries all 32 lanes evaluate |z| (the expensive part: a division and a
-// square root per entry) into a per-warp shared buffer, lanes 0..7 run
-// numpy's eight accumulators, and a 3-level shuffle tree combines them in
-// numpy's order, so the result is numpy's bit for bit.
-__device__ double rownorm_leaf(const double2* __restrict__ row, int off, int n, double* buf, int lane) {
-  for (int i = lane; i < n; i += 32) {
-    const double2 v = row[off + i];
-    buf[i] = np_cabs(v.y, -v.x);
+// np.abs(a).sum(axis=1)), bit for bit: one WARP per row.  numpy's tree: a
+// node of n > 128 entries splits into n2 = n/2 - (n/2)%8 and n - n2; a leaf
+// (<= 128) sums with eight accumulators r_k (entries k, k+8, ... below the
+// last multiple of 8), combines ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and adds
+// the remainder in order.  The top Dg <= 2 levels of the tree are spread over
+// 2^Dg lane groups (deepest level in the lowest group bit, combined first by
+// xor shuffles — fp addition commutes, so the order is numpy's); each group
+// of GS = 32 / 2^Dg lanes walks its subtree's leaves, every lane evaluating
+// |z| (a correctly rounded division and square root: the cost) for one entry
+// per round of GS, the value shuffled to the lane owning its accumulator.
+static int rownorm_depth(int n) {
+  auto ok = [](auto&& self, int size, int d) -> bool {
+    if (d == 0) return true;
+    if (size <= 128) return false;
+    int n2 = size / 2;
+    n2 -= n2 % 8;
+    return self(self, n2, d - 1) && self(self, size - n2, d - 1);
+  };
+  int D = 0;
+  while (D < 2 && ok(ok, n, D + 1)) ++D;
+  return D;
+}
+
+template <int GS>
+struct RowNorm {
+  const double2* row;
+  unsigned mask;  // this group's lanes
+  int gbase;      // first lane of the group
+  int gl;         // lane within the group
+  __device__ double f(int c) const {
+    const double2 v = row[c];
+    return np_cabs(v.y, -v.x);
   }
-  __syncwarp();
-  double res = 0.0;
-  if (n < 8) {
-    if (lane == 0)
-      for (int i = 0; i < n; ++i) res = QADD(res, buf[i]);
-  } else {
-    const int n8 = n - (n % 8);
+  __device__ double leaf(int off, int n) const {
+    if (n < 8) {  // numpy: plain sequential sum (every lane alike)
+      double res = 0.0;
+      for (int i = 0; i < n; ++i) res = QADD(res, f(off + i));
+      return res;
+    }
+    const int n8 = n - (n % 8), k = gl & 7;
     double r = 0.0;
-    if (lane < 8) {
-      r = buf[lane];
-      for (int i = 8; i < n8; i += 8) r = QADD(r, buf[i + lane]);
+    for (int base = 0; base < n8; base += GS) {
+      const int idx = base + gl;
+      const double v = idx < n8 ? f(off + idx) : 0.0;
+#pragma unroll
+      for (int p = 0; p < GS / 8; ++p) {
+        const double w = __shfl_sync(mask, v, gbase + p * 8 + k);
+        const int e = base + p * 8 + k;  // the entry lane k accumulates now
+        if (gl < 8 && e < n8) r = e < 8 ? w : QADD(r, w);
+      }
     }
-    r = QADD(r, __shfl_down_sync(0xffffffffu, r, 1));  // lanes 0,2,4,6: r0+r1, r2+r3, ...
-    r = QADD(r, __shfl_down_sync(0xffffffffu, r, 2));  // lanes 0,4
-    r = QADD(r, __shfl_down_sync(0xffffffffu, r, 4));  // lane 0
-    if (lane == 0) {
-      res = r;
-      for (int i = n8; i < n; ++i) res = QADD(res, buf[i]);
-    }
+    r = QADD(r, __shfl_xor_sync(mask, r, 1));
+    r = QADD(r, __shfl_xor_sync(mask, r, 2));
+    r = QADD(r, __shfl_xor_sync(mask, r, 4));
+    for (int i = n8; i < n; ++i) r = QADD(r, f(off + i));
+    return __shfl_sync(mask, r, gbase);
   }
-  __syncwarp();  // buf is reused by the next leaf
-  return __shfl_sync(0xffffffffu, res, 0);
-}
+  __device__ __noinline__ double rec(int off, int n) const {
+    if (n <= 128) return leaf(off, n);
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    const double a = rec(off, n2);
+    const double b = rec(off + n2, n - n2);
+    return QADD(a, b);
+  }
+};
 
-__device__ __noinline__ double rownorm_rec(const double2* __restrict__ row, int off, int n, double* buf, int lane) {
-  if (n <= 128) return rownorm_leaf(row, off, n, buf, lane);
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  const double a = rownorm_rec(row, off, n2, buf, lane);
-  const double b = rownorm_rec(row, off + n2, n - n2, buf, lane);
-  return QADD(a, b);
-}
-
+template <int DG>
 __global__ void __launch_bounds__(256) rownorm_kernel(const double2* __restrict__ h, int n, int64_t batch,
                                                       unsigned long long* __restrict__ norm) {
-  __shared__ double s_buf[8][128];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp;
+  constexpr int GS = 32 >> DG;
+  const int lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= (int64_t)n * batch) return;
   const int64_t b = t / n, r = t - b * n;
-  const double s = rownorm_rec(h + b * (int64_t)n * n + r * n, 0, n, s_buf[warp], lane);
+  const int grp = lane / GS;
+  RowNorm<GS> rn;
+  rn.row = h + b * (int64_t)n * n + r * n;
+  rn.gbase = grp * GS;
+  rn.gl = lane - rn.gbase;
+  rn.mask = (GS == 32) ? 0xffffffffu : (((1u << GS) - 1u) << rn.gbase);
+  int off = 0, size = n;  // this group's subtree: group bits = left/right choices, deepest level in bit 0
+  for (int lv = 0; lv < DG; ++lv) {
+    int n2 = size / 2;
+    n2 -= n2 % 8;
+    if ((grp >> (DG - 1 - lv)) & 1) {
+      off += n2;
+      size -= n2;
+    } else {
+      size = n2;
+    }
+  }
+  double s = rn.rec(off, size);
+  for (int k = 0; k < DG; ++k) s = QADD(s, __shfl_xor_sync(0xffffffffu, s, GS << k));
   if (lane == 0) atomicMax(norm + b, (unsigned long long)__double_as_longlong(s));
+}
+
+static void rownorm_launch(const double2* h, int n, int64_t batch, unsigned long long* norm, cudaStream_t st) {
+  const int blocks = (int)((n * batch + 7) / 8);
+  switch (rownorm_depth(n)) {
+    case 0: rownorm_kernel<0><<<blocks, 256, 0, st>>>(h, n, batch, norm); break;
+    case 1: rownorm_kernel<1><<<blocks, 256, 0, st>>>(h, n, batch, norm); break;
+    default: rownorm_kernel<2><<<blocks, 256, 0, st>>>(h, n, batch, norm); break;
+  }
 }
 
 // a = (-i H) / 2**s ; out = I + a ; term = a  (Taylor k = 1)
@@ -899,7 +950,7 @@ static int expm_generic(const double2* h, int64_t batch, int n, double2* u, doub
   const int64_t nn = (int64_t)n * n;
   unsigned* hflag = (unsigned*)(norm + batch);
   QCH_CUDA(cudaMemsetAsync(norm, 0, sizeof(unsigned long long) * 2 * batch, st));
-  rownorm_kernel<<<(int)((n * batch + 7) / 8), 256, 0, st>>>(h, n, batch, norm);
+  rownorm_launch(h, n, batch, norm, st);
   herm_check_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, n, batch, hflag);
   QCH_LAUNCH_CHECK("herm_check_kernel");
   note_launch(2);
@@ -1032,8 +1083,7 @@ extern "C" int qch_expm_norm_c128(const void* d_h, int64_t batch, int64_t n, dou
   cudaStream_t st = (cudaStream_t)stream;
   QCH_CUDA(cudaMemsetAsync(d_out, 0, sizeof(double) * batch, st));
   if (n <= 0) return QCH_OK;
-  rownorm_kernel<<<(int)((n * batch + 7) / 8), 256, 0, st>>>((const double2*)d_h, (int)n, batch,
-                                                             (unsigned long long*)d_out);
+  rownorm_launch((const double2*)d_h, (int)n, batch, (unsigned long long*)d_out, st);
   QCH_LAUNCH_CHECK("rownorm_kernel");
   note_launch(1);
   return QCH_OK;
