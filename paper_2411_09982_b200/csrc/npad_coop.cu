@@ -74,7 +74,44 @@ struct CoopArgs {
   long long* out_applied;
   int* out_status;
   long long* stats;  // non-null (QCH_NPAD_STATS): CTA 0 phase cycles [wait, combine, scalars, rotate, rescan, publish], rescans
+  int mbx;           // cluster mode: records by st.async onto byte-counting mbarriers (else barrier.cluster)
 };
+
+// one 16-byte piece of a record field into a peer CTA's shared memory, its
+// bytes counted on the peer's mbarrier (st.async: the completion has release
+// semantics at cluster scope)
+__device__ __forceinline__ void st_async16(unsigned raddr, unsigned rbar, const void* src) {
+  const unsigned long long* p = (const unsigned long long*)src;
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "l"(p[0]), "l"(p[1]), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned map_rank(unsigned addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// wait for a phase of a local mbarrier; acquire at cluster scope (the peers'
+// matrix writes ordered before their records become visible)
+__device__ __forceinline__ void mbar_wait_cluster(unsigned bar, unsigned par) {
+  asm volatile(
+      "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(
+          bar),
+      "r"(par)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arm(unsigned bar, unsigned tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+}
+// a Cand field (48 bytes) of this CTA's record into peer `rank`
+__device__ __forceinline__ void send_cand(const Cand& c, Cand* local_field, unsigned local_bar, unsigned rank) {
+  static_assert(sizeof(Cand) == 48, "Cand layout");
+  const unsigned ra = map_rank(smem_addr(local_field), rank), rb = map_rank(local_bar, rank);
+  const unsigned char* src = (const unsigned char*)&c;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) st_async16(ra + 16 * k, rb, src + 16 * k);
+}
 
 __device__ __forceinline__ int ld_acq(const int* p) {
   int v;
@@ -144,6 +181,7 @@ template <bool EK, bool CL>
 __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid_constant__ CoopArgs a) {
   namespace cg = cooperative_groups;
   __shared__ CoopRec s_rec[CL ? 2 : 1][CL ? kClusterMax : 1];
+  __shared__ __align__(8) unsigned long long s_xbar[2];  // CL + mbx: record bytes of a publication
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp_u = __shfl_sync(0xffffffffu, tid >> 5, 0);  // provably warp-uniform (converged shuffles)
   const int G = gridDim.x, g = blockIdx.x;
@@ -176,12 +214,31 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
   long long applied = 0;
   int status = 0;
   int pi_row = -1, pj_row = -1;  // rows whose state comes from the partials of the last rotation
+  const bool mbx = CL && a.mbx != 0;
+  const unsigned xtx = (unsigned)(G * 3 * sizeof(Cand));  // record bytes a CTA receives per publication
+  if (mbx) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_xbar[0])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_xbar[1])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_arm(smem_addr(&s_xbar[0]), xtx);
+    }
+    cg::this_cluster().sync();  // every CTA's barriers initialised before any record is sent
+  }
   // first publication: own bests only
   {
     Cand own = cand_none();
     for (int k = tid; k < nr; k += kCoopThreads) cand_take(own, s_row[k]);
     own = block_best_p(own, s_part);
-    if (CL) {
+    if (mbx) {
+      if (tid < G) {
+        const Cand none = cand_none();
+        const unsigned lb = smem_addr(&s_xbar[0]);
+        send_cand(own, &s_rec[0][g].own, lb, tid);
+        send_cand(none, &s_rec[0][g].pi, lb, tid);
+        send_cand(none, &s_rec[0][g].pj, lb, tid);
+      }
+    } else if (CL) {
       if (tid < G) {
         CoopRec* r = cg::this_cluster().map_shared_rank(&s_rec[0][g], tid);
         r->own = own;
@@ -212,6 +269,11 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     // (waiting for every CTA's record of this epoch is the grid barrier: the
     // acquire makes each publisher's matrix writes visible)
     const CoopRec* rec = CL ? s_rec[applied & 1] : a.rec + (size_t)(applied & 1) * G;
+    if (mbx) {
+      mbar_wait_cluster(smem_addr(&s_xbar[applied & 1]), (unsigned)((applied >> 1) & 1));
+      // the barrier of the next publication: its previous phase completed one rotation ago
+      if (tid == 0) mbar_arm(smem_addr(&s_xbar[(applied + 1) & 1]), xtx);
+    }
     if (!CL) {
       if (tid < 32) {
         for (int k = tid; k < G; k += 32)
@@ -443,16 +505,24 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
         Cand x = lane < kCoopWarps ? s_part[warp_u * kCoopWarps + lane] : cand_none();
         x = warp_best(x);
         if (lane < G) {
-          CoopRec* r = cg::this_cluster().map_shared_rank(&s_rec[applied & 1][g], lane);
-          if (warp_u == 0)
-            r->own = x;
-          else if (warp_u == 1)
-            r->pi = x;
-          else
-            r->pj = x;
+          if (mbx) {
+            CoopRec* lr = &s_rec[applied & 1][g];
+            send_cand(x, warp_u == 0 ? &lr->own : warp_u == 1 ? &lr->pi : &lr->pj,
+                      smem_addr(&s_xbar[applied & 1]), lane);
+          } else {
+            CoopRec* r = cg::this_cluster().map_shared_rank(&s_rec[applied & 1][g], lane);
+            if (warp_u == 0)
+              r->own = x;
+            else if (warp_u == 1)
+              r->pi = x;
+            else
+              r->pj = x;
+          }
         }
       }
-      cg::this_cluster().sync();  // release/acquire: records and matrix writes
+      // release/acquire: records and matrix writes (mbx: the records' st.async
+      // completions release, the next phase B's wait acquires)
+      if (!mbx) cg::this_cluster().sync();
     } else {
       block_best3_w0(own, ppi, ppj, s_part);  // valid in warp 0: the record writer
       tick(7);
@@ -470,6 +540,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     pj_row = j;
     tick(5);
   }
+  if (mbx) cg::this_cluster().sync();  // no CTA leaves while a peer may still address it
   if (a.stats != nullptr && tid == 0)
     for (int k = 0; k < 8; ++k) a.stats[8 * g + k] = cyc[k];
   if (g == 0 && tid == 0) {
@@ -569,6 +640,8 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   a.pivots = pivots;
   a.pivot_cap = pivot_cap;
   a.stats = nullptr;
+  static const int mbx_env = getenv("QCH_NPAD_COOP_MBX") ? atoi(getenv("QCH_NPAD_COOP_MBX")) : 1;
+  a.mbx = mbx_env;
   static long long* d_cstats = nullptr;
   if (getenv("QCH_NPAD_STATS")) {
     if (d_cstats == nullptr) QCH_CUDA(cudaMalloc(&d_cstats, 8 * kMaxCoopCtas * sizeof(long long)));
