@@ -60,6 +60,9 @@ namespace qch {
 constexpr int kFusedWarps = 4;
 constexpr int kFusedThreads = 32 * kFusedWarps;
 constexpr int kR = 2;  // consecutive intervals per thread
+#ifndef QCH_FUSED_MINB
+#define QCH_FUSED_MINB 3  // resident CTAs per SM asked of ptxas for N <= 3 (4: 128 registers + spills, 1.94e9 vs 2.04e9 intervals/s)
+#endif
 constexpr int kTile = kFusedThreads * kR;  // intervals per tile (one block)
 
 constexpr int kOpsInline = (1 + kMaxK) * 16;
@@ -366,7 +369,7 @@ __device__ __forceinline__ void group_lead(const FusedArgs& g, int64_t gi, int64
 }
 
 template <int N>
-__global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : 3))
+__global__ void __launch_bounds__(kFusedThreads, (N >= 4 ? 2 : QCH_FUSED_MINB))
     magnus_fused_kernel(const __grid_constant__ FusedArgs g) {
   extern __shared__ __align__(16) double2 fsm[];
   const int K = g.s.ca.K;
