@@ -353,7 +353,7 @@ __global__ void select_square_kernel(double2* __restrict__ out, const double2* _
 // prefetched into L2 before the barrier wait.  Norms accumulate into one of 3
 // rotating slots, checked by CTA 0 after each barrier.
 constexpr int kChainThreads = 256;
-template <int kChainRB>  // rows per warp in flight
+template <int kChainRB, int kUnr>  // rows per warp in flight, column-loop unroll
 __global__ void __launch_bounds__(kChainThreads) chain_grid_kernel(const double2* __restrict__ u, int n, int64_t mb,
                                                                    const double2* __restrict__ psi_in,
                                                                    double2* __restrict__ traj_rows, int64_t m0,
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_grid_kernel(const double2
       double ar[kChainRB], ai[kChainRB];
 #pragma unroll
       for (int q = 0; q < kChainRB; ++q) ar[q] = ai[q] = 0.0;
-      for (int c = lane; c < n; c += 32) {
+      auto col = [&](int c) {
         const double2 b = __ldcg(x + c);
 #pragma unroll
         for (int q = 0; q < kChainRB; ++q) {
@@ -385,6 +385,12 @@ __global__ void __launch_bounds__(kChainThreads) chain_grid_kernel(const double2
             ai[q] = fma(a.y, b.x, ai[q]);
           }
         }
+      };
+      if constexpr (kUnr == 0) {  // the compiler's choice
+        for (int c = lane; c < n; c += 32) col(c);
+      } else {
+#pragma unroll kUnr
+        for (int c = lane; c < n; c += 32) col(c);
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1)
@@ -403,8 +409,9 @@ __global__ void __launch_bounds__(kChainThreads) chain_grid_kernel(const double2
       }
     }
     if (lane == 0 && part != 0.0) atomicAdd(nrm3 + (m % 3), part);
-    // prefetch this CTA's rows of the next propagator into L2
-    if (m + 1 < mb) {
+    // prefetch this CTA's rows of the next propagator into L2 (when a
+    // propagator fits a quarter of L2; a larger one would only evict itself)
+    if (m + 1 < mb && nn * (int64_t)sizeof(double2) <= (32ll << 20)) {
       const char* nxt = (const char*)(um + nn + (int64_t)r0 * n);
       const int64_t bytes = (int64_t)(r1 - r0) * n * sizeof(double2);
       for (int64_t off = (int64_t)threadIdx.x * 128; off < bytes; off += (int64_t)kChainThreads * 128)
@@ -1249,10 +1256,24 @@ static int chain_run(const double2* u, int64_t N, int64_t cm, const double2* psi
     void* args[] = {(void*)&u, (void*)&nI, (void*)&cmv, (void*)&pin, (void*)&traj_rows, (void*)&m0v,
                     (void*)&barp, (void*)&nrm3, (void*)&bad_norm};
     // rows in flight per warp: as many as the CTA's rows allow
-    const int R = (int)((N + G - 1) / G), per_warp = R / (kChainThreads / 32);
-    auto kern = per_warp >= 8 ? chain_grid_kernel<8>
-              : per_warp >= 4 ? chain_grid_kernel<4>
-              : per_warp >= 2 ? chain_grid_kernel<2> : chain_grid_kernel<1>;
+    const int R = (int)((N + G - 1) / G);
+    static const int rb_env = getenv("QCH_CHAIN_RB") ? atoi(getenv("QCH_CHAIN_RB")) : 0;
+    const int per_warp = rb_env > 0 ? rb_env : R / (kChainThreads / 32);
+    // measured (tools/chain_probe.py): N <= 1024 the compiler-unrolled
+    // column loop with rows per warp from R; above, 4 rows per warp with
+    // the column loop unrolled 8 deep (64 loads in flight per lane group;
+    // N = 4096: 139 -> 56 us per step, 4.8 TB/s)
+    static const int unr_env = getenv("QCH_CHAIN_UNR") ? atoi(getenv("QCH_CHAIN_UNR")) : -1;
+    const bool deep = unr_env >= 0 ? unr_env == 8 : N > 1024;
+    const int pw = rb_env > 0 ? per_warp : deep ? 4 : per_warp;
+    auto kern = deep ? (pw >= 8   ? chain_grid_kernel<8, 8>
+                        : pw >= 4 ? chain_grid_kernel<4, 8>
+                        : pw >= 2 ? chain_grid_kernel<2, 8>
+                                  : chain_grid_kernel<1, 8>)
+                     : (pw >= 8   ? chain_grid_kernel<8, 0>
+                        : pw >= 4 ? chain_grid_kernel<4, 0>
+                        : pw >= 2 ? chain_grid_kernel<2, 0>
+                                  : chain_grid_kernel<1, 0>);
     void* pr = prof_begin("chain_grid_kernel", st);
     if (G > 1)
       QCH_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(kChainThreads), args, 0, st));

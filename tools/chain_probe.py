@@ -16,7 +16,7 @@ def main():
     lib = _lib.load()
     tag = os.environ.get("QCH_CHAIN_CLUSTER_MAX", "default")
     for n in [int(v) for v in os.environ.get("CHAIN_NS", "96,128,192,256,320,384,512,768").split(",")]:
-        m = 2048 if n <= 512 else 512
+        m = 2048 if n <= 512 else 512 if n <= 1024 else 64
         u = torch.randn((m, n, n), dtype=torch.complex128, device="cuda")
         u = torch.linalg.qr(u)[0]
         psi = torch.zeros(n, dtype=torch.complex128, device="cuda")
