@@ -75,6 +75,7 @@ struct CoopArgs {
   int* out_status;
   long long* stats;  // non-null (QCH_NPAD_STATS): CTA 0 phase cycles [wait, combine, scalars, rotate, rescan, publish], rescans
   int mbx;           // cluster mode: records by st.async onto byte-counting mbarriers (else barrier.cluster)
+  int pf_rescan;     // bulk-prefetch the rows about to be rescanned into L2 when the pivot is known
 };
 
 // one 16-byte piece of a record field into a peer CTA's shared memory, its
@@ -354,6 +355,19 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     }
     tick(1);
     const int i = (int)(piv.cr >> 16), j = (int)(piv.cr & 0xffffu);
+    // own rows whose best sat in column i or j will be rescanned after the
+    // rotation: their lower-triangle entries start moving into L2 now (one
+    // bulk prefetch per row), under the scalars and the rotation
+    if (a.pf_rescan)
+      for (int k = tid; k < nr; k += kCoopThreads) {
+        const Cand st = s_row[k];
+        const int bc = (st.q > 0.0) ? (int)(st.cr >> 16) : -1;
+        const int x = r0 + k;
+        if ((bc == i || bc == j) && x != i && x != j && x > 0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(h + (size_t)x * n),
+                       "r"((unsigned)(x * sizeof(double2)))
+                       : "memory");
+      }
     if (g == 0 && tid == 0 && a.pivots != nullptr && applied < a.pivot_cap) {
       a.pivots[2 * applied] = i;
       a.pivots[2 * applied + 1] = j;
@@ -642,6 +656,8 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   a.stats = nullptr;
   static const int mbx_env = getenv("QCH_NPAD_COOP_MBX") ? atoi(getenv("QCH_NPAD_COOP_MBX")) : 1;
   a.mbx = mbx_env;
+  static const int pf_env = getenv("QCH_NPAD_COOP_PF") ? atoi(getenv("QCH_NPAD_COOP_PF")) : 1;
+  a.pf_rescan = pf_env;
   static long long* d_cstats = nullptr;
   if (getenv("QCH_NPAD_STATS")) {
     if (d_cstats == nullptr) QCH_CUDA(cudaMalloc(&d_cstats, 8 * kMaxCoopCtas * sizeof(long long)));
