@@ -1,6 +1,7 @@
 """The ordered product psi <- U_m psi (magnus.py:249-252) through
 qch_magnus_chain_c128 at both kernels' size ranges: the one-cluster DSMEM
-chain (4 < N <= 384) and the cooperative grid (larger N), including ragged N and chunks of 1..3 intervals, against a
+chain (4 < N <= 384) and the cooperative grid (larger N; 4 rows per warp
+above 1024), including ragged N and chunks of 1..3 intervals, against a
 numpy sequential product (fp64, bar 1e-12 relative per row); and the
 NormDrift check (magnus.py:270-273) flagging the first non-unitary interval
 with its index."""
@@ -39,7 +40,7 @@ def _ref(us, psi):
 
 @pytest.mark.parametrize("n,m", [(5, 9), (8, 3), (17, 30), (48, 5), (64, 64), (65, 7), (100, 3), (128, 40),
                                  (129, 2), (200, 17), (256, 33), (256, 1), (300, 9), (384, 12), (385, 4),
-                                 (512, 6)])
+                                 (512, 6), (1100, 3), (2048, 2)])
 def test_chain_vs_numpy(n, m):
     us = _unitaries(n, m, seed=n + m)
     rng = np.random.default_rng(n)
