@@ -360,8 +360,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     // bulk prefetch per row), under the scalars and the rotation
     if (a.pf_rescan)
       for (int k = tid; k < nr; k += kCoopThreads) {
-        const Cand st = s_row[k];
-        const int bc = (st.q > 0.0) ? (int)(st.cr >> 16) : -1;
+        const int bc = (int)(s_row[k].cr >> 16);  // (no candidate: cr = ~0 -> column 0xffff, never i or j)
         const int x = r0 + k;
         if ((bc == i || bc == j) && x != i && x != j && x > 0)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(h + (size_t)x * n),
