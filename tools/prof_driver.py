@@ -1,6 +1,6 @@
 """Run ONE instance of a hot-path workload (after a warm-up) so ncu can
 capture its kernels:  python tools/prof_driver.py <case> [arg]
-cases: npad60 | npad4096 [max_iter] | sweep [points] | magnus2 [intervals] | magnus4096 | zgemm4096 | herm4096
+cases: npad60 | npad4096 [max_iter] | sweep [points] | magnus2 [intervals] | magnus4096 | zgemm4096 | herm4096 | herm256
 """
 import sys
 from pathlib import Path
@@ -97,6 +97,16 @@ def main():
                          lib.stream_ptr())
             else:
                 lib.call("qch_zgemm_herm_batched", lib.dptr(h), lib.dptr(h), lib.dptr(c), n, 1, lib.stream_ptr())
+        print(case, "done")
+    elif case == "herm256":  # the mid-size line's Hermitian products: 2048 x (256 x 256) on DMMA
+        from paper_2411_09982_b200 import _lib as lib
+
+        n, b = 256, 2048
+        a = torch.randn(b, n, n, dtype=torch.complex128, device="cuda")
+        h = (a + a.mH) * 0.5
+        c = torch.empty_like(a)
+        for _ in range(2):
+            lib.call("qch_zgemm_herm_batched", lib.dptr(h), lib.dptr(h), lib.dptr(c), n, b, lib.stream_ptr())
         print(case, "done")
     elif case == "oz4096":
         from paper_2411_09982_b200 import _lib as lib
