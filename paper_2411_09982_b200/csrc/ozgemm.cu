@@ -537,31 +537,30 @@ struct OzSliceOut {
 // pass 1: the row exponents e (frexp of the row max of each component)
 __global__ void __launch_bounds__(256) oz_rowexp_kernel(const double2* __restrict__ x, int rows, int cols,
                                                         int64_t xstride, OzSliceOut o) {
-  const int r = blockIdx.x;
+  // one WARP per row (8 rows per block): no block barrier, 8 row loads in
+  // flight per lane
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
   const int64_t b = blockIdx.y;
   const double2* xr = x + b * xstride + (int64_t)r * cols;
   double m[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+#pragma unroll 8
+  for (int c = lane; c < cols; c += 32) {
     const double2 v = xr[c];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       if (q < o.nc) m[q] = fmax(m[q], fabs(oz_comp(v, o.comp[q])));
   }
-  __shared__ double s_m[4][8];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
+    if (q >= o.nc) break;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m[q] = fmax(m[q], __shfl_xor_sync(0xffffffffu, m[q], off));
-    if ((threadIdx.x & 31) == 0) s_m[q][threadIdx.x >> 5] = m[q];
-  }
-  __syncthreads();
-  if (threadIdx.x < 4 && (int)threadIdx.x < o.nc) {
-    const int q = threadIdx.x;
-    double mx = s_m[q][0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, s_m[q][w]);
-    int e = 0;
-    if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1): |x| < 2^e
-    o.ex[q][b * rows + r] = e;
+    if (lane == q) {
+      int e = 0;
+      if (m[q] > 0.0) frexp(m[q], &e);  // m = f 2^e, f in [0.5, 1): |x| < 2^e
+      o.ex[q][b * rows + r] = e;
+    }
   }
 }
 
@@ -645,7 +644,7 @@ static int oz_slicev(const double2* x, int rows, int cols, int64_t batch, int64_
     }
     void* pr = prof_begin("oz_slice", st);
     const double2* xb = x + b0 * xstride;
-    oz_rowexp_kernel<<<dim3(rows, (unsigned)nb), 256, 0, st>>>(xb, rows, cols, xstride, ob);
+    oz_rowexp_kernel<<<dim3((rows + 7) / 8, (unsigned)nb), 256, 0, st>>>(xb, rows, cols, xstride, ob);
     const int64_t groups = nb * rows * (int64_t)(ld / 8);
     const int blocks = (int)std::min<int64_t>((groups + 255) / 256, (int64_t)sm_count() * 64);
     switch (s) {
