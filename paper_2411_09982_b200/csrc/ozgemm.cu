@@ -574,11 +574,37 @@ __device__ __forceinline__ unsigned long long oz_fixed(double y, int e) {
   return t >= 0 ? (m << t) : (t > -64 ? (m >> -t) : 0ull);
 }
 
+// the same |A| = floor(|y| 2^(7S - e)) as its two 28-bit halves, on the FP64
+// pipe instead of 64-bit integer shifts: u = |y| 2^(7S-28-e) < 2^28 (exact:
+// a power-of-two scaling), hi = floor(u) and lo = floor((u - hi) 2^28), each
+// floor read from the low word of x + 2^52 added with round-toward-zero
+// (exact: u - hi by Sterbenz, the products by powers of two; a result below
+// the normal range only where the digit is 0 anyway).  Valid while the scale
+// 2^(7S-28-e) is a normal double: 7S - 1051 <= e <= 7S + 994 (oz_cut_fp_ok).
+template <int S>
+__device__ __forceinline__ bool oz_cut_fp_ok(int e) {
+  return e >= 7 * S - 1051 && e <= 7 * S + 994;
+}
+template <int S>
+__device__ __forceinline__ void oz_halves(double y, int e, bool fp, unsigned& hi, unsigned& lo) {
+  if (fp) {
+    constexpr double k52 = 4503599627370496.0;  // 2^52
+    const double u = fabs(y) * __longlong_as_double((long long)(7 * S - 28 - e + 1023) << 52);
+    const double hb = __dadd_rz(u, k52);
+    hi = (unsigned)__double2loint(hb);
+    lo = (unsigned)__double2loint(__dadd_rz((u - (hb - k52)) * 268435456.0, k52));
+  } else {
+    const unsigned long long mg = oz_fixed<S>(y, e);
+    hi = (unsigned)(mg >> 28);
+    lo = (unsigned)mg & 0x0FFFFFFFu;
+  }
+}
+
 // pass 2: every (item, row, 8 columns) independently — 8 consecutive columns
 // per thread, 8 bytes per slice plane
 template <int S>
 __global__ void __launch_bounds__(256) oz_cut_kernel(const double2* __restrict__ x, int rows, int cols,
-                                                     int64_t xstride, OzSliceOut o, int64_t groups) {
+                                                     int64_t xstride, OzSliceOut o, int64_t groups, int fpcut) {
   const int ld = oz_ld(cols);  // slice row stride: padding columns are written as zeros
   const int gpr = ld >> 3;
   const int64_t plane = (int64_t)rows * ld;
@@ -602,14 +628,13 @@ __global__ void __launch_bounds__(256) oz_cut_kernel(const double2* __restrict__
     for (int q = 0; q < 4; ++q) {
       if (q >= o.nc) break;
       const int e = o.ex[q][br];
+      const bool fp = fpcut && oz_cut_fp_ok<S>(e);
       // |A| = hi 2^28 + lo (28-bit halves); digit i = bits [7(S-1-i), +7)
       unsigned hi[8], lo[8], nm0 = 0, nm1 = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const double y = oz_comp(v[j], o.comp[q]);
-        const unsigned long long mg = oz_fixed<S>(y, e);
-        hi[j] = (unsigned)(mg >> 28);
-        lo[j] = (unsigned)mg & 0x0FFFFFFFu;
+        oz_halves<S>(y, e, fp, hi[j], lo[j]);
         if (y < 0.0) {
           if (j < 4) nm0 |= 0xFFu << (8 * j);
           else nm1 |= 0xFFu << (8 * (j - 4));
@@ -646,10 +671,11 @@ static int oz_slicev(const double2* x, int rows, int cols, int64_t batch, int64_
     const double2* xb = x + b0 * xstride;
     oz_rowexp_kernel<<<dim3((rows + 7) / 8, (unsigned)nb), 256, 0, st>>>(xb, rows, cols, xstride, ob);
     const int64_t groups = nb * rows * (int64_t)(ld / 8);
+    static const int fpcut = getenv("QCH_OZ_FPCUT") ? atoi(getenv("QCH_OZ_FPCUT")) : 1;
     const int blocks = (int)std::min<int64_t>((groups + 255) / 256, (int64_t)sm_count() * 64);
     switch (s) {
 #define OZ_SL(k) \
-  case k: oz_cut_kernel<k><<<blocks, 256, 0, st>>>(xb, rows, cols, xstride, ob, groups); break;
+  case k: oz_cut_kernel<k><<<blocks, 256, 0, st>>>(xb, rows, cols, xstride, ob, groups, fpcut); break;
       OZ_SL(1) OZ_SL(2) OZ_SL(3) OZ_SL(4) OZ_SL(5) OZ_SL(6) OZ_SL(7) OZ_SL(8)
 #undef OZ_SL
       default: return fail(QCH_ERR_VALUE, "ozaki: 1..8 slices");
