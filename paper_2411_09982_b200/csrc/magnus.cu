@@ -671,16 +671,40 @@ struct DevBuf {
 
 
 // H bitwise Hermitian?  flag[b] |= 1 for any H[r][c] != conj(H[c][r]) (r > c)
-__global__ void herm_check_kernel(const double2* __restrict__ h, int n, int64_t batch, unsigned* __restrict__ flag) {
-  const int64_t nn = (int64_t)n * n;
-  const int64_t total = nn * batch;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = k / nn, e = k - b * nn;
-    const int r = (int)(e / n), c = (int)(e - (int64_t)r * n);
-    if (r <= c) continue;
-    const double2 x = h[k], y = h[b * nn + (int64_t)c * n + r];
-    if (!(x.x == y.x && x.y == -y.y)) flag[b] = 1u;
+// bitwise Hermiticity per batch item: one 32 x 32 tile of the lower
+// triangle and its mirror tile per block, both read row-wise (coalesced)
+// into shared memory, so every entry is read once
+__global__ void __launch_bounds__(256) herm_check_kernel(const double2* __restrict__ h, int n, int64_t batch,
+                                                         unsigned* __restrict__ flag) {
+  __shared__ double2 ta[32][33], tb[32][33];
+  const int t = blockIdx.x;
+  int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  while (I * (I + 1) / 2 > t) --I;
+  const int J = t - I * (I + 1) / 2;  // lower tile (I, J), J <= I
+  const int64_t b = blockIdx.y;
+  const double2* hb = h + b * (int64_t)n * n;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int rl = ty + 8 * k;
+    const int ra = I * 32 + rl, ca = J * 32 + tx;  // tile (I, J)
+    const int rb = J * 32 + rl, cb = I * 32 + tx;  // mirror tile (J, I)
+    ta[rl][tx] = (ra < n && ca < n) ? hb[(int64_t)ra * n + ca] : make_double2(0.0, 0.0);
+    tb[rl][tx] = (rb < n && cb < n) ? hb[(int64_t)rb * n + cb] : make_double2(0.0, 0.0);
   }
+  __syncthreads();
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int rl = ty + 8 * k;
+    const int r = I * 32 + rl, c = J * 32 + tx;
+    if (r < n && c < n && r >= c) {  // the diagonal too: a real diagonal is part of Hermiticity
+      const double2 x = ta[rl][tx], y = tb[tx][rl];  // h[r][c] and h[c][r]
+      if (!(x.x == y.x && x.y == -y.y)) bad = true;
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) flag[b] = 1u;
 }
 
 // hs = H * 2^-s_b
@@ -958,7 +982,12 @@ static int expm_generic(const double2* h, int64_t batch, int n, double2* u, doub
   unsigned* hflag = (unsigned*)(norm + batch);
   QCH_CUDA(cudaMemsetAsync(norm, 0, sizeof(unsigned long long) * 2 * batch, st));
   rownorm_launch(h, n, batch, norm, st);
-  herm_check_kernel<<<grid_for(nn * batch), 256, 0, st>>>(h, n, batch, hflag);
+  {
+    const int tn = (n + 31) / 32;
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535)
+      herm_check_kernel<<<dim3((unsigned)(tn * (tn + 1) / 2), (unsigned)std::min<int64_t>(65535, batch - b0)), 256, 0,
+                          st>>>(h + b0 * nn, n, std::min<int64_t>(65535, batch - b0), hflag + b0);
+  }
   QCH_LAUNCH_CHECK("herm_check_kernel");
   note_launch(2);
   std::vector<unsigned long long> hn(2 * batch);

@@ -338,3 +338,21 @@ def test_zgemm_herm_int8_tensor_path_vs_numpy(E, n):
     assert rel_fro(got, h2 @ h) <= 1e-14
     iu = np.triu_indices(n, 1)
     np.testing.assert_array_equal(got[iu], got.T[iu].conj())
+
+
+@pytest.mark.parametrize("pos", [(5, 5), (70, 3), (99, 98), (40, 64)])
+def test_expm_nearly_hermitian_takes_general_path(E, pos):
+    # Hermitian except ONE entry (an imaginary diagonal entry, or one
+    # off-diagonal entry in a diagonal / off-diagonal / last partial tile):
+    # the Hermitian-only (half-GEMM) path must not be taken
+    from oracle import expm_oracle
+
+    n = 100
+    rng = np.random.default_rng(sum(pos))
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = (a + a.conj().T) * (0.3 / np.sqrt(n))
+    r, c = pos
+    h[r, c] += 0.05j if r == c else 0.05
+    got = E.expm_batch([h], check=False)[0].entries
+    ref = expm_oracle.expm_minus_i(h)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-10
