@@ -670,8 +670,7 @@ struct DevBuf {
 };
 
 
-// H bitwise Hermitian?  flag[b] |= 1 for any H[r][c] != conj(H[c][r]) (r > c)
-// bitwise Hermiticity per batch item: one 32 x 32 tile of the lower
+// bitwise Hermiticity per batch item (flag[b] = 1 for any H[r][c] != conj(H[c][r]), r >= c): one 32 x 32 tile of the lower
 // triangle and its mirror tile per block, both read row-wise (coalesced)
 // into shared memory, so every entry is read once
 __global__ void __launch_bounds__(256) herm_check_kernel(const double2* __restrict__ h, int n, int64_t batch,
