@@ -298,13 +298,17 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       // every warp finds the pivot; the row-i / row-j states are reduced by
       // warps 1 and 2 of their owner CTAs, in parallel with the others
       const bool red_i = own_pi && warp_u == 1, red_j = own_pj && warp_u == 2;  // warp-uniform
-      for (int k = lane; k < G; k += 32) {
-        const Cand ro = rec[k].own, rpi = rec[k].pi, rpj = rec[k].pj;
+      // G <= 16 records: lanes 0..15 fold own + pi of record `lane`, lanes
+      // 16..31 pj of record `lane - 16` (two dependent folds per lane, not three)
+      if (lane < G) {
+        const Cand ro = rec[lane].own, rpi = rec[lane].pi;
         cand_take(piv, ro);
         cand_take(piv, rpi);
+        if (red_i) cpi = rpi;
+      } else if (lane >= 16 && lane - 16 < G) {
+        const Cand rpj = rec[lane - 16].pj;
         cand_take(piv, rpj);
-        if (red_i) cand_take(cpi, rpi);
-        if (red_j) cand_take(cpj, rpj);
+        if (red_j) cpj = rpj;
       }
       piv = warp_best(piv);
       if (red_i) {
