@@ -138,39 +138,38 @@ __device__ __forceinline__ Cand warp_best(Cand c) {
   return (wl >= 0) ? shfl_cand_p(c, wl) : cand_none();
 }
 
-// three independent warp argmaxes with their REDUX / ballot steps
-// interleaved (the same winners as three warp_best calls; the rare near-tie
-// path stays exact)
-__device__ __forceinline__ void warp_best3(Cand& c1, Cand& c2, Cand& c3) {
-  Cand* cs[3] = {&c1, &c2, &c3};
-  unsigned long long bb[3];
-  unsigned hh[3], hm[3], lm[3], nb[3];
-  bool nf[3];
+// T independent warp argmaxes with their REDUX / ballot steps interleaved
+// (the same winners as T warp_best calls; the rare near-tie path stays exact)
+template <int T>
+__device__ __forceinline__ void warp_best_n(Cand* const (&cs)[T]) {
+  unsigned long long bb[T];
+  unsigned hh[T], hm[T], lm[T], nb[T];
+  bool nf[T];
 #pragma unroll
-  for (int t = 0; t < 3; ++t) {
+  for (int t = 0; t < T; ++t) {
     bb[t] = (cs[t]->q > 0.0) ? (unsigned long long)__double_as_longlong(cs[t]->q) : 0ull;
     hh[t] = (unsigned)(bb[t] >> 32);
   }
 #pragma unroll
-  for (int t = 0; t < 3; ++t) hm[t] = __reduce_max_sync(kFull, hh[t]);
+  for (int t = 0; t < T; ++t) hm[t] = __reduce_max_sync(kFull, hh[t]);
 #pragma unroll
-  for (int t = 0; t < 3; ++t) lm[t] = __reduce_max_sync(kFull, (hh[t] == hm[t]) ? (unsigned)bb[t] : 0u);
+  for (int t = 0; t < T; ++t) lm[t] = __reduce_max_sync(kFull, (hh[t] == hm[t]) ? (unsigned)bb[t] : 0u);
 #pragma unroll
-  for (int t = 0; t < 3; ++t) {
+  for (int t = 0; t < T; ++t) {
     const double qs = __longlong_as_double((long long)(((unsigned long long)hm[t] << 32) | lm[t]));
     nf[t] = (cs[t]->q > 0.0) && (cs[t]->q >= qs * (1.0 - kRel));
   }
 #pragma unroll
-  for (int t = 0; t < 3; ++t) nb[t] = __ballot_sync(kFull, nf[t]);
-  int w[3];
+  for (int t = 0; t < T; ++t) nb[t] = __ballot_sync(kFull, nf[t]);
+  int w[T];
 #pragma unroll
-  for (int t = 0; t < 3; ++t) {
+  for (int t = 0; t < T; ++t) {
     w[t] = -1;
     if (hm[t] != 0u)
       w[t] = (__popc(nb[t]) == 1) ? __ffs(nb[t]) - 1 : warp_argmax_exact(cs[t]->v, cs[t]->m, cs[t]->cr, nf[t]);
   }
 #pragma unroll
-  for (int t = 0; t < 3; ++t) {
+  for (int t = 0; t < T; ++t) {
     const Cand o = shfl_cand_p(*cs[t], w[t] >= 0 ? w[t] : 0);
     *cs[t] = w[t] >= 0 ? o : cand_none();
   }
@@ -548,7 +547,10 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
       // per-warp bests, then warps 0, 1, 2 reduce own / pi / pj in parallel
       // and each writes its field of the record into every CTA
       Cand wa = own, wb = ppi, wc = ppj;
-      warp_best3(wa, wb, wc);
+      {
+        Cand* const cs3[3] = {&wa, &wb, &wc};
+        warp_best_n<3>(cs3);
+      }
       if (lane == 0) {
         s_part[warp_u] = wa;
         s_part[kCoopWarps + warp_u] = wb;
