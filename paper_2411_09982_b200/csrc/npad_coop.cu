@@ -215,7 +215,7 @@ constexpr int kClusterMax = 16;
 // s_rec) and the per-rotation barrier is barrier.cluster (release/acquire at
 // cluster scope, which also orders the CTAs' global matrix writes) instead of
 // polling epoch-flagged records in global memory.
-template <bool EK, bool CL>
+template <bool EK, bool CL, bool ST>  // ST: per-phase cycle counters (QCH_NPAD_STATS)
 __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid_constant__ CoopArgs a) {
   namespace cg = cooperative_groups;
   __shared__ CoopRec s_rec[CL ? 2 : 1][CL ? kClusterMax : 1];
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
   long long cyc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long ck = clock64();
   auto tick = [&](int k) {
-    if (a.stats != nullptr) {
+    if (ST) {
       const long long c2 = clock64();
       cyc[k] += c2 - ck;
       ck = c2;
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) npad_coop_kernel(const __grid
     tick(5);
   }
   if (mbx) cg::this_cluster().sync();  // no CTA leaves while a peer may still address it
-  if (a.stats != nullptr && tid == 0)
+  if (ST && tid == 0)
     for (int k = 0; k < 8; ++k) a.stats[8 * g + k] = cyc[k];
   if (g == 0 && tid == 0) {
     *a.out_applied = applied;
@@ -641,8 +641,15 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
   // one cluster of G <= 16 CTAs when the device can place it (QCH_NPAD_COOP_CLUSTER=0 disables)
   const char* ce = getenv("QCH_NPAD_COOP_CLUSTER");
   bool cl = (ce == nullptr || atoi(ce) != 0) && G <= kClusterMax;
-  auto kern = ek ? (cl ? npad_coop_kernel<true, true> : npad_coop_kernel<true, false>)
-                 : (cl ? npad_coop_kernel<false, true> : npad_coop_kernel<false, false>);
+  const bool stats_on = getenv("QCH_NPAD_STATS") != nullptr;
+  auto pick = [&](bool cluster) {
+    if (stats_on)
+      return ek ? (cluster ? npad_coop_kernel<true, true, true> : npad_coop_kernel<true, false, true>)
+                : (cluster ? npad_coop_kernel<false, true, true> : npad_coop_kernel<false, false, true>);
+    return ek ? (cluster ? npad_coop_kernel<true, true, false> : npad_coop_kernel<true, false, false>)
+              : (cluster ? npad_coop_kernel<false, true, false> : npad_coop_kernel<false, false, false>);
+  };
+  auto kern = pick(cl);
   QCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (cl) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
@@ -667,7 +674,7 @@ int npad_run_coop(double2* h, int n, double threshold, long long max_iter, int e
       }
     }
     if (!cl) {
-      kern = ek ? npad_coop_kernel<true, false> : npad_coop_kernel<false, false>;
+      kern = pick(false);
       QCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
   }
