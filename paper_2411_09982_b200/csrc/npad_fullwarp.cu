@@ -83,7 +83,7 @@ __device__ __forceinline__ void warp_best2(Cand& c1, Cand& c2) {
 }
 
 // EK: exact-magnitude keys (compile-time, so make_cand carries no branch)
-template <bool EK>
+template <bool EK, bool ST>  // ST: per-phase cycle counters (QCH_NPAD_STATS), compiled out otherwise
 __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict__ jobs, NpadCommon2 cm) {
   extern __shared__ __align__(16) double2 hs[];  // n rows x kPitch
   NpadJob2* job = jobs + blockIdx.x;
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       break;
     }
     long long c1 = 0;
-    if (cm.stats) {
+    if (ST) {
       c1 = clock64();
       cyc[0] += c1 - c0;
     }
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       job->pivots[2 * applied + 1] = j;
     }
     long long c2 = 0;
-    if (cm.stats) {
+    if (ST) {
       c2 = clock64();
       cyc[1] += c2 - c1;
     }
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       cand_take(pj, make_cand(c2d(blk.ji), ((unsigned)i << 16) | (unsigned)j, ek));
     }
     long long c3 = 0;
-    if (cm.stats) {
+    if (ST) {
       c3 = clock64();
       cyc[2] += c3 - c2;
     }
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
     // rows whose argmax column was i or j: whole-warp rescans
     unsigned m0 = __ballot_sync(kFull, resc[0]), m1 = __ballot_sync(kFull, resc[1]);
     long long c4 = 0;
-    if (cm.stats) {
+    if (ST) {
       c4 = clock64();
       cyc[3] += c4 - c3;
       nresc += __popc(m0) + __popc(m1);
@@ -256,12 +256,12 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
       }
     }
     ++applied;
-    if (cm.stats) {
+    if (ST) {
       c0 = clock64();
       cyc[4] += c0 - c4;
     }
   }
-  if (cm.stats && lane == 0) {
+  if (ST && lane == 0) {
     const double a = applied > 0 ? (double)applied : 1.0;
     printf("npad full-warp n=%d: %lld rotations, cycles/rotation select %.0f scalars %.0f rotate %.0f rows-ij %.0f "
            "rescans %.0f (%.2f rows)\n",
@@ -297,13 +297,11 @@ bool npad_full_warp_ok(const NpadCommon2& cm, bool herm, bool trows) {
 
 int npad_launch_full_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (size_t)cm.n * kPitch;
-  QCH_CUDA(smem_attr((const void*)npad_full_warp_kernel<false>, (int)(sizeof(double2) * kMaxN * kPitch)));
-  QCH_CUDA(smem_attr((const void*)npad_full_warp_kernel<true>, (int)(sizeof(double2) * kMaxN * kPitch)));
+  auto kern = cm.stats ? (cm.ek ? npad_full_warp_kernel<true, true> : npad_full_warp_kernel<false, true>)
+                       : (cm.ek ? npad_full_warp_kernel<true, false> : npad_full_warp_kernel<false, false>);
+  QCH_CUDA(smem_attr((const void*)kern, (int)(sizeof(double2) * kMaxN * kPitch)));
   void* pr = prof_begin("npad_run_kernel", st);
-  if (cm.ek)
-    npad_full_warp_kernel<true><<<njobs, 32, smem, st>>>(jobs, cm);
-  else
-    npad_full_warp_kernel<false><<<njobs, 32, smem, st>>>(jobs, cm);
+  kern<<<njobs, 32, smem, st>>>(jobs, cm);
   prof_end(pr, st);
   QCH_LAUNCH_CHECK("npad_full_warp_kernel");
   note_launch(1);
