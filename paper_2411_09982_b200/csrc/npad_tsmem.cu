@@ -106,7 +106,7 @@ __device__ __forceinline__ Cand block_best_s(Cand c, Cand* s_part, int lane, int
   return b;
 }
 
-template <bool EK>
+template <bool EK, bool ST>  // ST: per-phase cycle counters (QCH_NPAD_STATS), compiled out otherwise
 __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __restrict__ jobs, NpadCommon2 cm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = cm.n, nT = cm.n_target;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
 
   long long cyc[5] = {0, 0, 0, 0, 0};  // QCH_NPAD_STATS: select, row u + rotate, block best, fold, rescans
   while (true) {
-    const long long c0 = cm.stats ? clock64() : 0;
+    const long long c0 = ST ? clock64() : 0;
     // ---- selection (every warp, identical result)
     const int pl = warp_argmax(mine);
     Cand piv = cand_none();
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
       pivots[2 * applied] = i;
       pivots[2 * applied + 1] = j;
     }
-    const long long c1 = cm.stats ? clock64() : 0;
+    const long long c1 = ST ? clock64() : 0;
     // ---- the partner row u: the ONE global round trip (all loads in flight)
     constexpr int kMaxCpt = 8;  // n <= 2048
     double2 ru[kMaxCpt];
@@ -241,9 +241,9 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
     // H[j, i] is a candidate of T-row t
     const Block2 blk = rotate_block(c, s, mkc(hii, 0.0), cconj(v), v, mkc(hjj, 0.0));
     if (tid == 0) cand_take(pt, make_cand(c2d(blk.ji), ((unsigned)i << 16) | (unsigned)j, ek));
-    const long long c2 = cm.stats ? clock64() : 0;
+    const long long c2 = ST ? clock64() : 0;
     const Cand bt = block_best_s(pt, s_part, lane, warp);  // barrier: rows and folds visible
-    const long long c3 = cm.stats ? clock64() : 0;
+    const long long c3 = ST ? clock64() : 0;
     ++clock;
     if (tid == 0) {
       const double2 bii = c2d(blk.ii), bij = c2d(blk.ij), bji = c2d(blk.ji), bjj = c2d(blk.jj);
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
     }
     unsigned rm = __ballot_sync(kFull, need);
     __syncthreads();  // 2x2 block, diagonal and clocks visible; s_part reusable
-    const long long c4 = cm.stats ? clock64() : 0;
+    const long long c4 = ST ? clock64() : 0;
     // ---- rescans of T-rows: shared memory only
     while (rm) {
       const int kr = __ffs(rm) - 1;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
       if (lane == kr) mine = br;
       __syncthreads();  // s_part reuse
     }
-    if (cm.stats) {
+    if (ST) {
       const long long c5 = clock64();
       cyc[0] += c1 - c0;
       cyc[1] += c2 - c1;
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
     }
     ++applied;
   }
-  if (cm.stats && tid == 0 && applied > 0)
+  if (ST && tid == 0 && applied > 0)
     printf("npad tsmem driver: chain %d: %lld rotations, %.2f rescans/rot, cycles/rot: select %.0f, row u + rotate "
            "%.0f, block best %.0f, fold %.0f, rescans %.0f\n",
            blockIdx.x, applied, (double)rescans / applied, (double)cyc[0] / applied, (double)cyc[1] / applied,
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kTsThreads, 1) npad_tsmem_kernel(NpadJob2* __r
   if (tid == 0) {
     job->applied = applied;
     job->status = status;
-    if (cm.stats) job->stats[0] += rescans;
+    if (ST) job->stats[0] += rescans;
   }
 }
 
@@ -361,7 +361,8 @@ size_t npad_tsmem_bytes(const NpadCommon2& cm) {
 int npad_launch_tsmem(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cudaStream_t st) {
   const size_t smem = npad_tsmem_bytes(cm);
   if (smem == 0) return fail(QCH_ERR_UNSUPPORTED, "npad: shared-memory T-rows driver does not fit");
-  auto kern = cm.ek ? npad_tsmem_kernel<true> : npad_tsmem_kernel<false>;
+  auto kern = cm.stats ? (cm.ek ? npad_tsmem_kernel<true, true> : npad_tsmem_kernel<false, true>)
+                       : (cm.ek ? npad_tsmem_kernel<true, false> : npad_tsmem_kernel<false, false>);
   QCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* pr = prof_begin("npad_run_kernel", st);
   kern<<<njobs, kTsThreads, smem, st>>>(jobs, cm);

@@ -239,7 +239,7 @@ __device__ __forceinline__ void touch(Touch& tc, int r, int w, int lane) {
 
 // EK: exact keys (q := numpy |z|) for matrices whose entries could leave the
 // normal range of |z|^2 (npad.cu:exact_keys) — the generic candidate path.
-template <bool EK, bool FULL>
+template <bool EK, bool FULL, bool ST>  // ST: per-phase cycle counters (QCH_NPAD_STATS), compiled out otherwise
 __global__ void __launch_bounds__(256, 1) npad_trows_warp_kernel(NpadJob2* __restrict__ jobs, int njobs,
                                                               NpadCommon2 cm) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(256, 1) npad_trows_warp_kernel(NpadJob2* __res
 
   long long cyc_sel = 0, cyc_stage = 0, cyc_post = 0;
   while (true) {
-    const long long c0 = cm.stats ? clock64() : 0;
+    const long long c0 = ST ? clock64() : 0;
     // ---- selection over the |T| T-row candidates
     Cand sel = mine;
     const int pl = warp_argmax(sel);
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(256, 1) npad_trows_warp_kernel(NpadJob2* __res
     // matrix is then fully consistent and nothing is stale)
     if (tc.count + 2 > kTouchCap) flush_columns(tc, h, n, lane);
 
-    const long long c1 = cm.stats ? clock64() : 0;
+    const long long c1 = ST ? clock64() : 0;
     // ---- stale lists + their async gathers and the two diagonal entries
     // (rows own their diagonal: never stale) ride in the first commit group
     // with ring stage 0; the ring streams rows i, j
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(256, 1) npad_trows_warp_kernel(NpadJob2* __res
       __syncwarp();  // ring slot reuse
     }
     cpa_wait<0>();
-    const long long c2 = cm.stats ? clock64() : 0;
+    const long long c2 = ST ? clock64() : 0;
     __syncwarp();  // provisional writes of columns i, j before the 2x2 block
     if (!EK && lbt.x >= 0) pt = tcand(lbt.v, t, lbt.x, ek);
     // the 2x2 block (npad.py:136-144 incl. the Hermitian pin) and its
@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(256, 1) npad_trows_warp_kernel(NpadJob2* __res
       const Cand best = (wl >= 0) ? shfl_cand(pr, wl) : cand_none();
       if (lane == kr) mine = best;
     }
-    if (cm.stats) {
+    if (ST) {
       const long long c3 = clock64();
       cyc_sel += c1 - c0;
       cyc_stage += c2 - c1;
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(256, 1) npad_trows_warp_kernel(NpadJob2* __res
     job->applied = applied;
     job->status = status;
     if (cm.live != nullptr && status != 2) atomicSub(cm.live, 1);
-    if (cm.stats) {
+    if (ST) {
       job->stats[0] += rescans;
       job->stats[1] += cyc_sel;
       job->stats[2] += cyc_stage;
@@ -560,8 +560,12 @@ int npad_launch_trows_warp(NpadJob2* jobs, int njobs, const NpadCommon2& cm, cud
   const size_t smem = trows_warp_smem(cm.n, wpb);
   if (smem > (size_t)max_smem_optin()) return fail(QCH_ERR_UNSUPPORTED, "npad: warp T-rows driver shared memory");
   const bool full = cm.n % kStageCols == 0 && cm.n <= 1024;
-  auto kern = cm.ek ? (full ? npad_trows_warp_kernel<true, true> : npad_trows_warp_kernel<true, false>)
-                    : (full ? npad_trows_warp_kernel<false, true> : npad_trows_warp_kernel<false, false>);
+  auto kern = cm.stats
+                  ? (cm.ek ? (full ? npad_trows_warp_kernel<true, true, true> : npad_trows_warp_kernel<true, false, true>)
+                           : (full ? npad_trows_warp_kernel<false, true, true> : npad_trows_warp_kernel<false, false, true>))
+                  : (cm.ek ? (full ? npad_trows_warp_kernel<true, true, false> : npad_trows_warp_kernel<true, false, false>)
+                           : (full ? npad_trows_warp_kernel<false, true, false>
+                                   : npad_trows_warp_kernel<false, false, false>));
   QCH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = (njobs + wpb - 1) / wpb;
   void* pr = prof_begin("npad_run_kernel", st);
