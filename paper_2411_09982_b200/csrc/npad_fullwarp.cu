@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
 
   long long applied = job->applied;
   const double thr = job->threshold;
+  int* const piv_log = job->pivots;  // loaded once (the stores through it could alias the job record)
+  const long long piv_cap = job->pivot_cap;
   int status = 0;
   long long cyc[5] = {0, 0, 0, 0, 0}, nresc = 0;  // select, scalars, rotate, rows i/j, rescans
   long long c0 = clock64();
@@ -148,9 +150,9 @@ __global__ void __launch_bounds__(32) npad_full_warp_kernel(NpadJob2* __restrict
     cplx s;
     givens_fast(v, hii, hjj, &c, &s);
     const Block2 blk = rotate_block(c, s, mkc(hii, 0.0), cconj(v), v, mkc(hjj, 0.0));
-    if (lane == 0 && job->pivots != nullptr && applied < job->pivot_cap) {
-      job->pivots[2 * applied] = i;
-      job->pivots[2 * applied + 1] = j;
+    if (lane == 0 && piv_log != nullptr && applied < piv_cap) {
+      piv_log[2 * applied] = i;
+      piv_log[2 * applied + 1] = j;
     }
     long long c2 = 0;
     if (ST) {
