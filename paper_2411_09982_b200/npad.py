@@ -445,7 +445,10 @@ class BatchResult:
         return HermitianOperator._from_device(mats[k])
 
     def diagonals(self) -> np.ndarray:
-        return np.concatenate([_lib.to_host(m.diagonal(dim1=1, dim2=2).real.contiguous()) for _, m in self.parts])
+        # one part (one device): the page-locked array to_host filled is the
+        # result — concatenating would copy it into fresh pageable pages
+        arrs = [_lib.to_host(m.diagonal(dim1=1, dim2=2).real.contiguous()) for _, m in self.parts]
+        return arrs[0] if len(arrs) == 1 else np.concatenate(arrs)
 
 
 def max_abs_batch(mats):
